@@ -1,0 +1,258 @@
+/* ecoserve.h -- C ABI of the B200-native PaDG instance hot path.
+ *
+ * EcoServe (arXiv 2504.18154) runs every serving instance in temporally
+ * disaggregated phases (Sec. 3.2.1): a prefill-only phase
+ * over a batch of new requests, and a decode-only phase over the running set,
+ * switched by the instance scheduler under the macro
+ * instance's routing (Alg. 1/2). This header exposes those two
+ * phases as calls on an instance object, plus the host-side macro scheduler.
+ * The computation inside a phase is the Llama-family decoder of Eq. 1-3
+ * with the readings listed in DESIGN.md section 3.
+ *
+ * Conventions
+ *  - Every function returns ecoserve_status; nothing throws across the ABI.
+ *  - Pointers documented "device" are CUDA device pointers on the instance's
+ *    device; "host" are CPU pointers. Sizes are element counts unless noted.
+ *  - Borrowed memory (weights, prepared buffer, KV pool, stream) is allocated by
+ *    the caller and must outlive the instance. The library owns its host state
+ *    (allocator, block tables, request table) and its device workspace.
+ *  - CUDA errors are sticky: the instance reports dead in its status and every
+ *    later call returns ECOSERVE_ERR_CUDA. ecoserve_last_error() explains.
+ *  - An instance is single-threaded (one worker thread per GPU); a macro object
+ *    is single-threaded (the dispatcher thread).
+ */
+#ifndef ECOSERVE_H_
+#define ECOSERVE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ECOSERVE_OK = 0,
+  ECOSERVE_ERR_INVALID_ARG = 1, /* bad pointer/size/shape; nothing changed */
+  ECOSERVE_ERR_KV_EXHAUSTED = 2, /* not enough free KV blocks; all-or-nothing: nothing allocated */
+  ECOSERVE_ERR_STATE = 3,        /* unknown or duplicate req_id, decode before prefill, dead instance */
+  ECOSERVE_ERR_UNSUPPORTED = 4,  /* shape/feature this build does not implement */
+  ECOSERVE_ERR_CUDA = 5,         /* sticky CUDA error */
+  ECOSERVE_ERR_NCCL = 6
+} ecoserve_status;
+
+/* Model shape, Table 1 notation: L, H, M, D plus the GQA
+ * kv-head count, SwiGLU width F and vocabulary V (reading A1). */
+typedef struct {
+  int32_t n_layers;   /* L */
+  int32_t hidden;     /* H, multiple of 64 */
+  int32_t n_heads;    /* M */
+  int32_t n_kv_heads; /* Mkv, divides M, M/Mkv <= 16 */
+  int32_t head_dim;   /* D in {32, 64, 128} */
+  int32_t ffn_dim;    /* F, multiple of 64 */
+  int32_t vocab;      /* V */
+  float rope_theta;   /* reading A3 */
+  float rms_eps;      /* reading A4 */
+  int32_t tp_size;    /* 1 (TP=2 pairs: ECOSERVE_ERR_UNSUPPORTED in this build) */
+} ecoserve_model_shape;
+
+/* Paged KV pool (PagedAttention). Layout, block-major so a
+ * block migrates as one contiguous copy:
+ *   pool[num_blocks][n_layers][2 (K,V)][n_kv_heads][block_tokens][head_dim] bf16
+ * `pool` is a borrowed device pointer of ecoserve_kv_pool_bytes() bytes; the
+ * instance zero-fills it at creation. block_tokens must be 64. */
+typedef struct {
+  int32_t block_tokens;
+  int64_t num_blocks;
+  void* pool;
+} ecoserve_kv_pool;
+
+/* Raw weights, bf16, matrices [out][in] row-major (device pointers):
+ *   embed [V][H], lm_head [V][H] (untied), final_norm [H];
+ *   layers[l][0..8] = attn_norm [H], wq [M*D][H], wk [Mkv*D][H], wv [Mkv*D][H],
+ *                     wo [H][M*D], ffn_norm [H], w_gate [F][H], w_up [F][H],
+ *                     w_down [H][F].
+ * wq/wk/wv/w_gate/w_up are read only during ecoserve_instance_create (they are
+ * re-laid-out into the prepared buffer); all others are read by every phase. */
+typedef struct {
+  const void* embed;
+  const void* lm_head;
+  const void* final_norm;
+  const void* const* layers; /* host array of n_layers*9 device pointers */
+} ecoserve_weights;
+
+/* Engine configuration (NULL = defaults in brackets). */
+typedef struct {
+  int32_t token_budget;  /* max prompt tokens per prefill batch T [16384] */
+  int32_t max_batch;     /* max decode batch B [512]; also max requests per prefill batch */
+  int32_t max_positions; /* max prompt + output length [16384] */
+  int32_t debug_hidden;  /* keep per-layer residuals of the last phase call [0] */
+} ecoserve_engine_config;
+
+/* One request handed to a prefill phase. The prompt is copied during the call. */
+typedef struct {
+  int64_t req_id;
+  const int32_t* prompt; /* host [prompt_len], token ids in [0, V) */
+  int32_t prompt_len;    /* S >= 1 */
+  int32_t max_new_tokens;/* G >= 1, counts the prefill token (reading A7) */
+} ecoserve_request;
+
+typedef struct {
+  int32_t alive;          /* 0 after a sticky CUDA error */
+  int32_t n_requests;     /* resident (unfinished + finished-not-released) */
+  int64_t blocks_total;
+  int64_t blocks_used;
+} ecoserve_instance_status;
+
+typedef struct {
+  int64_t req_id;
+  int32_t prompt_len;
+  int32_t n_generated;    /* tokens produced so far, incl. the prefill token */
+  int32_t finished;       /* n_generated == max_new_tokens */
+  int32_t n_blocks;
+} ecoserve_req_status;
+
+typedef struct ecoserve_instance ecoserve_instance;
+
+/* Bytes of the KV pool for `num_blocks` blocks (layout above). <0 on bad args. */
+int64_t ecoserve_kv_pool_bytes(const ecoserve_model_shape* shape, int32_t block_tokens, int64_t num_blocks);
+/* Bytes of the caller-allocated prepared-weight buffer (fused, re-laid-out QKV
+ * and gate/up matrices). <0 on bad args. */
+int64_t ecoserve_prepared_weight_bytes(const ecoserve_model_shape* shape);
+
+/* Create an instance on `device`. `prepared` is a caller-allocated device buffer
+ * of ecoserve_prepared_weight_bytes(); `cuda_stream` is a borrowed cudaStream_t
+ * (NULL = the library creates its own). tp_rank must be 0 and nccl_unique_id
+ * NULL in this build. */
+ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, const ecoserve_kv_pool* kv,
+                                         const ecoserve_weights* raw, void* prepared, int32_t device,
+                                         int32_t tp_rank, const void* nccl_unique_id, void* cuda_stream,
+                                         const ecoserve_engine_config* cfg, ecoserve_instance** out);
+
+/* Prefill-only phase: admit n new requests, run their
+ * prompts through the model in batches of <= token_budget tokens, write their
+ * KV into the pool, and return each request's first (greedy) token in
+ * first_tokens (host [n]). All-or-nothing on ECOSERVE_ERR_KV_EXHAUSTED /
+ * INVALID_ARG / STATE (duplicate or resident req_id). Synchronous: returns when
+ * the tokens are on the host. */
+ecoserve_status ecoserve_prefill_phase(ecoserve_instance* inst, const ecoserve_request* reqs, int32_t n,
+                                       int32_t* first_tokens);
+
+/* Decode-only phase (rows a13-a16): `steps` decode iterations over the running
+ * set req_ids[0..n) with continuous batching (a request leaves the batch once it
+ * has max_new_tokens tokens). tokens is host [n][steps]: the token produced for
+ * request i at step s, or -1 when the request had already finished.
+ * n_finished (host, may be NULL) receives the number of requests finished by
+ * the end of the call. A new KV block is allocated at every 64-token boundary;
+ * ECOSERVE_ERR_KV_EXHAUSTED leaves the step that could not allocate undone. */
+ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* req_ids, int32_t n, int32_t steps,
+                                      int32_t* tokens, int32_t* n_finished);
+
+/* Free the KV blocks of the given requests and forget them. */
+ecoserve_status ecoserve_release(ecoserve_instance* inst, const int64_t* req_ids, int32_t n);
+
+/* Instance status plus up to `cap` per-request records (host). */
+ecoserve_status ecoserve_get_status(const ecoserve_instance* inst, ecoserve_instance_status* out,
+                                    ecoserve_req_status* reqs, int32_t cap);
+
+/* Debug (engine_config.debug_hidden = 1): residual stream of `req_id` after
+ * layer `layer` (0 = embedding output, L = after the last layer) from the last
+ * phase call, fp32 host out [rows][H], rows = prompt_len (prefill) or 1
+ * (decode, last step). */
+ecoserve_status ecoserve_debug_hidden(ecoserve_instance* inst, int64_t req_id, int32_t layer, float* out);
+
+void ecoserve_instance_destroy(ecoserve_instance* inst);
+const char* ecoserve_last_error(const ecoserve_instance* inst);
+
+/* ------------------------------------------------------------------------
+ * Host-only macro-instance scheduler (Alg. 1 InterSchedule P:476-497 with the
+ * prose probing of P:556-559 (reading A9), Alg. 2 CheckConstraints P:499-540,
+ * readings A10-A14, A18). All times are int64 nanoseconds.
+ * ------------------------------------------------------------------------ */
+typedef struct ecoserve_macro ecoserve_macro;
+
+typedef struct {
+  int32_t n_instances;
+  int64_t slo_ttft_ns;
+  int64_t slo_tpot_ns;
+  int32_t reserve_tokens;      /* R of reading A14 */
+  int32_t block_tokens;        /* 64 */
+  int32_t probe_printed;       /* 0: cyclic probe (prose, A9); 1: Alg. 1 as printed */
+  /* prefill predictor: either the integer cost model a + (b S + c S^2)/1000
+   * (b, c in ps) when n_table == 0, or piecewise-linear over (table_len, table_ns). */
+  int64_t cost_a_ns, cost_b_ps, cost_c_ps;
+  int32_t n_table;
+  const int64_t* table_len;    /* host [n_table], strictly increasing */
+  const int64_t* table_ns;     /* host [n_table] */
+  const int64_t* total_blocks; /* host [n_instances] */
+} ecoserve_macro_config;
+
+typedef struct {
+  int64_t req_id;
+  int64_t arrival_ns;
+  int32_t prompt_len;
+} ecoserve_route_req;
+
+typedef struct {
+  int64_t req_id;
+  int64_t arrival_ns;
+  int32_t prompt_len;
+  int64_t t_first_ns;   /* -1 until the first token */
+  int32_t n_generated;
+  int32_t finished;
+} ecoserve_sched_req;
+
+typedef struct {
+  int32_t phase;        /* 0 idle, 1 prefill, 2 decode */
+  int64_t t_switch_ns;  /* last phase switch (Alg. 2 t_switch) */
+  int64_t total_blocks;
+  int32_t alive;
+} ecoserve_sched_status;
+
+typedef struct {
+  int64_t req_id;
+  int32_t instance;
+} ecoserve_routed;
+
+ecoserve_status ecoserve_macro_create(const ecoserve_macro_config* cfg, ecoserve_macro** out);
+/* Alg. 1. *inst = chosen instance, or -1 (Deferred: the caller queues it with
+ * ecoserve_macro_defer and retries with ecoserve_macro_drain_deferred).
+ * outcomes (host, may be NULL, cap n_instances) receives the Alg. 2 result of
+ * each probed instance in probe order (0 ok, 1 TTFT, 2 TPOT, 3 KV); *n_probed
+ * (may be NULL) their count. */
+ecoserve_status ecoserve_macro_route(ecoserve_macro* m, const ecoserve_route_req* req, int64_t now_ns, int32_t* inst,
+                                     int32_t* outcomes, int32_t* n_probed);
+/* Alg. 2 alone, against instance `inst` (no state change). *result as above. */
+ecoserve_status ecoserve_macro_check(const ecoserve_macro* m, int32_t inst, const ecoserve_route_req* req,
+                                     int64_t now_ns, int32_t* result);
+ecoserve_status ecoserve_macro_defer(ecoserve_macro* m, const ecoserve_route_req* req);
+/* Status push of instance `inst`: per-request records overwrite the
+ * macro's view by req_id; finished ones are dropped. */
+ecoserve_status ecoserve_macro_update_status(ecoserve_macro* m, int32_t inst, const ecoserve_sched_status* st,
+                                             const ecoserve_sched_req* reqs, int32_t n);
+/* Retry deferred requests FIFO, stopping at the first still-Deferred one. */
+ecoserve_status ecoserve_macro_drain_deferred(ecoserve_macro* m, int64_t now_ns, ecoserve_routed* out, int32_t cap,
+                                              int32_t* n);
+int32_t ecoserve_macro_prev_idx(const ecoserve_macro* m);
+int64_t ecoserve_macro_predict_prefill_ns(const ecoserve_macro* m, int32_t prompt_len);
+void ecoserve_macro_destroy(ecoserve_macro* m);
+
+/* Virtual-clock discrete-event simulation of a macro instance of n identical
+ * instances under the integer cost model (decision-parity mode):
+ * prefill batch = sum of predicted prefill ns; decode step =
+ * d + e*B + (f * sum(context))/1000 ns. Outputs per request (host arrays of n_req):
+ * instance, t_first, t_decode_begin, t_done (-1 if never admitted). */
+typedef struct {
+  int64_t cost_d_ns, cost_e_ns, cost_f_ps;
+  int32_t token_budget;
+} ecoserve_des_config;
+
+ecoserve_status ecoserve_des_run(const ecoserve_macro_config* mcfg, const ecoserve_des_config* dcfg,
+                                 const int64_t* arrival_ns, const int32_t* prompt_len, const int32_t* output_len,
+                                 int32_t n_req, int32_t* inst, int64_t* t_first, int64_t* t_decode_begin,
+                                 int64_t* t_done, int64_t* route_log /* host [cap][3]: (t_ns, req, inst), may be NULL */,
+                                 int32_t route_log_cap, int32_t* n_route_log);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ECOSERVE_H_ */

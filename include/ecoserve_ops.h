@@ -1,0 +1,58 @@
+/* ecoserve_ops.h -- op-level entry points of the same CUDA kernels the phases
+ * run, for kernel-by-kernel parity tests and microbenchmarks. All pointers are
+ * device pointers on the current device; every call is asynchronous on
+ * `stream` (a cudaStream_t, NULL = legacy default stream) and returns
+ * ECOSERVE_ERR_CUDA on a launch error, ECOSERVE_ERR_INVALID_ARG on bad sizes.
+ * Nothing is allocated except where noted (workspace arguments are caller
+ * memory). */
+#ifndef ECOSERVE_OPS_H_
+#define ECOSERVE_OPS_H_
+#include <stdint.h>
+#include "ecoserve.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* D = A B^T on tcgen05 (Table 2 projections). A [m][k], B [n][k] bf16
+ * row-major, k % 64 == 0 is not required (TMA zero-fills). out_mode 0: out f32
+ * [m][n]; 1: out bf16 [m][n]. bn in {64, 128, 256}. */
+ecoserve_status ecoserve_op_gemm(const void* A, const void* B, int32_t m, int32_t n, int32_t k, int32_t out_mode,
+                                 void* out, int32_t bn, void* stream);
+
+/* Decode-shaped ("swap-AB") GEMM: out f32 [n][m] = (W [m][k]) (X [n][k])^T with
+ * weights as the 128-row MMA M side, tokens as N, K split `splits` ways into the
+ * caller's workspace f32 [splits][n][m], then a fixed-order reduction. */
+ecoserve_status ecoserve_op_gemm_swap(const void* W, const void* X, int32_t m, int32_t n, int32_t k, int32_t splits,
+                                      float* workspace, float* out, int32_t bn, void* stream);
+
+/* Greedy LM head (rows a12/a16): tokens[i] = argmax_v (X [n][k] W[v][k]^T), lowest
+ * v on ties, logits never materialised. workspace: f32 [n][ceil(V/128)] and
+ * i32 [n][ceil(V/128)]. */
+ecoserve_status ecoserve_op_lm_argmax(const void* W, const void* X, int32_t V, int32_t n, int32_t k, float* ws_val,
+                                      int32_t* ws_idx, int32_t* tokens, void* stream);
+
+/* out bf16 [n][H] = rmsnorm(x f32 [rows[i] or i][H]) * gamma (A4). */
+ecoserve_status ecoserve_op_rmsnorm(const float* x, const int32_t* rows, const void* gamma, void* out, int32_t n,
+                                    int32_t H, float eps, void* stream);
+
+/* Causal varlen prefill attention over a paged pool laid out as in ecoserve.h
+ * for a single layer (n_layers = 1): q bf16 [T][M][D] (RoPE applied), out bf16
+ * [T][M*D]. block_tables int32 [n_seq][bt_ld] (physical block of each 64-token
+ * logical block). */
+ecoserve_status ecoserve_op_attention_prefill(const void* q, const void* pool, int64_t num_blocks, int32_t n_heads,
+                                              int32_t n_kv, int32_t head_dim, const int32_t* cu_seqlens_host,
+                                              int32_t n_seq, const int32_t* block_tables, int32_t bt_ld, void* out,
+                                              void* stream);
+
+/* Split-K decode attention over the same pool: q bf16 [B][M][D], ctx_lens int32
+ * [B] (device), out bf16 [B][M*D]. n_splits x blocks_per_split must cover the
+ * longest context; workspace f32 [B][M][n_splits][D + 2]. */
+ecoserve_status ecoserve_op_attention_decode(const void* q, const void* pool, int32_t n_heads, int32_t n_kv,
+                                             int32_t head_dim, const int32_t* ctx_lens, int32_t B,
+                                             const int32_t* block_tables, int32_t bt_ld, int32_t n_splits,
+                                             int32_t blocks_per_split, float* workspace, void* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

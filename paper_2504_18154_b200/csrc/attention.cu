@@ -1,0 +1,453 @@
+// Attention over the paged KV pool (Eq. 2; Table 2 rows
+// "Attention QK^T" / "(QK^T)V"; PagedAttention P:824).
+//
+// * Prefill: causal varlen flash attention. One CTA = one
+//   64-query tile of one sequence x one q head; 4 warps x 16 query rows; K/V
+//   streamed one 64-token pool block at a time (cp.async double buffer, XOR
+//   swizzled smem), QK^T and PV on mma.sync m16n8k16 (bf16 -> f32), online
+//   softmax in the exp2 domain; only the diagonal tile is masked.
+// * Decode (a14): split-K over the context. One CTA = (sequence, kv head,
+//   split); the G = M/Mkv q heads sharing the kv head are packed into the 16
+//   MMA rows so every K/V byte read from HBM feeds G heads (GQA). Each of the
+//   4 warps owns 16 of the 64 tokens of every block; per-warp online softmax,
+//   then a fixed-order combine across warps and (if split) across splits.
+//
+// The pool must be zero-initialised at allocation (slots beyond a sequence's
+// length are read and masked; masked V rows must be finite).
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace eco {
+
+// 16-byte chunk index of (row r, chunk c) in a swizzled [rows][D] bf16 tile.
+template <int D>
+__device__ __forceinline__ int swz(int r, int c) {
+  constexpr int CPR = D / 8;
+  if constexpr (CPR >= 8)
+    return r * CPR + (c ^ (r & 7));
+  else
+    return r * CPR + (c ^ ((r >> 1) & 3));
+}
+
+// Load a [64][D] bf16 tile (64 rows contiguous in global) into swizzled smem.
+template <int D, int NT>
+__device__ __forceinline__ void load_tile64(bf16* smem, const bf16* g, int tid) {
+  constexpr int CPR = D / 8;
+  const uint32_t base = smem_u32(smem);
+#pragma unroll
+  for (int i = tid; i < 64 * CPR; i += NT) {
+    const int r = i / CPR, c = i % CPR;
+    cp_async16(base + swz<D>(r, c) * 16, g + (int64_t)r * D + c * 8);
+  }
+}
+
+// ------------------------------------------------------------------ prefill
+template <int D>
+__global__ void __launch_bounds__(128) attn_prefill_kernel(PrefillAttnArgs a) {
+  constexpr int CPR = D / 8;
+  constexpr int NK = D / 16;  // k16 steps over the head dim
+  constexpr int ND = D / 8;   // n8 tiles over the head dim
+  extern __shared__ __align__(128) uint8_t sm[];
+  bf16* sQ = reinterpret_cast<bf16*>(sm);
+  bf16* sK = sQ + 64 * D;  // [2][64][D]
+  bf16* sV = sK + 2 * 64 * D;
+
+  const int tile = blockIdx.x, h = blockIdx.y;
+  const int seq = a.tiles[2 * tile], q_start = a.tiles[2 * tile + 1];
+  const int tok0 = a.cu_seqlens[seq];
+  const int len = a.cu_seqlens[seq + 1] - tok0;
+  const int kvh = h / (a.n_heads / a.n_kv);
+  const int* bt = a.block_tables + (int64_t)seq * a.bt_ld;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+
+  // Q tile (rows past the sequence end are clamped to its last row, results discarded)
+  {
+    const uint32_t base = smem_u32(sQ);
+    for (int i = tid; i < 64 * CPR; i += 128) {
+      const int r = i / CPR, c = i % CPR;
+      const int qrow = min(q_start + r, len - 1);
+      cp_async16(base + swz<D>(r, c) * 16, a.q + ((int64_t)(tok0 + qrow) * a.n_heads + h) * D + c * 8);
+    }
+  }
+  const int n_kv_tiles = (min(q_start + 64, len) + 63) / 64;
+  auto kv_ptr = [&](const bf16* cache, int j) {
+    return cache + (int64_t)bt[j] * a.blk_stride + (int64_t)kvh * 64 * D;
+  };
+  load_tile64<D, 128>(sK, kv_ptr(a.k_cache, 0), tid);
+  load_tile64<D, 128>(sV, kv_ptr(a.v_cache, 0), tid);
+  cp_async_commit();
+
+  uint32_t qf[NK][4];
+  float o[ND][4];
+#pragma unroll
+  for (int i = 0; i < ND; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+  const int g = lane >> 2, t4 = lane & 3;
+  const int qpos0 = q_start + warp * 16 + g;  // rows g and g+8 of this warp
+
+  for (int j = 0; j < n_kv_tiles; ++j) {
+    const int buf = j & 1;
+    if (j + 1 < n_kv_tiles) {
+      load_tile64<D, 128>(sK + (buf ^ 1) * 64 * D, kv_ptr(a.k_cache, j + 1), tid);
+      load_tile64<D, 128>(sV + (buf ^ 1) * 64 * D, kv_ptr(a.v_cache, j + 1), tid);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (j == 0) {
+      const uint32_t qb = smem_u32(sQ);
+#pragma unroll
+      for (int kk = 0; kk < NK; ++kk) {
+        const int r = warp * 16 + (lane & 15);
+        ldmatrix_x4(qb + swz<D>(r, kk * 2 + (lane >> 4)) * 16, qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3]);
+      }
+    }
+    const uint32_t kb = smem_u32(sK + buf * 64 * D), vb = smem_u32(sV + buf * 64 * D);
+    // S = Q K^T : 16 x 64 per warp
+    float s[8][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk) {
+#pragma unroll
+      for (int n = 0; n < 8; n += 2) {
+        uint32_t b0, b1, b2, b3;
+        const int r = n * 8 + (lane & 7) + ((lane >> 4) << 3);
+        ldmatrix_x4(kb + swz<D>(r, kk * 2 + ((lane >> 3) & 1)) * 16, b0, b1, b2, b3);
+        mma_bf16_16816(s[n], qf[kk], b0, b1);
+        mma_bf16_16816(s[n + 1], qf[kk], b2, b3);
+      }
+    }
+    // scale, causal mask on the diagonal tile, online softmax (log2 domain)
+    const bool diag = (j * 64 + 63 > q_start);
+    float mnew[2] = {mrow[0], mrow[1]};
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float v = s[n][e] * a.scale_log2;
+        if (diag) {
+          const int kpos = j * 64 + n * 8 + 2 * t4 + (e & 1);
+          const int qpos = qpos0 + (e >> 1) * 8;
+          if (kpos > qpos) v = -INFINITY;
+        }
+        s[n][e] = v;
+        mnew[e >> 1] = fmaxf(mnew[e >> 1], v);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mnew[r] = fmaxf(mnew[r], __shfl_xor_sync(0xffffffffu, mnew[r], 1));
+      mnew[r] = fmaxf(mnew[r], __shfl_xor_sync(0xffffffffu, mnew[r], 2));
+    }
+    float corr[2], rs[2] = {0.f, 0.f};
+#pragma unroll
+    for (int r = 0; r < 2; ++r) corr[r] = (mrow[r] == -INFINITY) ? 0.f : exp2f(mrow[r] - mnew[r]);
+    uint32_t pf[4][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      float p0 = (mnew[0] == -INFINITY) ? 0.f : exp2f(s[n][0] - mnew[0]);
+      float p1 = (mnew[0] == -INFINITY) ? 0.f : exp2f(s[n][1] - mnew[0]);
+      float p2 = (mnew[1] == -INFINITY) ? 0.f : exp2f(s[n][2] - mnew[1]);
+      float p3 = (mnew[1] == -INFINITY) ? 0.f : exp2f(s[n][3] - mnew[1]);
+      rs[0] += p0 + p1;
+      rs[1] += p2 + p3;
+      pf[n >> 1][(n & 1) * 2 + 0] = pack_bf16x2(p0, p1);
+      pf[n >> 1][(n & 1) * 2 + 1] = pack_bf16x2(p2, p3);
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      lrow[r] = lrow[r] * corr[r] + rs[r];
+      mrow[r] = mnew[r];
+    }
+#pragma unroll
+    for (int i = 0; i < ND; ++i) {
+      o[i][0] *= corr[0]; o[i][1] *= corr[0];
+      o[i][2] *= corr[1]; o[i][3] *= corr[1];
+    }
+    // O += P V
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      // A fragment: a0 (row g, keys 16kk+2t..), a1 (row g+8), a2 (row g, keys +8), a3 (row g+8, keys +8)
+      uint32_t af[4] = {pf[kk][0], pf[kk][1], pf[kk][2], pf[kk][3]};
+#pragma unroll
+      for (int dn = 0; dn < ND; dn += 2) {
+        uint32_t b0, b1, b2, b3;
+        const int r = kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+        ldmatrix_x4_trans(vb + swz<D>(r, dn + (lane >> 4)) * 16, b0, b1, b2, b3);
+        mma_bf16_16816(o[dn], af, b0, b1);
+        mma_bf16_16816(o[dn + 1], af, b2, b3);
+      }
+    }
+    __syncthreads();
+  }
+  // row sums across the quad, normalise, store bf16
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 1);
+    lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 2);
+  }
+  const float inv0 = 1.f / lrow[0], inv1 = 1.f / lrow[1];
+  const int ld = a.n_heads * D;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int qrow = q_start + warp * 16 + g + r * 8;
+    if (qrow < len) {
+      bf16* dst = a.out + (int64_t)(tok0 + qrow) * ld + h * D;
+      const float inv = r ? inv1 : inv0;
+#pragma unroll
+      for (int i = 0; i < ND; ++i)
+        *reinterpret_cast<uint32_t*>(dst + i * 8 + 2 * t4) = pack_bf16x2(o[i][2 * r] * inv, o[i][2 * r + 1] * inv);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ decode
+static constexpr int DEC_STAGES = 3;
+
+template <int D>
+__global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a) {
+  constexpr int NK = D / 16, ND = D / 8;
+  extern __shared__ __align__(128) uint8_t sm[];
+  bf16* sK = reinterpret_cast<bf16*>(sm);                  // [STAGES][64][D]
+  bf16* sV = sK + DEC_STAGES * 64 * D;
+  bf16* sQ = sV + DEC_STAGES * 64 * D;                     // [16][D]
+  float* red = reinterpret_cast<float*>(sm);               // reused after the main loop
+
+  const int b = blockIdx.x, kvh = blockIdx.y, split = blockIdx.z;
+  const int G = a.n_heads / a.n_kv;
+  const int ctx = a.ctx_lens[b];
+  const int n_blocks = (ctx + 63) / 64;
+  const int blk0 = split * a.blocks_per_split;
+  const int blk1 = min(n_blocks, blk0 + a.blocks_per_split);
+  const int* bt = a.block_tables + (int64_t)b * a.bt_ld;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int g = lane >> 2, t4 = lane & 3;
+
+  // q rows: head kvh*G + r for r < G, zero rows above
+  for (int i = tid; i < 16 * (D / 8); i += 128) {
+    const int r = i / (D / 8), c = i % (D / 8);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < G) v = *reinterpret_cast<const uint4*>(a.q + ((int64_t)b * a.n_heads + kvh * G + r) * D + c * 8);
+    *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sQ) + swz<D>(r, c) * 16) = v;
+  }
+  auto issue = [&](int blk, int st) {
+    const int64_t off = (int64_t)bt[blk] * a.blk_stride + (int64_t)kvh * 64 * D;
+    load_tile64<D, 128>(sK + st * 64 * D, a.k_cache + off, tid);
+    load_tile64<D, 128>(sV + st * 64 * D, a.v_cache + off, tid);
+  };
+  // prologue
+#pragma unroll
+  for (int s = 0; s < DEC_STAGES - 1; ++s) {
+    if (blk0 + s < blk1) issue(blk0 + s, s);
+    cp_async_commit();
+  }
+  __syncthreads();
+  uint32_t qf[NK][4];
+  {
+    const uint32_t qb = smem_u32(sQ);
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk)
+      ldmatrix_x4(qb + swz<D>(lane & 15, kk * 2 + (lane >> 4)) * 16, qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3]);
+  }
+  float o[ND][4];
+#pragma unroll
+  for (int i = 0; i < ND; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+
+  for (int blk = blk0; blk < blk1; ++blk) {
+    const int it = blk - blk0;
+    {
+      const int nb = blk + DEC_STAGES - 1;
+      if (nb < blk1) issue(nb, (it + DEC_STAGES - 1) % DEC_STAGES);
+      cp_async_commit();
+    }
+    cp_async_wait<DEC_STAGES - 1>();
+    __syncthreads();
+    const int st = it % DEC_STAGES;
+    const uint32_t kb = smem_u32(sK + st * 64 * D), vb = smem_u32(sV + st * 64 * D);
+    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk) {
+      uint32_t b0, b1, b2, b3;
+      const int r = warp * 16 + (lane & 7) + ((lane >> 4) << 3);
+      ldmatrix_x4(kb + swz<D>(r, kk * 2 + ((lane >> 3) & 1)) * 16, b0, b1, b2, b3);
+      mma_bf16_16816(s[0], qf[kk], b0, b1);
+      mma_bf16_16816(s[1], qf[kk], b2, b3);
+    }
+    float mnew[2] = {mrow[0], mrow[1]};
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int kpos = blk * 64 + warp * 16 + n * 8 + 2 * t4 + (e & 1);
+        float v = (kpos < ctx) ? s[n][e] * a.scale_log2 : -INFINITY;
+        s[n][e] = v;
+        mnew[e >> 1] = fmaxf(mnew[e >> 1], v);
+      }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mnew[r] = fmaxf(mnew[r], __shfl_xor_sync(0xffffffffu, mnew[r], 1));
+      mnew[r] = fmaxf(mnew[r], __shfl_xor_sync(0xffffffffu, mnew[r], 2));
+    }
+    float corr[2], rs[2] = {0.f, 0.f};
+#pragma unroll
+    for (int r = 0; r < 2; ++r) corr[r] = (mrow[r] == -INFINITY) ? 0.f : exp2f(mrow[r] - mnew[r]);
+    uint32_t af[4];
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+      float p0 = (mnew[0] == -INFINITY) ? 0.f : exp2f(s[n][0] - mnew[0]);
+      float p1 = (mnew[0] == -INFINITY) ? 0.f : exp2f(s[n][1] - mnew[0]);
+      float p2 = (mnew[1] == -INFINITY) ? 0.f : exp2f(s[n][2] - mnew[1]);
+      float p3 = (mnew[1] == -INFINITY) ? 0.f : exp2f(s[n][3] - mnew[1]);
+      rs[0] += p0 + p1;
+      rs[1] += p2 + p3;
+      af[n * 2 + 0] = pack_bf16x2(p0, p1);
+      af[n * 2 + 1] = pack_bf16x2(p2, p3);
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      lrow[r] = lrow[r] * corr[r] + rs[r];
+      mrow[r] = mnew[r];
+    }
+#pragma unroll
+    for (int i = 0; i < ND; ++i) {
+      o[i][0] *= corr[0]; o[i][1] *= corr[0];
+      o[i][2] *= corr[1]; o[i][3] *= corr[1];
+    }
+#pragma unroll
+    for (int dn = 0; dn < ND; dn += 2) {
+      uint32_t b0, b1, b2, b3;
+      const int r = warp * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+      ldmatrix_x4_trans(vb + swz<D>(r, dn + (lane >> 4)) * 16, b0, b1, b2, b3);
+      mma_bf16_16816(o[dn], af, b0, b1);
+      mma_bf16_16816(o[dn + 1], af, b2, b3);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  // quad sums of l
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 1);
+    lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 2);
+  }
+  // cross-warp combine (fixed order): red = [4 warps][16 rows][D + 2]
+  constexpr int RS = D + 2;
+  float* myred = red + warp * 16 * RS;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int row = g + r * 8;
+#pragma unroll
+    for (int i = 0; i < ND; ++i) {
+      myred[row * RS + i * 8 + 2 * t4] = o[i][2 * r];
+      myred[row * RS + i * 8 + 2 * t4 + 1] = o[i][2 * r + 1];
+    }
+    if (t4 == 0) {
+      myred[row * RS + D] = mrow[r];
+      myred[row * RS + D + 1] = lrow[r];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < G * D; i += 128) {
+    const int row = i / D, d = i % D;
+    float M = -INFINITY;
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, red[(w * 16 + row) * RS + D]);
+    float acc = 0.f, l = 0.f;
+    for (int w = 0; w < 4; ++w) {
+      const float mw = red[(w * 16 + row) * RS + D];
+      const float f = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
+      acc += f * red[(w * 16 + row) * RS + d];
+      l += f * red[(w * 16 + row) * RS + D + 1];
+    }
+    const int h = kvh * G + row;
+    if (a.n_splits == 1) {
+      a.out[(int64_t)b * a.n_heads * D + h * D + d] = __float2bfloat16_rn(acc / l);
+    } else {
+      const int64_t pi = ((int64_t)b * a.n_heads + h) * a.n_splits + split;
+      a.part_o[pi * D + d] = acc;
+      if (d == 0) {
+        a.part_ml[pi * 2] = M;
+        a.part_ml[pi * 2 + 1] = l;
+      }
+    }
+  }
+}
+
+template <int D>
+__global__ void attn_combine_kernel(DecodeAttnArgs a) {
+  const int b = blockIdx.x, h = blockIdx.y;
+  const int64_t p0 = ((int64_t)b * a.n_heads + h) * a.n_splits;
+  float M = -INFINITY;
+  for (int s = 0; s < a.n_splits; ++s) M = fmaxf(M, a.part_ml[(p0 + s) * 2]);
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float acc = 0.f, l = 0.f;
+    for (int s = 0; s < a.n_splits; ++s) {
+      const float ms = a.part_ml[(p0 + s) * 2];
+      const float f = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
+      acc += f * a.part_o[(p0 + s) * D + d];
+      l += f * a.part_ml[(p0 + s) * 2 + 1];
+    }
+    a.out[(int64_t)b * a.n_heads * D + h * D + d] = __float2bfloat16_rn(acc / l);
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+template <int D>
+static cudaError_t prefill_d(const PrefillAttnArgs& a, cudaStream_t s) {
+  const int smem = 5 * 64 * D * 2;
+  static bool cfg = false;
+  if (!cfg) {
+    cudaError_t e = cudaFuncSetAttribute(attn_prefill_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    cfg = true;
+  }
+  if (a.n_tiles == 0) return cudaSuccess;
+  attn_prefill_kernel<D><<<dim3(a.n_tiles, a.n_heads), 128, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t attn_prefill_launch(const PrefillAttnArgs& a, int head_dim, cudaStream_t s) {
+  switch (head_dim) {
+    case 32: return prefill_d<32>(a, s);
+    case 64: return prefill_d<64>(a, s);
+    case 128: return prefill_d<128>(a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int D>
+static cudaError_t decode_d(const DecodeAttnArgs& a, cudaStream_t s) {
+  int smem = (2 * DEC_STAGES * 64 * D + 16 * D) * 2;
+  const int red_bytes = 4 * 16 * (D + 2) * 4;
+  if (smem < red_bytes) smem = red_bytes;
+  static bool cfg = false;
+  if (!cfg) {
+    cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    cfg = true;
+  }
+  if (a.B == 0) return cudaSuccess;
+  if (a.n_heads / a.n_kv > 16) return cudaErrorInvalidValue;
+  attn_decode_kernel<D><<<dim3(a.B, a.n_kv, a.n_splits), 128, smem, s>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || a.n_splits == 1) return e;
+  attn_combine_kernel<D><<<dim3(a.B, a.n_heads), D, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t attn_decode_launch(const DecodeAttnArgs& a, int head_dim, cudaStream_t s) {
+  switch (head_dim) {
+    case 32: return decode_d<32>(a, s);
+    case 64: return decode_d<64>(a, s);
+    case 128: return decode_d<128>(a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace eco

@@ -1,0 +1,765 @@
+// The PaDG instance engine behind include/ecoserve.h: KV block allocator and
+// block tables, weight preparation, and the two phase
+// executors that temporal disaggregation alternates between (PAPER.md Sec.
+// 3.2.1):
+//   prefill phase  (a6-a12): embed -> L x [RMSNorm, QKV GEMM + RoPE + KV write,
+//                  causal varlen attention, O GEMM + residual, RMSNorm,
+//                  gate/up GEMM + SiLU*up, down GEMM + residual] -> final norm of
+//                  each sequence's last row -> LM head + greedy argmax
+//   decode phase   (a13-a16): the same per step with B rows, skinny split-K
+//                  "swap-AB" GEMMs (weights on the MMA M side), split-K paged
+//                  attention, continuous batching (finished requests leave).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/ecoserve.h"
+#include "kernels.h"
+
+using namespace eco;
+
+namespace {
+
+constexpr int BLOCK = 64;
+constexpr int BN_PREFILL = 256;
+
+struct Req {
+  int64_t id;
+  std::vector<int> prompt;
+  int S = 0;
+  int max_new = 1;
+  int n_gen = 0;
+  int last_token = -1;
+  bool finished = false;
+  std::vector<int> blocks;
+};
+
+struct ActMaps {  // one activation buffer as GEMM operand
+  CUtensorMap a;          // as A (box 128 rows): prefill
+  CUtensorMap b[3];       // as B with box 64 / 128 / 256 rows: decode (swap-AB)
+};
+
+struct LayerW {
+  const bf16 *attn_norm, *ffn_norm, *wo, *wd;
+  bf16 *wqkv, *wgu;
+  CUtensorMap qkv_a, qkv_b, o_a, o_b, gu_a, gu_b, d_a, d_b;  // _a: box 128 (decode A), _b: box 256 (prefill B)
+};
+
+int bn_index(int bn) { return bn == 64 ? 0 : bn == 128 ? 1 : 2; }
+int pick_bn(int rows) { return rows <= 64 ? 64 : rows <= 128 ? 128 : 256; }
+
+}  // namespace
+
+struct ecoserve_instance {
+  ecoserve_model_shape shape{};
+  int L = 0, H = 0, M = 0, Mkv = 0, D = 0, F = 0, V = 0, QKV = 0;
+  int device = 0, num_sms = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool dead = false;
+  std::string err;
+  // config
+  int T_max = 16384, B_max = 512, P_max = 16384;
+  bool debug = false;
+  // pool
+  bf16* pool = nullptr;
+  int64_t num_blocks = 0;
+  int64_t blk_stride = 0;  // elements per physical block (all layers)
+  std::vector<int> free_blocks;
+  // weights
+  const bf16 *embed = nullptr, *lm_head = nullptr, *final_norm = nullptr;
+  std::vector<LayerW> lw;
+  CUtensorMap lm_a;
+  // workspace
+  float* x = nullptr;            // [T_max][H] residual stream
+  bf16* h = nullptr;             // [T_max][H] normed GEMM input
+  bf16* q = nullptr;             // [T_max][M][D]
+  bf16* ao = nullptr;            // [T_max][M*D] attention output
+  bf16* act = nullptr;           // [T_max][F]
+  bf16* hl = nullptr;            // [B_max][H] final-normed last rows
+  ActMaps m_h, m_ao, m_act, m_hl;
+  float* part = nullptr;         // split-K partials
+  int64_t part_elems = 0;
+  float* attn_ws = nullptr;      // decode attention partials
+  int64_t attn_ws_elems = 0;
+  float* am_val = nullptr;
+  int* am_idx = nullptr;
+  int am_ld = 0;
+  int* d_tokens = nullptr;
+  int* d_nan = nullptr;
+  float *rope_cos = nullptr, *rope_sin = nullptr;
+  int* d_meta = nullptr;
+  int* h_meta = nullptr;         // pinned
+  int64_t meta_cap = 0;
+  int* h_tokens = nullptr;       // pinned [B_max]
+  float* dbg = nullptr;          // [(L+1)][T_max][H]
+  std::unordered_map<int64_t, std::pair<int, int>> dbg_rows;  // req -> (row0, nrows) of the last phase call
+  std::unordered_map<int64_t, Req> reqs;
+
+  bool fail(const char* what, cudaError_t e) {
+    err = std::string(what) + ": " + cudaGetErrorString(e);
+    dead = true;
+    return false;
+  }
+};
+
+#define CK(expr)                                                  \
+  do {                                                            \
+    cudaError_t _e = (expr);                                      \
+    if (_e != cudaSuccess) {                                      \
+      inst->fail(#expr, _e);                                      \
+      return ECOSERVE_ERR_CUDA;                                   \
+    }                                                             \
+  } while (0)
+
+static bool shape_ok(const ecoserve_model_shape* s) {
+  if (!s) return false;
+  if (s->n_layers < 1 || s->hidden < 64 || s->hidden % 64 || s->n_heads < 1 || s->n_kv_heads < 1) return false;
+  if (s->n_heads % s->n_kv_heads || s->n_heads / s->n_kv_heads > 16) return false;
+  if (!(s->head_dim == 32 || s->head_dim == 64 || s->head_dim == 128)) return false;
+  if (s->ffn_dim < 64 || s->ffn_dim % 64 || s->vocab < 1) return false;
+  if ((s->n_heads * s->head_dim) % 64) return false;
+  return true;
+}
+
+extern "C" {
+
+int64_t ecoserve_kv_pool_bytes(const ecoserve_model_shape* s, int32_t block_tokens, int64_t num_blocks) {
+  if (!shape_ok(s) || block_tokens != BLOCK || num_blocks < 1) return -1;
+  return num_blocks * (int64_t)s->n_layers * 2 * s->n_kv_heads * BLOCK * s->head_dim * 2;
+}
+
+int64_t ecoserve_prepared_weight_bytes(const ecoserve_model_shape* s) {
+  if (!shape_ok(s)) return -1;
+  const int64_t qkv = (int64_t)(s->n_heads + 2 * s->n_kv_heads) * s->head_dim * s->hidden;
+  const int64_t gu = 2LL * s->ffn_dim * s->hidden;
+  return (int64_t)s->n_layers * (qkv + gu) * 2;
+}
+
+const char* ecoserve_last_error(const ecoserve_instance* inst) { return inst ? inst->err.c_str() : "null instance"; }
+
+static ecoserve_status make_act_maps(ecoserve_instance* inst, ActMaps& m, const void* ptr, int64_t rows, int64_t cols) {
+  if (make_tmap_bf16(&m.a, ptr, rows, cols, 128)) return ECOSERVE_ERR_CUDA;
+  const int boxes[3] = {64, 128, 256};
+  for (int i = 0; i < 3; ++i)
+    if (make_tmap_bf16(&m.b[i], ptr, rows, cols, boxes[i])) return ECOSERVE_ERR_CUDA;
+  return ECOSERVE_OK;
+}
+
+void ecoserve_instance_destroy(ecoserve_instance* inst) {
+  if (!inst) return;
+  cudaSetDevice(inst->device);
+  if (inst->stream) cudaStreamSynchronize(inst->stream);
+  void* dev[] = {inst->x, inst->h, inst->q, inst->ao, inst->act, inst->hl, inst->part, inst->attn_ws, inst->am_val,
+                 inst->am_idx, inst->d_tokens, inst->d_nan, inst->rope_cos, inst->rope_sin, inst->d_meta, inst->dbg};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  if (inst->h_meta) cudaFreeHost(inst->h_meta);
+  if (inst->h_tokens) cudaFreeHost(inst->h_tokens);
+  if (inst->own_stream && inst->stream) cudaStreamDestroy(inst->stream);
+  delete inst;
+}
+
+ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, const ecoserve_kv_pool* kv,
+                                         const ecoserve_weights* raw, void* prepared, int32_t device,
+                                         int32_t tp_rank, const void* nccl_unique_id, void* cuda_stream,
+                                         const ecoserve_engine_config* cfg, ecoserve_instance** out) {
+  if (!out) return ECOSERVE_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (!shape_ok(shape) || !kv || !raw || !prepared || !kv->pool || kv->block_tokens != BLOCK || kv->num_blocks < 1 ||
+      !raw->embed || !raw->lm_head || !raw->final_norm || !raw->layers)
+    return ECOSERVE_ERR_INVALID_ARG;
+  if (shape->tp_size != 1 || tp_rank != 0 || nccl_unique_id) return ECOSERVE_ERR_UNSUPPORTED;
+  std::unique_ptr<ecoserve_instance> holder(new ecoserve_instance());
+  ecoserve_instance* inst = holder.get();
+  inst->shape = *shape;
+  inst->L = shape->n_layers;
+  inst->H = shape->hidden;
+  inst->M = shape->n_heads;
+  inst->Mkv = shape->n_kv_heads;
+  inst->D = shape->head_dim;
+  inst->F = shape->ffn_dim;
+  inst->V = shape->vocab;
+  inst->QKV = (inst->M + 2 * inst->Mkv) * inst->D;
+  if (cfg) {
+    if (cfg->token_budget > 0) inst->T_max = cfg->token_budget;
+    if (cfg->max_batch > 0) inst->B_max = cfg->max_batch;
+    if (cfg->max_positions > 0) inst->P_max = cfg->max_positions;
+    inst->debug = cfg->debug_hidden != 0;
+  }
+  if (inst->B_max > inst->T_max) inst->T_max = inst->B_max;
+  inst->device = device;
+  CK(cudaSetDevice(device));
+  CK(cudaDeviceGetAttribute(&inst->num_sms, cudaDevAttrMultiProcessorCount, device));
+  if (cuda_stream) {
+    inst->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  } else {
+    CK(cudaStreamCreateWithFlags(&inst->stream, cudaStreamNonBlocking));
+    inst->own_stream = true;
+  }
+  cudaStream_t st = inst->stream;
+  const int L = inst->L, H = inst->H, M = inst->M, Mkv = inst->Mkv, D = inst->D, F = inst->F, V = inst->V;
+  const int T = inst->T_max;
+
+  // ---- KV pool
+  inst->pool = reinterpret_cast<bf16*>(kv->pool);
+  inst->num_blocks = kv->num_blocks;
+  inst->blk_stride = (int64_t)L * 2 * Mkv * BLOCK * D;
+  CK(cudaMemsetAsync(inst->pool, 0, ecoserve_kv_pool_bytes(shape, BLOCK, kv->num_blocks), st));
+  inst->free_blocks.resize(kv->num_blocks);
+  for (int64_t i = 0; i < kv->num_blocks; ++i) inst->free_blocks[i] = (int)(kv->num_blocks - 1 - i);  // pop_back -> 0,1,..
+
+  // ---- weights: fused + re-laid-out QKV (pair-interleaved q/k rows for RoPE) and gate/up (interleaved)
+  inst->embed = reinterpret_cast<const bf16*>(raw->embed);
+  inst->lm_head = reinterpret_cast<const bf16*>(raw->lm_head);
+  inst->final_norm = reinterpret_cast<const bf16*>(raw->final_norm);
+  const int QKV = inst->QKV;
+  std::vector<int> sel_qkv(QKV), row_qkv(QKV), sel_gu(2 * F), row_gu(2 * F);
+  for (int r = 0; r < QKV; ++r) {
+    int base, src_sel;
+    if (r < M * D) { base = 0; src_sel = 0; }
+    else if (r < (M + Mkv) * D) { base = M * D; src_sel = 1; }
+    else { base = (M + Mkv) * D; src_sel = 2; }
+    const int rr = r - base;
+    sel_qkv[r] = src_sel;
+    if (src_sel == 2) {
+      row_qkv[r] = rr;
+    } else {  // prepared row 2j <- row j, 2j+1 <- row j + D/2 (within a head)
+      const int head = rr / D, i = rr % D;
+      row_qkv[r] = head * D + ((i & 1) ? i / 2 + D / 2 : i / 2);
+    }
+  }
+  for (int r = 0; r < 2 * F; ++r) { sel_gu[r] = r & 1; row_gu[r] = r / 2; }
+  int* d_map = nullptr;
+  CK(cudaMalloc(&d_map, sizeof(int) * (2 * QKV + 4 * F)));
+  CK(cudaMemcpyAsync(d_map, sel_qkv.data(), sizeof(int) * QKV, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_map + QKV, row_qkv.data(), sizeof(int) * QKV, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_map + 2 * QKV, sel_gu.data(), sizeof(int) * 2 * F, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_map + 2 * QKV + 2 * F, row_gu.data(), sizeof(int) * 2 * F, cudaMemcpyHostToDevice, st));
+  bf16* prep = reinterpret_cast<bf16*>(prepared);
+  inst->lw.resize(L);
+  for (int l = 0; l < L; ++l) {
+    const void* const* p = raw->layers + 9 * l;
+    for (int i = 0; i < 9; ++i)
+      if (!p[i]) return ECOSERVE_ERR_INVALID_ARG;
+    LayerW& w = inst->lw[l];
+    w.attn_norm = reinterpret_cast<const bf16*>(p[0]);
+    w.wo = reinterpret_cast<const bf16*>(p[4]);
+    w.ffn_norm = reinterpret_cast<const bf16*>(p[5]);
+    w.wd = reinterpret_cast<const bf16*>(p[8]);
+    w.wqkv = prep;
+    prep += (int64_t)QKV * H;
+    w.wgu = prep;
+    prep += 2LL * F * H;
+    CK(row_gather_launch(reinterpret_cast<const bf16*>(p[1]), reinterpret_cast<const bf16*>(p[2]),
+                         reinterpret_cast<const bf16*>(p[3]), d_map, d_map + QKV, w.wqkv, QKV, H, st));
+    CK(row_gather_launch(reinterpret_cast<const bf16*>(p[6]), reinterpret_cast<const bf16*>(p[7]), nullptr,
+                         d_map + 2 * QKV, d_map + 2 * QKV + 2 * F, w.wgu, 2 * F, H, st));
+    if (make_tmap_bf16(&w.qkv_a, w.wqkv, QKV, H, 128) || make_tmap_bf16(&w.qkv_b, w.wqkv, QKV, H, BN_PREFILL) ||
+        make_tmap_bf16(&w.o_a, w.wo, H, M * D, 128) || make_tmap_bf16(&w.o_b, w.wo, H, M * D, BN_PREFILL) ||
+        make_tmap_bf16(&w.gu_a, w.wgu, 2 * F, H, 128) || make_tmap_bf16(&w.gu_b, w.wgu, 2 * F, H, BN_PREFILL) ||
+        make_tmap_bf16(&w.d_a, w.wd, H, F, 128) || make_tmap_bf16(&w.d_b, w.wd, H, F, BN_PREFILL)) {
+      inst->err = "cuTensorMapEncodeTiled failed (weights)";
+      return ECOSERVE_ERR_CUDA;
+    }
+  }
+  if (make_tmap_bf16(&inst->lm_a, inst->lm_head, V, H, 128)) {
+    inst->err = "cuTensorMapEncodeTiled failed (lm_head)";
+    return ECOSERVE_ERR_CUDA;
+  }
+
+  // ---- workspace
+  CK(cudaMalloc(&inst->x, sizeof(float) * (int64_t)T * H));
+  CK(cudaMalloc(&inst->h, 2LL * T * H));
+  CK(cudaMalloc(&inst->q, 2LL * T * M * D));
+  CK(cudaMalloc(&inst->ao, 2LL * T * M * D));
+  CK(cudaMalloc(&inst->act, 2LL * T * F));
+  CK(cudaMalloc(&inst->hl, 2LL * inst->B_max * H));
+  CK(cudaMemsetAsync(inst->h, 0, 2LL * T * H, st));
+  CK(cudaMemsetAsync(inst->ao, 0, 2LL * T * M * D, st));
+  CK(cudaMemsetAsync(inst->act, 0, 2LL * T * F, st));
+  CK(cudaMemsetAsync(inst->hl, 0, 2LL * inst->B_max * H, st));
+  if (make_act_maps(inst, inst->m_h, inst->h, T, H) || make_act_maps(inst, inst->m_ao, inst->ao, T, M * D) ||
+      make_act_maps(inst, inst->m_act, inst->act, T, F) || make_act_maps(inst, inst->m_hl, inst->hl, inst->B_max, H)) {
+    inst->err = "cuTensorMapEncodeTiled failed (activations)";
+    return ECOSERVE_ERR_CUDA;
+  }
+  const int nmax = std::max(QKV, std::max(2 * F, H));
+  inst->part_elems = 8LL * inst->B_max * nmax;
+  CK(cudaMalloc(&inst->part, sizeof(float) * inst->part_elems));
+  const int max_blocks_seq = (inst->P_max + BLOCK - 1) / BLOCK;
+  inst->attn_ws_elems = (int64_t)inst->B_max * M * 64 * (D + 2);
+  CK(cudaMalloc(&inst->attn_ws, sizeof(float) * inst->attn_ws_elems));
+  inst->am_ld = (V + 127) / 128;
+  CK(cudaMalloc(&inst->am_val, sizeof(float) * (int64_t)inst->B_max * inst->am_ld));
+  CK(cudaMalloc(&inst->am_idx, sizeof(int) * (int64_t)inst->B_max * inst->am_ld));
+  CK(cudaMalloc(&inst->d_tokens, sizeof(int) * inst->B_max));
+  CK(cudaMalloc(&inst->d_nan, sizeof(int)));
+  inst->meta_cap = 6LL * T + 4 + (int64_t)inst->B_max * (max_blocks_seq + 8) + 2LL * (T / 64 + inst->B_max);
+  CK(cudaMalloc(&inst->d_meta, sizeof(int) * inst->meta_cap));
+  CK(cudaMallocHost(&inst->h_meta, sizeof(int) * inst->meta_cap));
+  CK(cudaMallocHost(&inst->h_tokens, sizeof(int) * inst->B_max));
+  // RoPE table: angle(p, i) = p * theta^(-2i/D) in fp64, stored fp32 (reading A3)
+  {
+    const int half = D / 2;
+    std::vector<float> c((int64_t)inst->P_max * half), s((int64_t)inst->P_max * half);
+    for (int p = 0; p < inst->P_max; ++p)
+      for (int i = 0; i < half; ++i) {
+        const double ang = (double)p * pow((double)shape->rope_theta, -2.0 * i / D);
+        c[(int64_t)p * half + i] = (float)cos(ang);
+        s[(int64_t)p * half + i] = (float)sin(ang);
+      }
+    CK(cudaMalloc(&inst->rope_cos, sizeof(float) * c.size()));
+    CK(cudaMalloc(&inst->rope_sin, sizeof(float) * s.size()));
+    CK(cudaMemcpyAsync(inst->rope_cos, c.data(), sizeof(float) * c.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(inst->rope_sin, s.data(), sizeof(float) * s.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  if (inst->debug) CK(cudaMalloc(&inst->dbg, sizeof(float) * (int64_t)(L + 1) * T * H));
+  CK(cudaStreamSynchronize(st));
+  cudaFree(d_map);
+  *out = holder.release();
+  return ECOSERVE_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ forward
+namespace {
+
+struct LayerIO {
+  int rows;          // tokens in this batch
+  const int* pos;    // device
+  const int* slot;   // device
+};
+
+GemmEpi epi_base(ecoserve_instance* inst) {
+  GemmEpi e;
+  memset(&e, 0, sizeof(e));
+  e.rope_cos = inst->rope_cos;
+  e.rope_sin = inst->rope_sin;
+  e.n_heads = inst->M;
+  e.n_kv = inst->Mkv;
+  e.head_dim = inst->D;
+  e.blk_stride = inst->blk_stride;
+  e.q_out = inst->q;
+  return e;
+}
+
+bf16* k_layer(ecoserve_instance* inst, int l) { return inst->pool + (int64_t)l * 2 * inst->Mkv * BLOCK * inst->D; }
+bf16* v_layer(ecoserve_instance* inst, int l) { return k_layer(inst, l) + (int64_t)inst->Mkv * BLOCK * inst->D; }
+
+// Skinny decode GEMM: part = W x^T split-K, then the fixed-order reduce + epilogue.
+cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const ActMaps& xm, int n_out, int K, int B,
+                        int red_mode, GemmEpi e) {
+  const int bn = pick_bn(B);
+  const int m_tiles = (n_out + 127) / 128, n_tiles = (B + bn - 1) / bn;
+  int splits = (inst->num_sms + m_tiles * n_tiles - 1) / (m_tiles * n_tiles);
+  splits = std::min(splits, 8);
+  splits = gemm_effective_splits(K, splits);
+  GemmEpi ge;
+  memset(&ge, 0, sizeof(ge));
+  ge.mode = EPI_SWAP_F32;
+  ge.out = inst->part;
+  ge.ldo = n_out;
+  cudaError_t r = gemm_launch(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, splits, ge, inst->num_sms, inst->stream);
+  if (r != cudaSuccess) return r;
+  return splitk_reduce_launch(red_mode, inst->part, splits, B, n_out, n_out, e, inst->stream);
+}
+
+}  // namespace
+
+static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const int* d_ids, const int* d_pos,
+                                          const int* d_slot, const int* d_cu, const int* d_bt, int bt_ld,
+                                          const int* d_tiles, int n_tiles) {
+  cudaStream_t st = inst->stream;
+  const int L = inst->L, H = inst->H, M = inst->M, D = inst->D, F = inst->F;
+  const float eps = inst->shape.rms_eps;
+  CK(embed_launch(d_ids, inst->embed, inst->x, T, H, st));
+  if (inst->debug) CK(cudaMemcpyAsync(inst->dbg, inst->x, sizeof(float) * (int64_t)T * H, cudaMemcpyDeviceToDevice, st));
+  for (int l = 0; l < L; ++l) {
+    LayerW& w = inst->lw[l];
+    CK(rmsnorm_launch(inst->x, H, nullptr, w.attn_norm, inst->h, T, H, eps, st));
+    GemmEpi e = epi_base(inst);
+    e.mode = EPI_QKV;
+    e.pos = d_pos;
+    e.slot = d_slot;
+    e.k_cache = k_layer(inst, l);
+    e.v_cache = v_layer(inst, l);
+    CK(gemm_launch(&inst->m_h.a, &w.qkv_b, T, inst->QKV, H, BN_PREFILL, 1, e, inst->num_sms, st));
+    PrefillAttnArgs a;
+    a.q = inst->q;
+    a.k_cache = k_layer(inst, l);
+    a.v_cache = v_layer(inst, l);
+    a.blk_stride = inst->blk_stride;
+    a.cu_seqlens = d_cu;
+    a.block_tables = d_bt;
+    a.bt_ld = bt_ld;
+    a.tiles = d_tiles;
+    a.n_tiles = n_tiles;
+    a.out = inst->ao;
+    a.n_heads = M;
+    a.n_kv = inst->Mkv;
+    a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
+    CK(attn_prefill_launch(a, D, st));
+    GemmEpi eo = epi_base(inst);
+    eo.mode = EPI_RESID;
+    eo.resid = inst->x;
+    eo.ldr = H;
+    CK(gemm_launch(&inst->m_ao.a, &w.o_b, T, H, M * D, BN_PREFILL, 1, eo, inst->num_sms, st));
+    CK(rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, T, H, eps, st));
+    GemmEpi eg = epi_base(inst);
+    eg.mode = EPI_SILU;
+    eg.out = inst->act;
+    eg.ldo = F;
+    CK(gemm_launch(&inst->m_h.a, &w.gu_b, T, 2 * F, H, BN_PREFILL, 1, eg, inst->num_sms, st));
+    GemmEpi ed = epi_base(inst);
+    ed.mode = EPI_RESID;
+    ed.resid = inst->x;
+    ed.ldr = H;
+    CK(gemm_launch(&inst->m_act.a, &w.d_b, T, H, F, BN_PREFILL, 1, ed, inst->num_sms, st));
+    if (inst->debug)
+      CK(cudaMemcpyAsync(inst->dbg + (int64_t)(l + 1) * inst->T_max * H, inst->x, sizeof(float) * (int64_t)T * H,
+                         cudaMemcpyDeviceToDevice, st));
+  }
+  return ECOSERVE_OK;
+}
+
+static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const int* d_ids, const int* d_pos,
+                                         const int* d_slot, const int* d_ctx, const int* d_bt, int bt_ld,
+                                         int max_blocks) {
+  cudaStream_t st = inst->stream;
+  const int L = inst->L, H = inst->H, M = inst->M, D = inst->D, F = inst->F;
+  const float eps = inst->shape.rms_eps;
+  CK(embed_launch(d_ids, inst->embed, inst->x, B, H, st));
+  if (inst->debug) CK(cudaMemcpyAsync(inst->dbg, inst->x, sizeof(float) * (int64_t)B * H, cudaMemcpyDeviceToDevice, st));
+  // split the context so that B x Mkv x splits fills the SMs about twice
+  int n_splits = std::max(1, (2 * inst->num_sms + B * inst->Mkv - 1) / (B * inst->Mkv));
+  n_splits = std::min(std::min(n_splits, max_blocks), 64);
+  const int bps = (max_blocks + n_splits - 1) / n_splits;
+  n_splits = (max_blocks + bps - 1) / bps;
+  if ((int64_t)B * M * n_splits * (D + 2) > inst->attn_ws_elems) return ECOSERVE_ERR_INVALID_ARG;
+  for (int l = 0; l < L; ++l) {
+    LayerW& w = inst->lw[l];
+    CK(rmsnorm_launch(inst->x, H, nullptr, w.attn_norm, inst->h, B, H, eps, st));
+    GemmEpi e = epi_base(inst);
+    e.pos = d_pos;
+    e.slot = d_slot;
+    e.k_cache = k_layer(inst, l);
+    e.v_cache = v_layer(inst, l);
+    CK(decode_gemm(inst, w.qkv_a, inst->m_h, inst->QKV, H, B, RED_QKV, e));
+    DecodeAttnArgs a;
+    a.q = inst->q;
+    a.k_cache = k_layer(inst, l);
+    a.v_cache = v_layer(inst, l);
+    a.blk_stride = inst->blk_stride;
+    a.ctx_lens = d_ctx;
+    a.block_tables = d_bt;
+    a.bt_ld = bt_ld;
+    a.B = B;
+    a.n_heads = M;
+    a.n_kv = inst->Mkv;
+    a.n_splits = n_splits;
+    a.blocks_per_split = bps;
+    a.part_o = inst->attn_ws;
+    a.part_ml = inst->attn_ws + (int64_t)B * M * n_splits * D;
+    a.out = inst->ao;
+    a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
+    CK(attn_decode_launch(a, D, st));
+    GemmEpi eo = epi_base(inst);
+    eo.resid = inst->x;
+    eo.ldr = H;
+    CK(decode_gemm(inst, w.o_a, inst->m_ao, H, M * D, B, RED_RESID, eo));
+    CK(rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, B, H, eps, st));
+    GemmEpi eg = epi_base(inst);
+    eg.out = inst->act;
+    eg.ldo = F;
+    CK(decode_gemm(inst, w.gu_a, inst->m_h, 2 * F, H, B, RED_SILU, eg));
+    GemmEpi ed = epi_base(inst);
+    ed.resid = inst->x;
+    ed.ldr = H;
+    CK(decode_gemm(inst, w.d_a, inst->m_act, H, F, B, RED_RESID, ed));
+    if (inst->debug)
+      CK(cudaMemcpyAsync(inst->dbg + (int64_t)(l + 1) * inst->T_max * H, inst->x, sizeof(float) * (int64_t)B * H,
+                         cudaMemcpyDeviceToDevice, st));
+  }
+  return ECOSERVE_OK;
+}
+
+// final RMSNorm of the selected rows + LM head + greedy argmax -> h_tokens[0..n)
+static ecoserve_status lm_head_argmax(ecoserve_instance* inst, const int* d_rows, int n) {
+  cudaStream_t st = inst->stream;
+  const int H = inst->H;
+  CK(rmsnorm_launch(inst->x, H, d_rows, inst->final_norm, inst->hl, n, H, inst->shape.rms_eps, st));
+  GemmEpi e;
+  memset(&e, 0, sizeof(e));
+  e.mode = EPI_SWAP_ARGMAX;
+  e.am_val = inst->am_val;
+  e.am_idx = inst->am_idx;
+  e.am_ld = inst->am_ld;
+  const int bn = pick_bn(n);
+  CK(gemm_launch(&inst->lm_a, &inst->m_hl.b[bn_index(bn)], inst->V, n, H, bn, 1, e, inst->num_sms, st));
+  CK(argmax_reduce_launch(inst->am_val, inst->am_idx, n, inst->am_ld, inst->am_ld, inst->d_tokens, inst->d_nan, st));
+  CK(cudaMemcpyAsync(inst->h_tokens, inst->d_tokens, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+  return ECOSERVE_OK;
+}
+
+extern "C" {
+
+ecoserve_status ecoserve_prefill_phase(ecoserve_instance* inst, const ecoserve_request* reqs, int32_t n,
+                                       int32_t* first_tokens) {
+  if (!inst) return ECOSERVE_ERR_INVALID_ARG;
+  if (inst->dead) return ECOSERVE_ERR_CUDA;
+  if (n < 0 || (n > 0 && (!reqs || !first_tokens))) return ECOSERVE_ERR_INVALID_ARG;
+  if (n == 0) return ECOSERVE_OK;
+  // ---- validate everything first (all-or-nothing)
+  int64_t need_blocks = 0;
+  {
+    std::unordered_map<int64_t, int> seen;
+    for (int i = 0; i < n; ++i) {
+      const ecoserve_request& r = reqs[i];
+      if (r.prompt_len < 1 || !r.prompt || r.max_new_tokens < 1 || r.prompt_len > inst->T_max ||
+          r.prompt_len + r.max_new_tokens > inst->P_max) {
+        inst->err = "invalid request " + std::to_string(r.req_id);
+        return ECOSERVE_ERR_INVALID_ARG;
+      }
+      for (int t = 0; t < r.prompt_len; ++t)
+        if (r.prompt[t] < 0 || r.prompt[t] >= inst->V) {
+          inst->err = "token id out of range in request " + std::to_string(r.req_id);
+          return ECOSERVE_ERR_INVALID_ARG;
+        }
+      if (inst->reqs.count(r.req_id) || seen.count(r.req_id)) {
+        inst->err = "duplicate req_id " + std::to_string(r.req_id);
+        return ECOSERVE_ERR_STATE;
+      }
+      seen[r.req_id] = i;
+      need_blocks += (r.prompt_len + BLOCK - 1) / BLOCK;
+    }
+  }
+  if (need_blocks > (int64_t)inst->free_blocks.size()) {
+    inst->err = "KV pool exhausted";
+    return ECOSERVE_ERR_KV_EXHAUSTED;
+  }
+  // ---- allocate and register
+  std::vector<Req*> rs(n);
+  for (int i = 0; i < n; ++i) {
+    Req r;
+    r.id = reqs[i].req_id;
+    r.S = reqs[i].prompt_len;
+    r.max_new = reqs[i].max_new_tokens;
+    r.prompt.assign(reqs[i].prompt, reqs[i].prompt + r.S);
+    const int nb = (r.S + BLOCK - 1) / BLOCK;
+    for (int b = 0; b < nb; ++b) {
+      r.blocks.push_back(inst->free_blocks.back());
+      inst->free_blocks.pop_back();
+    }
+    rs[i] = &(inst->reqs[r.id] = std::move(r));
+  }
+  // ---- batches of <= T_max tokens and <= B_max sequences (FIFO, reading A16)
+  inst->dbg_rows.clear();
+  int i0 = 0;
+  while (i0 < n) {
+    int i1 = i0, tok = 0;
+    while (i1 < n && (i1 == i0 || (tok + rs[i1]->S <= inst->T_max && i1 - i0 < inst->B_max))) tok += rs[i1++]->S;
+    const int ns = i1 - i0;
+    int bt_ld = 1;
+    for (int i = i0; i < i1; ++i) bt_ld = std::max(bt_ld, (int)rs[i]->blocks.size());
+    // q tiles, longest-first
+    std::vector<std::pair<int, int>> tiles;
+    for (int i = i0; i < i1; ++i)
+      for (int qs = 0; qs < rs[i]->S; qs += 64) tiles.push_back({i - i0, qs});
+    std::stable_sort(tiles.begin(), tiles.end(),
+                     [](const std::pair<int, int>& a, const std::pair<int, int>& b) { return a.second > b.second; });
+    // pack metadata: ids[T] pos[T] slot[T] cu[ns+1] rows[ns] bt[ns][bt_ld] tiles[2*nt]
+    int* hm = inst->h_meta;
+    int* ids = hm;
+    int* pos = ids + tok;
+    int* slot = pos + tok;
+    int* cu = slot + tok;
+    int* rows = cu + ns + 1;
+    int* bt = rows + ns;
+    int* tl = bt + ns * bt_ld;
+    const int64_t used = (tl - hm) + 2LL * tiles.size();
+    if (used > inst->meta_cap) {
+      inst->err = "metadata buffer too small";
+      return ECOSERVE_ERR_INVALID_ARG;
+    }
+    int t = 0;
+    for (int i = i0; i < i1; ++i) {
+      Req* r = rs[i];
+      cu[i - i0] = t;
+      for (int p = 0; p < r->S; ++p, ++t) {
+        ids[t] = r->prompt[p];
+        pos[t] = p;
+        slot[t] = r->blocks[p / BLOCK] * BLOCK + p % BLOCK;
+      }
+      rows[i - i0] = t - 1;
+      for (int b = 0; b < bt_ld; ++b) bt[(i - i0) * bt_ld + b] = b < (int)r->blocks.size() ? r->blocks[b] : 0;
+      if (inst->debug) inst->dbg_rows[r->id] = {cu[i - i0], r->S};
+    }
+    cu[ns] = t;
+    for (size_t k = 0; k < tiles.size(); ++k) {
+      tl[2 * k] = tiles[k].first;
+      tl[2 * k + 1] = tiles[k].second;
+    }
+    cudaStream_t st = inst->stream;
+    CK(cudaMemcpyAsync(inst->d_meta, hm, sizeof(int) * used, cudaMemcpyHostToDevice, st));
+    int* d = inst->d_meta;
+    ecoserve_status s = run_layers_prefill(inst, tok, d, d + (pos - hm), d + (slot - hm), d + (cu - hm),
+                                           d + (bt - hm), bt_ld, d + (tl - hm), (int)tiles.size());
+    if (s != ECOSERVE_OK) return s;
+    s = lm_head_argmax(inst, d + (rows - hm), ns);
+    if (s != ECOSERVE_OK) return s;
+    CK(cudaStreamSynchronize(st));
+    for (int i = i0; i < i1; ++i) {
+      Req* r = rs[i];
+      r->last_token = inst->h_tokens[i - i0];
+      r->n_gen = 1;
+      r->finished = r->n_gen >= r->max_new;
+      first_tokens[i] = r->last_token;
+    }
+    i0 = i1;
+  }
+  return ECOSERVE_OK;
+}
+
+ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* req_ids, int32_t n, int32_t steps,
+                                      int32_t* tokens, int32_t* n_finished) {
+  if (!inst) return ECOSERVE_ERR_INVALID_ARG;
+  if (inst->dead) return ECOSERVE_ERR_CUDA;
+  if (n < 0 || steps < 0 || (n > 0 && (!req_ids || !tokens))) return ECOSERVE_ERR_INVALID_ARG;
+  if (n > inst->B_max) return ECOSERVE_ERR_INVALID_ARG;
+  std::vector<Req*> rs(n);
+  for (int i = 0; i < n; ++i) {
+    auto it = inst->reqs.find(req_ids[i]);
+    if (it == inst->reqs.end() || it->second.n_gen < 1) {
+      inst->err = "decode of unknown or unprefilled req_id " + std::to_string(req_ids[i]);
+      return ECOSERVE_ERR_STATE;
+    }
+    rs[i] = &it->second;
+  }
+  for (int i = 0; i < n * steps; ++i) tokens[i] = -1;
+  for (int s = 0; s < steps; ++s) {
+    std::vector<int> live;
+    for (int i = 0; i < n; ++i)
+      if (!rs[i]->finished) live.push_back(i);
+    const int B = (int)live.size();
+    if (B == 0) break;
+    // blocks for the token fed at position S + n_gen - 1
+    int need = 0;
+    for (int i : live) {
+      const int p = rs[i]->S + rs[i]->n_gen - 1;
+      if (p / BLOCK >= (int)rs[i]->blocks.size()) ++need;
+    }
+    if (need > (int)inst->free_blocks.size()) {
+      inst->err = "KV pool exhausted during decode";
+      return ECOSERVE_ERR_KV_EXHAUSTED;
+    }
+    int bt_ld = 1, max_blocks = 1;
+    for (int i : live) {
+      Req* r = rs[i];
+      const int p = r->S + r->n_gen - 1;
+      if (p / BLOCK >= (int)r->blocks.size()) {
+        r->blocks.push_back(inst->free_blocks.back());
+        inst->free_blocks.pop_back();
+      }
+      bt_ld = std::max(bt_ld, (int)r->blocks.size());
+    }
+    max_blocks = bt_ld;
+    int* hm = inst->h_meta;
+    int* ids = hm;
+    int* pos = ids + B;
+    int* slot = pos + B;
+    int* ctx = slot + B;
+    int* rows = ctx + B;
+    int* bt = rows + B;
+    const int64_t used = (bt - hm) + (int64_t)B * bt_ld;
+    if (used > inst->meta_cap) return ECOSERVE_ERR_INVALID_ARG;
+    if (inst->debug) inst->dbg_rows.clear();
+    for (int k = 0; k < B; ++k) {
+      Req* r = rs[live[k]];
+      const int p = r->S + r->n_gen - 1;
+      ids[k] = r->last_token;
+      pos[k] = p;
+      slot[k] = r->blocks[p / BLOCK] * BLOCK + p % BLOCK;
+      ctx[k] = p + 1;
+      rows[k] = k;
+      for (int b = 0; b < bt_ld; ++b) bt[k * bt_ld + b] = b < (int)r->blocks.size() ? r->blocks[b] : 0;
+      if (inst->debug) inst->dbg_rows[r->id] = {k, 1};
+    }
+    cudaStream_t st = inst->stream;
+    CK(cudaMemcpyAsync(inst->d_meta, hm, sizeof(int) * used, cudaMemcpyHostToDevice, st));
+    int* d = inst->d_meta;
+    ecoserve_status es =
+        run_layers_decode(inst, B, d, d + (pos - hm), d + (slot - hm), d + (ctx - hm), d + (bt - hm), bt_ld, max_blocks);
+    if (es != ECOSERVE_OK) return es;
+    es = lm_head_argmax(inst, d + (rows - hm), B);
+    if (es != ECOSERVE_OK) return es;
+    CK(cudaStreamSynchronize(st));
+    for (int k = 0; k < B; ++k) {
+      Req* r = rs[live[k]];
+      r->last_token = inst->h_tokens[k];
+      r->n_gen += 1;
+      r->finished = r->n_gen >= r->max_new;
+      tokens[(int64_t)live[k] * steps + s] = r->last_token;
+    }
+  }
+  if (n_finished) {
+    int c = 0;
+    for (int i = 0; i < n; ++i) c += rs[i]->finished ? 1 : 0;
+    *n_finished = c;
+  }
+  return ECOSERVE_OK;
+}
+
+ecoserve_status ecoserve_release(ecoserve_instance* inst, const int64_t* req_ids, int32_t n) {
+  if (!inst || n < 0 || (n > 0 && !req_ids)) return ECOSERVE_ERR_INVALID_ARG;
+  for (int i = 0; i < n; ++i)
+    if (!inst->reqs.count(req_ids[i])) return ECOSERVE_ERR_STATE;
+  for (int i = 0; i < n; ++i) {
+    auto it = inst->reqs.find(req_ids[i]);
+    for (int b : it->second.blocks) inst->free_blocks.push_back(b);
+    inst->reqs.erase(it);
+  }
+  return ECOSERVE_OK;
+}
+
+ecoserve_status ecoserve_get_status(const ecoserve_instance* inst, ecoserve_instance_status* out,
+                                    ecoserve_req_status* reqs, int32_t cap) {
+  if (!inst || !out || cap < 0 || (cap > 0 && !reqs)) return ECOSERVE_ERR_INVALID_ARG;
+  out->alive = inst->dead ? 0 : 1;
+  out->n_requests = (int32_t)inst->reqs.size();
+  out->blocks_total = inst->num_blocks;
+  out->blocks_used = inst->num_blocks - (int64_t)inst->free_blocks.size();
+  int k = 0;
+  for (auto& kvp : inst->reqs) {
+    if (k >= cap) break;
+    const Req& r = kvp.second;
+    reqs[k].req_id = r.id;
+    reqs[k].prompt_len = r.S;
+    reqs[k].n_generated = r.n_gen;
+    reqs[k].finished = r.finished ? 1 : 0;
+    reqs[k].n_blocks = (int32_t)r.blocks.size();
+    ++k;
+  }
+  return ECOSERVE_OK;
+}
+
+ecoserve_status ecoserve_debug_hidden(ecoserve_instance* inst, int64_t req_id, int32_t layer, float* out) {
+  if (!inst || !out || layer < 0 || layer > inst->L) return ECOSERVE_ERR_INVALID_ARG;
+  if (!inst->debug) return ECOSERVE_ERR_UNSUPPORTED;
+  auto it = inst->dbg_rows.find(req_id);
+  if (it == inst->dbg_rows.end()) return ECOSERVE_ERR_STATE;
+  const float* src = inst->dbg + ((int64_t)layer * inst->T_max + it->second.first) * inst->H;
+  CK(cudaMemcpy(out, src, sizeof(float) * (int64_t)it->second.second * inst->H, cudaMemcpyDeviceToHost));
+  return ECOSERVE_OK;
+}
+
+}  // extern "C"

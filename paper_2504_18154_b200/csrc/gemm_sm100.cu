@@ -1,0 +1,401 @@
+// tcgen05 / TMEM / TMA warp-specialised persistent GEMM for sm_100a with the
+// fused epilogues of the PaDG instance hot path (SURVEY 8(a) rows a7, a9-a13,
+// a15, a16; Table 2: the six projections are the dense
+// contractions; Eq. 1, Eq. 3).
+//
+//   D[m, n] = sum_k A[m, k] * B[n, k]       A, B bf16 K-major, D f32 in TMEM
+//
+// CTA = 6 warps: warp 0 TMA producer, warp 1 MMA issuer (one elected lane)
+// + TMEM owner, warps 2..5 epilogue (one TMEM lane quarter each, warp % 4).
+// Tile 128 x BN x 64, multi-stage smem ring (full/empty mbarriers), two TMEM
+// accumulators so the epilogue of tile i overlaps the MMAs of tile i+1.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <stdio.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace eco {
+
+static constexpr int BM = 128;
+static constexpr int BK = 64;
+static constexpr int GEMM_THREADS = 192;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ float silu_f(float z) { return z / (1.f + __expf(-z)); }
+
+// ---------------------------------------------------------------- epilogues
+// Non-swapped: this thread owns output row `m` (token), columns n0..n0+31 in v[].
+__device__ __forceinline__ void epi_rows(const GemmEpi& e, int m, int n0, int n_rows, const uint32_t (&v)[32]) {
+  float f[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+  const int ncols = min(32, n_rows - n0);
+  switch (e.mode) {
+    case EPI_F32: {
+      float* o = reinterpret_cast<float*>(e.out) + (int64_t)m * e.ldo + n0;
+      if (ncols == 32) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(f[i], f[i + 1], f[i + 2], f[i + 3]);
+      } else {
+        for (int i = 0; i < ncols; ++i) o[i] = f[i];
+      }
+    } break;
+    case EPI_BF16: {
+      bf16* o = reinterpret_cast<bf16*>(e.out) + (int64_t)m * e.ldo + n0;
+      if (ncols == 32) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+          *reinterpret_cast<uint4*>(o + i) = make_uint4(pack_bf16x2(f[i], f[i + 1]), pack_bf16x2(f[i + 2], f[i + 3]),
+                                                        pack_bf16x2(f[i + 4], f[i + 5]), pack_bf16x2(f[i + 6], f[i + 7]));
+      } else {
+        for (int i = 0; i < ncols; ++i) o[i] = __float2bfloat16_rn(f[i]);
+      }
+    } break;
+    case EPI_RESID: {
+      float* o = e.resid + (int64_t)m * e.ldr + n0;
+      if (ncols == 32) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          float4 r = *reinterpret_cast<float4*>(o + i);
+          r.x += f[i]; r.y += f[i + 1]; r.z += f[i + 2]; r.w += f[i + 3];
+          *reinterpret_cast<float4*>(o + i) = r;
+        }
+      } else {
+        for (int i = 0; i < ncols; ++i) o[i] += f[i];
+      }
+    } break;
+    case EPI_SILU: {  // rows of W_gu are interleaved (gate j, up j) -> output column n0/2 + j
+      bf16* o = reinterpret_cast<bf16*>(e.out) + (int64_t)m * e.ldo + n0 / 2;
+      uint32_t p[8];
+#pragma unroll
+      for (int j = 0; j < 16; j += 2)
+        p[j / 2] = pack_bf16x2(silu_f(f[2 * j]) * f[2 * j + 1], silu_f(f[2 * j + 2]) * f[2 * j + 3]);
+      if (ncols == 32) {
+        *reinterpret_cast<uint4*>(o) = make_uint4(p[0], p[1], p[2], p[3]);
+        *reinterpret_cast<uint4*>(o + 8) = make_uint4(p[4], p[5], p[6], p[7]);
+      } else {
+        for (int j = 0; j < ncols / 2; ++j) o[j] = __float2bfloat16_rn(silu_f(f[2 * j]) * f[2 * j + 1]);
+      }
+    } break;
+    case EPI_QKV: {
+      // 32 columns never straddle a head (D in {32, 64, 128, 256}, n0 % 32 == 0).
+      const int D = e.head_dim, half = D / 2;
+      const int qd = e.n_heads * D, kd = e.n_kv * D;
+      const int p = e.pos[m];
+      if (n0 < qd + kd) {
+        const bool is_q = n0 < qd;
+        const int head = is_q ? n0 / D : (n0 - qd) / D;
+        const int j0 = (n0 % D) / 2;  // pair index of f[0]
+        const float* cs = e.rope_cos + (int64_t)p * half + j0;
+        const float* sn = e.rope_sin + (int64_t)p * half + j0;
+        uint32_t lo[8], hi[8];
+#pragma unroll
+        for (int j = 0; j < 16; j += 2) {
+          float c0 = cs[j], s0 = sn[j], c1 = cs[j + 1], s1 = sn[j + 1];
+          float a0 = f[2 * j], b0 = f[2 * j + 1], a1 = f[2 * j + 2], b1 = f[2 * j + 3];
+          lo[j / 2] = pack_bf16x2(a0 * c0 - b0 * s0, a1 * c1 - b1 * s1);
+          hi[j / 2] = pack_bf16x2(b0 * c0 + a0 * s0, b1 * c1 + a1 * s1);
+        }
+        bf16* dst;
+        if (is_q) {
+          dst = e.q_out + ((int64_t)m * e.n_heads + head) * D;
+        } else {
+          const int s = e.slot[m];
+          dst = e.k_cache + (int64_t)(s >> 6) * e.blk_stride + ((int64_t)head * 64 + (s & 63)) * D;
+        }
+        *reinterpret_cast<uint4*>(dst + j0) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        *reinterpret_cast<uint4*>(dst + j0 + 8) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+        *reinterpret_cast<uint4*>(dst + half + j0) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(dst + half + j0 + 8) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+      } else {
+        const int c = n0 - qd - kd;
+        const int head = c / D, d0 = c % D;
+        const int s = e.slot[m];
+        bf16* dst = e.v_cache + (int64_t)(s >> 6) * e.blk_stride + ((int64_t)head * 64 + (s & 63)) * D + d0;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+          *reinterpret_cast<uint4*>(dst + i) = make_uint4(pack_bf16x2(f[i], f[i + 1]), pack_bf16x2(f[i + 2], f[i + 3]),
+                                                          pack_bf16x2(f[i + 4], f[i + 5]), pack_bf16x2(f[i + 6], f[i + 7]));
+      }
+    } break;
+    default:
+      break;
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int m_rows,
+                   int n_rows, int K, int splits, GemmEpi epi) {
+  using C = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + C::STAGES;
+  uint64_t* tfull_bar = empty_bar + C::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_base_ptr = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  __shared__ float am_v[4][BN];
+  __shared__ int am_i[4][BN];
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m_tiles = (m_rows + BM - 1) / BM;
+  const int n_tiles = (n_rows + BN - 1) / BN;
+  const int kb_total = (K + BK - 1) / BK;
+  const int kb_per = (kb_total + splits - 1) / splits;
+  const int n_work = m_tiles * n_tiles * splits;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapB);
+  }
+  if (warp == 1) tmem_alloc(tmem_base_ptr, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_ptr;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        const int ks = w % splits;
+        const int t = w / splits;
+        const int mt = t / n_tiles, nt = t % n_tiles;
+        const int kb0 = ks * kb_per, kb1 = min(kb_total, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          uint8_t* sb = sa + C::A_BYTES;
+          mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+          tma_load_2d(sa, &mapA, &full_bar[stage], kb * BK, mt * BM);
+          tma_load_2d(sb, &mapB, &full_bar[stage], kb * BK, nt * BN);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        const int ks = w % splits;
+        const int kb0 = ks * kb_per, kb1 = min(kb_total, kb0 + kb_per);
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sb = sa + C::A_BYTES;
+          const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sb);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // advance 16 bf16 = 32 B along K inside the 128 B swizzle row: +2 in 16-byte units
+            tc_mma_f16(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          tc_commit(&empty_bar[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull_bar[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int ep_tid = (warp - 2) * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+      const int ks = w % splits;
+      const int t = w / splits;
+      const int mt = t / n_tiles, nt = t % n_tiles;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = q * 32 + lane;  // accumulator row (TMEM lane)
+      const int m = mt * BM + row;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if (epi.mode == EPI_SWAP_ARGMAX) {
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tbase + c0, v);
+          tc_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            float val = (m < m_rows) ? __uint_as_float(v[i]) : -INFINITY;
+            int idx = m;
+            // warp argmax, lowest index on ties (reading A6); NaN propagates as "largest"
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+              float ov = __shfl_xor_sync(0xffffffffu, val, off);
+              int oi = __shfl_xor_sync(0xffffffffu, idx, off);
+              bool take = (ov > val) || (ov == val && oi < idx) || (isnan(ov) && !isnan(val));
+              if (take) { val = ov; idx = oi; }
+            }
+            if (lane == 0) { am_i[q][c0 + i] = idx; am_v[q][c0 + i] = val; }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int c = ep_tid; c < BN; c += 128) {
+          const int n = nt * BN + c;
+          if (n < n_rows) {
+            float bv = am_v[0][c];
+            int bi = am_i[0][c];
+            for (int qq = 1; qq < 4; ++qq) {
+              float ov = am_v[qq][c];
+              int oi = am_i[qq][c];
+              if ((ov > bv) || (ov == bv && oi < bi) || (isnan(ov) && !isnan(bv))) { bv = ov; bi = oi; }
+            }
+            epi.am_val[(int64_t)n * epi.am_ld + mt] = bv;
+            epi.am_idx[(int64_t)n * epi.am_ld + mt] = bi;
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      } else if (epi.mode == EPI_SWAP_F32) {
+        float* out = reinterpret_cast<float*>(epi.out) + (int64_t)ks * n_rows * epi.ldo;
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tbase + c0, v);
+          tc_wait_ld();
+          if (m < m_rows) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int n = nt * BN + c0 + i;
+              if (n < n_rows) out[(int64_t)n * epi.ldo + m] = __uint_as_float(v[i]);
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      } else {
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tbase + c0, v);
+          tc_wait_ld();
+          const int n0 = nt * BN + c0;
+          if (m < m_rows && n0 < n_rows) epi_rows(epi, m, n0, n_rows, v);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    __syncwarp();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+int make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return -1;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)r;
+}
+
+int gemm_effective_splits(int K, int splits) {
+  // every split must own at least one K block (an empty split would publish an unwritten accumulator)
+  const int kb_total = (K + BK - 1) / BK;
+  if (splits > kb_total) splits = kb_total;
+  if (splits < 1) splits = 1;
+  const int kb_per = (kb_total + splits - 1) / splits;
+  return (kb_total + kb_per - 1) / kb_per;
+}
+
+int gemm_smem_bytes(int bn) {
+  switch (bn) {
+    case 64: return GemmCfg<64>::SMEM;
+    case 128: return GemmCfg<128>::SMEM;
+    default: return GemmCfg<256>::SMEM;
+  }
+}
+
+template <int BN>
+static cudaError_t launch_bn(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K,
+                             int splits, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         GemmCfg<BN>::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int m_tiles = (m_rows + BM - 1) / BM, n_tiles = (n_rows + BN - 1) / BN;
+  const int work = m_tiles * n_tiles * splits;
+  const int grid = work < num_sms ? work : num_sms;
+  if (grid <= 0) return cudaSuccess;
+  gemm_tc_kernel<BN><<<grid, GEMM_THREADS, GemmCfg<BN>::SMEM, stream>>>(*mapA, *mapB, m_rows, n_rows, K, splits, epi);
+  return cudaGetLastError();
+}
+
+cudaError_t gemm_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K, int bn,
+                        int splits, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+  if (splits < 1 || (splits > 1 && epi.mode != EPI_SWAP_F32)) return cudaErrorInvalidValue;
+  splits = gemm_effective_splits(K, splits);
+  switch (bn) {
+    case 64: return launch_bn<64>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
+    case 128: return launch_bn<128>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
+    case 256: return launch_bn<256>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace eco

@@ -1,0 +1,110 @@
+// Internal launchers of the sm_100a kernels (not part of the C ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace eco {
+
+typedef __nv_bfloat16 bf16;
+
+// ------------------------------------------------------------------ GEMM
+// D[m, n] = sum_k A[m, k] * B[n, k]; A [m_rows, K], B [n_rows, K] bf16 row-major.
+// "rows"/"cols" below are the logical output (token, feature) coordinates:
+//   non-swapped modes: m = token, n = feature   (prefill projections)
+//   swapped modes    : m = feature, n = token   (decode skinny GEMMs, LM head)
+enum EpiMode : int {
+  EPI_F32 = 0,          // out f32 [m][ldo]
+  EPI_BF16 = 1,         // out bf16 [m][ldo]
+  EPI_RESID = 2,        // resid f32 [m][ldr] += acc
+  EPI_SILU = 3,         // out bf16 [m][ldo] at n/2: silu(acc[2j]) * acc[2j+1]
+  EPI_QKV = 4,          // RoPE on pair-interleaved q/k heads, q -> q_out, k/v -> paged pool
+  EPI_SWAP_F32 = 5,     // out f32 [split][n][ldo] (ldo = padded m), partial sums of a K split
+  EPI_SWAP_ARGMAX = 6,  // per token n, per 128-row m tile: (max, lowest argmax) -> am_val/am_idx [n][am_ld]
+};
+
+struct GemmEpi {
+  int mode;
+  void* out;
+  int64_t ldo;
+  float* resid;
+  int64_t ldr;
+  // QKV epilogue
+  const int* pos;          // [rows] position of each token
+  const int* slot;         // [rows] physical slot = block * 64 + offset
+  const float* rope_cos;   // [max_pos][D/2]
+  const float* rope_sin;
+  bf16* q_out;             // [rows][n_heads][D]
+  bf16* k_cache;           // layer base of K (block 0, kv head 0)
+  bf16* v_cache;
+  int64_t blk_stride;      // elements between consecutive physical blocks
+  int n_heads, n_kv, head_dim;
+  // argmax epilogue
+  float* am_val;
+  int* am_idx;
+  int am_ld;
+};
+
+// Creates a 2D bf16 tensor map (rows x cols, row-major, 128B swizzle, box 64 x box_rows).
+int make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int box_rows);
+
+// Launch; tile width bn in {64, 128, 256}; splits > 1 only with EPI_SWAP_F32.
+cudaError_t gemm_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K, int bn,
+                        int splits, const GemmEpi& epi, int num_sms, cudaStream_t stream);
+int gemm_smem_bytes(int bn);
+// The number of K splits gemm_launch actually runs for a requested count (every
+// split owns >= 1 K block); the reduction must use the same number.
+int gemm_effective_splits(int K, int splits);
+
+// ------------------------------------------------------------------ attention
+// Prefill causal varlen attention over the paged pool (mma.sync, FA2-style online softmax).
+struct PrefillAttnArgs {
+  const bf16* q;            // [T][M][D]
+  const bf16* k_cache;      // layer base
+  const bf16* v_cache;
+  int64_t blk_stride;
+  const int* cu_seqlens;    // [n_seq + 1]
+  const int* block_tables;  // [n_seq][bt_ld]
+  int bt_ld;
+  const int* tiles;         // [n_tiles][2]: (seq, q_start) for 128-row q tiles
+  int n_tiles;
+  bf16* out;                // [T][M*D]
+  int n_heads, n_kv;
+  float scale_log2;         // log2(e) / sqrt(D)
+};
+cudaError_t attn_prefill_launch(const PrefillAttnArgs& a, int head_dim, cudaStream_t s);
+
+// Decode split-K paged attention + combine.
+struct DecodeAttnArgs {
+  const bf16* q;            // [B][M][D]
+  const bf16* k_cache;
+  const bf16* v_cache;
+  int64_t blk_stride;
+  const int* ctx_lens;      // [B] tokens incl. the current one
+  const int* block_tables;  // [B][bt_ld]
+  int bt_ld;
+  int B, n_heads, n_kv;
+  int n_splits, blocks_per_split;
+  float* part_o;            // [B][M][n_splits][D]
+  float* part_ml;           // [B][M][n_splits][2] (max (log2 domain), sum)
+  bf16* out;                // [B][M*D]
+  float scale_log2;
+};
+cudaError_t attn_decode_launch(const DecodeAttnArgs& a, int head_dim, cudaStream_t s);
+
+// ------------------------------------------------------------------ small kernels
+cudaError_t embed_launch(const int* ids, const bf16* E, float* x, int n, int H, cudaStream_t s);
+cudaError_t rmsnorm_launch(const float* x, int64_t ldx, const int* rows, const bf16* gamma, bf16* out, int n, int H,
+                           float eps, cudaStream_t s);
+// dst[r] = src_sel[r][row[r]] (row copy of `cols` bf16), sel in {0,1,2} -> s0/s1/s2.
+cudaError_t row_gather_launch(const bf16* s0, const bf16* s1, const bf16* s2, const int* sel, const int* row, bf16* dst,
+                              int nrows, int cols, cudaStream_t s);
+cudaError_t argmax_reduce_launch(const float* val, const int* idx, int n, int parts, int ld, int* tokens,
+                                 int* nan_flag, cudaStream_t s);
+// Decode epilogues (after a split-K swap GEMM): sum partial[split][row][col] in fixed split order, then
+enum RedMode : int { RED_BF16 = 0, RED_RESID = 1, RED_SILU = 2, RED_QKV = 3, RED_F32 = 4 };
+cudaError_t splitk_reduce_launch(int mode, const float* part, int splits, int rows, int cols, int64_t ld_part,
+                                 const GemmEpi& epi, cudaStream_t s);
+
+}  // namespace eco

@@ -1,0 +1,158 @@
+// Op-level entry points of include/ecoserve_ops.h: thin wrappers that run the
+// same kernels the phase executors use, for kernel-by-kernel parity tests.
+#include <string.h>
+
+#include <vector>
+
+#include "../../include/ecoserve_ops.h"
+#include "kernels.h"
+
+using namespace eco;
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_num_sms;
+}
+
+#define OPCK(expr)                                   \
+  do {                                               \
+    if ((expr) != cudaSuccess) return ECOSERVE_ERR_CUDA; \
+  } while (0)
+
+extern "C" {
+
+ecoserve_status ecoserve_op_gemm(const void* A, const void* B, int32_t m, int32_t n, int32_t k, int32_t out_mode,
+                                 void* out, int32_t bn, void* stream) {
+  if (!A || !B || !out || m < 1 || n < 1 || k < 1 || k % 8 || (out_mode != 0 && out_mode != 1)) return ECOSERVE_ERR_INVALID_ARG;
+  if (bn != 64 && bn != 128 && bn != 256) return ECOSERVE_ERR_INVALID_ARG;
+  CUtensorMap ma, mb;
+  if (make_tmap_bf16(&ma, A, m, k, 128) || make_tmap_bf16(&mb, B, n, k, bn)) return ECOSERVE_ERR_CUDA;
+  GemmEpi e;
+  memset(&e, 0, sizeof(e));
+  e.mode = out_mode == 0 ? EPI_F32 : EPI_BF16;
+  e.out = out;
+  e.ldo = n;
+  if (out_mode == 1 && n % 8) return ECOSERVE_ERR_INVALID_ARG;
+  if (out_mode == 0 && n % 4) return ECOSERVE_ERR_INVALID_ARG;
+  OPCK(gemm_launch(&ma, &mb, m, n, k, bn, 1, e, num_sms(), (cudaStream_t)stream));
+  return ECOSERVE_OK;
+}
+
+ecoserve_status ecoserve_op_gemm_swap(const void* W, const void* X, int32_t m, int32_t n, int32_t k, int32_t splits,
+                                      float* workspace, float* out, int32_t bn, void* stream) {
+  if (!W || !X || !workspace || !out || m < 1 || n < 1 || k < 1 || k % 8 || m % 2 || splits < 1)
+    return ECOSERVE_ERR_INVALID_ARG;
+  if (bn != 64 && bn != 128 && bn != 256) return ECOSERVE_ERR_INVALID_ARG;
+  CUtensorMap ma, mb;
+  if (make_tmap_bf16(&ma, W, m, k, 128) || make_tmap_bf16(&mb, X, n, k, bn)) return ECOSERVE_ERR_CUDA;
+  const int eff = gemm_effective_splits(k, splits);
+  GemmEpi e;
+  memset(&e, 0, sizeof(e));
+  e.mode = EPI_SWAP_F32;
+  e.out = workspace;
+  e.ldo = m;
+  OPCK(gemm_launch(&ma, &mb, m, n, k, bn, eff, e, num_sms(), (cudaStream_t)stream));
+  GemmEpi r;
+  memset(&r, 0, sizeof(r));
+  r.out = out;
+  r.ldo = m;
+  OPCK(splitk_reduce_launch(RED_F32, workspace, eff, n, m, m, r, (cudaStream_t)stream));
+  return ECOSERVE_OK;
+}
+
+ecoserve_status ecoserve_op_lm_argmax(const void* W, const void* X, int32_t V, int32_t n, int32_t k, float* ws_val,
+                                      int32_t* ws_idx, int32_t* tokens, void* stream) {
+  if (!W || !X || !ws_val || !ws_idx || !tokens || V < 1 || n < 1 || k < 1 || k % 8) return ECOSERVE_ERR_INVALID_ARG;
+  const int bn = n <= 64 ? 64 : n <= 128 ? 128 : 256;
+  CUtensorMap ma, mb;
+  if (make_tmap_bf16(&ma, W, V, k, 128) || make_tmap_bf16(&mb, X, n, k, bn)) return ECOSERVE_ERR_CUDA;
+  const int parts = (V + 127) / 128;
+  GemmEpi e;
+  memset(&e, 0, sizeof(e));
+  e.mode = EPI_SWAP_ARGMAX;
+  e.am_val = ws_val;
+  e.am_idx = ws_idx;
+  e.am_ld = parts;
+  OPCK(gemm_launch(&ma, &mb, V, n, k, bn, 1, e, num_sms(), (cudaStream_t)stream));
+  OPCK(argmax_reduce_launch(ws_val, ws_idx, n, parts, parts, tokens, nullptr, (cudaStream_t)stream));
+  return ECOSERVE_OK;
+}
+
+ecoserve_status ecoserve_op_rmsnorm(const float* x, const int32_t* rows, const void* gamma, void* out, int32_t n,
+                                    int32_t H, float eps, void* stream) {
+  if (!x || !gamma || !out || n < 0 || H < 4 || H % 4) return ECOSERVE_ERR_INVALID_ARG;
+  OPCK(rmsnorm_launch(x, H, rows, (const bf16*)gamma, (bf16*)out, n, H, eps, (cudaStream_t)stream));
+  return ECOSERVE_OK;
+}
+
+ecoserve_status ecoserve_op_attention_prefill(const void* q, const void* pool, int64_t num_blocks, int32_t n_heads,
+                                              int32_t n_kv, int32_t head_dim, const int32_t* cu_seqlens_host,
+                                              int32_t n_seq, const int32_t* block_tables, int32_t bt_ld, void* out,
+                                              void* stream) {
+  if (!q || !pool || !cu_seqlens_host || !block_tables || !out || n_seq < 1 || n_heads % n_kv || num_blocks < 1)
+    return ECOSERVE_ERR_INVALID_ARG;
+  std::vector<int> tiles;
+  for (int s = 0; s < n_seq; ++s) {
+    const int len = cu_seqlens_host[s + 1] - cu_seqlens_host[s];
+    if (len < 1 || (len + 63) / 64 > bt_ld) return ECOSERVE_ERR_INVALID_ARG;
+    for (int qs = 0; qs < len; qs += 64) { tiles.push_back(s); tiles.push_back(qs); }
+  }
+  int* d = nullptr;
+  const size_t bytes = sizeof(int) * (tiles.size() + n_seq + 1);
+  OPCK(cudaMallocAsync((void**)&d, bytes, (cudaStream_t)stream));
+  OPCK(cudaMemcpyAsync(d, cu_seqlens_host, sizeof(int) * (n_seq + 1), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  OPCK(cudaMemcpyAsync(d + n_seq + 1, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice,
+                       (cudaStream_t)stream));
+  PrefillAttnArgs a;
+  a.q = (const bf16*)q;
+  a.k_cache = (const bf16*)pool;
+  a.v_cache = (const bf16*)pool + (int64_t)n_kv * 64 * head_dim;
+  a.blk_stride = 2LL * n_kv * 64 * head_dim;
+  a.cu_seqlens = d;
+  a.block_tables = block_tables;
+  a.bt_ld = bt_ld;
+  a.tiles = d + n_seq + 1;
+  a.n_tiles = (int)tiles.size() / 2;
+  a.out = (bf16*)out;
+  a.n_heads = n_heads;
+  a.n_kv = n_kv;
+  a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)head_dim));
+  const cudaError_t e = attn_prefill_launch(a, head_dim, (cudaStream_t)stream);
+  cudaFreeAsync(d, (cudaStream_t)stream);
+  return e == cudaSuccess ? ECOSERVE_OK : ECOSERVE_ERR_CUDA;
+}
+
+ecoserve_status ecoserve_op_attention_decode(const void* q, const void* pool, int32_t n_heads, int32_t n_kv,
+                                             int32_t head_dim, const int32_t* ctx_lens, int32_t B,
+                                             const int32_t* block_tables, int32_t bt_ld, int32_t n_splits,
+                                             int32_t blocks_per_split, float* workspace, void* out, void* stream) {
+  if (!q || !pool || !ctx_lens || !block_tables || !out || B < 1 || n_heads % n_kv || n_splits < 1 ||
+      blocks_per_split < 1 || (n_splits > 1 && !workspace))
+    return ECOSERVE_ERR_INVALID_ARG;
+  DecodeAttnArgs a;
+  a.q = (const bf16*)q;
+  a.k_cache = (const bf16*)pool;
+  a.v_cache = (const bf16*)pool + (int64_t)n_kv * 64 * head_dim;
+  a.blk_stride = 2LL * n_kv * 64 * head_dim;
+  a.ctx_lens = ctx_lens;
+  a.block_tables = block_tables;
+  a.bt_ld = bt_ld;
+  a.B = B;
+  a.n_heads = n_heads;
+  a.n_kv = n_kv;
+  a.n_splits = n_splits;
+  a.blocks_per_split = blocks_per_split;
+  a.part_o = workspace;
+  a.part_ml = workspace ? workspace + (int64_t)B * n_heads * n_splits * head_dim : nullptr;
+  a.out = (bf16*)out;
+  a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)head_dim));
+  OPCK(attn_decode_launch(a, head_dim, (cudaStream_t)stream));
+  return ECOSERVE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,214 @@
+// Memory-bound helper kernels of the hot path:
+//  * embedding gather (Fig. 2) -> fp32 residual stream
+//  * RMSNorm (reading A4) of residual rows -> bf16 GEMM input
+//  * fixed-order split-K reduction with the decode epilogues (a13, a15):
+//    RoPE + paged KV append, residual add, SiLU*up
+//  * greedy argmax reduction over LM-head tile partials (a12, a16; reading A6)
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace eco {
+
+__global__ void embed_kernel(const int* __restrict__ ids, const bf16* __restrict__ E, float* __restrict__ x, int H) {
+  const int t = blockIdx.x;
+  const bf16* src = E + (int64_t)ids[t] * H;
+  float* dst = x + (int64_t)t * H;
+  for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8) {
+    uint4 v = *reinterpret_cast<const uint4*>(src + i);
+    float4 a = make_float4(bf16_lo(v.x), bf16_hi(v.x), bf16_lo(v.y), bf16_hi(v.y));
+    float4 b = make_float4(bf16_lo(v.z), bf16_hi(v.z), bf16_lo(v.w), bf16_hi(v.w));
+    *reinterpret_cast<float4*>(dst + i) = a;
+    *reinterpret_cast<float4*>(dst + i + 4) = b;
+  }
+}
+
+cudaError_t embed_launch(const int* ids, const bf16* E, float* x, int n, int H, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  embed_kernel<<<n, 128, 0, s>>>(ids, E, x, H);
+  return cudaGetLastError();
+}
+
+// out[i] = bf16( x[row_i] * rsqrt(mean(x[row_i]^2) + eps) * gamma ), row_i = rows ? rows[i] : i
+__global__ void rmsnorm_kernel(const float* __restrict__ x, int64_t ldx, const int* __restrict__ rows,
+                               const bf16* __restrict__ gamma, bf16* __restrict__ out, int H, float eps) {
+  const int i = blockIdx.x;
+  const int r = rows ? rows[i] : i;
+  const float* src = x + (int64_t)r * ldx;
+  float ss = 0.f;
+  for (int c = threadIdx.x * 4; c < H; c += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<const float4*>(src + c);
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  __shared__ float red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / H + eps);
+  bf16* dst = out + (int64_t)i * H;
+  for (int c = threadIdx.x * 4; c < H; c += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<const float4*>(src + c);
+    uint2 gv = *reinterpret_cast<const uint2*>(gamma + c);
+    uint2 o;
+    o.x = pack_bf16x2(v.x * inv * bf16_lo(gv.x), v.y * inv * bf16_hi(gv.x));
+    o.y = pack_bf16x2(v.z * inv * bf16_lo(gv.y), v.w * inv * bf16_hi(gv.y));
+    *reinterpret_cast<uint2*>(dst + c) = o;
+  }
+}
+
+cudaError_t rmsnorm_launch(const float* x, int64_t ldx, const int* rows, const bf16* gamma, bf16* out, int n, int H,
+                           float eps, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  if (H % 4) return cudaErrorInvalidValue;
+  const int threads = H >= 4096 ? 512 : (H >= 1024 ? 256 : 128);
+  rmsnorm_kernel<<<n, threads, 0, s>>>(x, ldx, rows, gamma, out, H, eps);
+  return cudaGetLastError();
+}
+
+__global__ void row_gather_kernel(const bf16* __restrict__ s0, const bf16* __restrict__ s1,
+                                  const bf16* __restrict__ s2, const int* __restrict__ sel,
+                                  const int* __restrict__ row, bf16* __restrict__ dst, int cols) {
+  const int r = blockIdx.x;
+  const bf16* src = (sel[r] == 0 ? s0 : sel[r] == 1 ? s1 : s2) + (int64_t)row[r] * cols;
+  bf16* d = dst + (int64_t)r * cols;
+  for (int c = threadIdx.x * 8; c < cols; c += blockDim.x * 8)
+    *reinterpret_cast<uint4*>(d + c) = *reinterpret_cast<const uint4*>(src + c);
+}
+
+cudaError_t row_gather_launch(const bf16* s0, const bf16* s1, const bf16* s2, const int* sel, const int* row, bf16* dst,
+                              int nrows, int cols, cudaStream_t s) {
+  if (nrows == 0) return cudaSuccess;
+  if (cols % 8) return cudaErrorInvalidValue;
+  row_gather_kernel<<<nrows, 128, 0, s>>>(s0, s1, s2, sel, row, dst, cols);
+  return cudaGetLastError();
+}
+
+// tokens[i] = argmax over parts of (val, idx): largest value, lowest index on ties.
+__global__ void argmax_reduce_kernel(const float* __restrict__ val, const int* __restrict__ idx, int parts, int ld,
+                                     int* __restrict__ tokens, int* __restrict__ nan_flag) {
+  const int i = blockIdx.x;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  bool nan = false;
+  for (int p = threadIdx.x; p < parts; p += blockDim.x) {
+    const float v = val[(int64_t)i * ld + p];
+    const int x = idx[(int64_t)i * ld + p];
+    if (isnan(v)) nan = true;
+    if (v > bv || (v == bv && x < bi)) { bv = v; bi = x; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  __shared__ int sn;
+  if (threadIdx.x == 0) sn = 0;
+  __syncthreads();
+  if (nan) atomicOr(&sn, 1);
+  if ((threadIdx.x & 31) == 0) { sv[threadIdx.x >> 5] = bv; si[threadIdx.x >> 5] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x / 32); ++w)
+      if (sv[w] > bv || (sv[w] == bv && si[w] < bi)) { bv = sv[w]; bi = si[w]; }
+    tokens[i] = bi;
+    if (sn && nan_flag) atomicOr(nan_flag, 1);
+  }
+}
+
+cudaError_t argmax_reduce_launch(const float* val, const int* idx, int n, int parts, int ld, int* tokens, int* nan_flag,
+                                 cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  argmax_reduce_kernel<<<n, 128, 0, s>>>(val, idx, parts, ld, tokens, nan_flag);
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ float silu_r(float z) { return z / (1.f + __expf(-z)); }
+
+// part [split][row][ld_part] f32; one thread per (row, column pair).
+__global__ void splitk_reduce_kernel(int mode, const float* __restrict__ part, int splits, int rows, int cols,
+                                     int64_t ld_part, GemmEpi e) {
+  const int pairs = cols / 2;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)rows * pairs) return;
+  const int row = gid / pairs, c = 2 * (int)(gid % pairs);
+  float a = 0.f, b = 0.f;
+  const int64_t plane = (int64_t)rows * ld_part;
+  for (int s = 0; s < splits; ++s) {  // fixed order: deterministic
+    const float2 v = *reinterpret_cast<const float2*>(part + s * plane + (int64_t)row * ld_part + c);
+    a += v.x;
+    b += v.y;
+  }
+  switch (mode) {
+    case RED_F32: {
+      float* o = reinterpret_cast<float*>(e.out) + (int64_t)row * e.ldo + c;
+      o[0] = a;
+      o[1] = b;
+    } break;
+    case RED_BF16:
+      *reinterpret_cast<uint32_t*>(reinterpret_cast<bf16*>(e.out) + (int64_t)row * e.ldo + c) = pack_bf16x2(a, b);
+      break;
+    case RED_RESID: {
+      float2* o = reinterpret_cast<float2*>(e.resid + (int64_t)row * e.ldr + c);
+      float2 r = *o;
+      r.x += a;
+      r.y += b;
+      *o = r;
+    } break;
+    case RED_SILU:
+      reinterpret_cast<bf16*>(e.out)[(int64_t)row * e.ldo + c / 2] = __float2bfloat16_rn(silu_r(a) * b);
+      break;
+    case RED_QKV: {
+      const int D = e.head_dim, half = D / 2;
+      const int qd = e.n_heads * D, kd = e.n_kv * D;
+      if (c < qd + kd) {
+        const bool is_q = c < qd;
+        const int head = is_q ? c / D : (c - qd) / D;
+        const int j = (c % D) / 2;
+        const int p = e.pos[row];
+        const float cs = e.rope_cos[(int64_t)p * half + j], sn = e.rope_sin[(int64_t)p * half + j];
+        bf16* dst;
+        if (is_q) {
+          dst = e.q_out + ((int64_t)row * e.n_heads + head) * D;
+        } else {
+          const int s = e.slot[row];
+          dst = e.k_cache + (int64_t)(s >> 6) * e.blk_stride + ((int64_t)head * 64 + (s & 63)) * D;
+        }
+        dst[j] = __float2bfloat16_rn(a * cs - b * sn);
+        dst[j + half] = __float2bfloat16_rn(b * cs + a * sn);
+      } else {
+        const int cc = c - qd - kd;
+        const int head = cc / D, d = cc % D;
+        const int s = e.slot[row];
+        bf16* dst = e.v_cache + (int64_t)(s >> 6) * e.blk_stride + ((int64_t)head * 64 + (s & 63)) * D + d;
+        *reinterpret_cast<uint32_t*>(dst) = pack_bf16x2(a, b);
+      }
+    } break;
+    default:
+      break;
+  }
+}
+
+cudaError_t splitk_reduce_launch(int mode, const float* part, int splits, int rows, int cols, int64_t ld_part,
+                                 const GemmEpi& epi, cudaStream_t s) {
+  const int64_t n = (int64_t)rows * (cols / 2);
+  if (n == 0) return cudaSuccess;
+  if (cols % 2) return cudaErrorInvalidValue;
+  const int threads = 256;
+  splitk_reduce_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(mode, part, splits, rows, cols,
+                                                                                    ld_part, epi);
+  return cudaGetLastError();
+}
+
+}  // namespace eco

@@ -1,0 +1,149 @@
+"""Python-side handle of one PaDG instance (include/ecoserve.h).
+
+PyTorch is used only as the device-memory allocator for the buffers the C ABI
+borrows (weights, prepared weights, KV pool); every computation runs in
+libecoserve.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+LAYER_TENSORS = ("attn_norm", "wq", "wk", "wv", "wo", "ffn_norm", "w_gate", "w_up", "w_down")
+
+
+def c_shape(s, tp_size: int = 1) -> L.ModelShape:
+    return L.ModelShape(s.n_layers, s.hidden, s.n_heads, s.n_kv_heads, s.head_dim, s.ffn_dim, s.vocab,
+                        float(s.rope_theta), float(s.rms_eps), tp_size)
+
+
+def upload_bf16(bits: np.ndarray, device) -> torch.Tensor:
+    """uint16 bf16 bit patterns (host) -> torch.bfloat16 tensor on `device`."""
+    t = torch.from_numpy(np.ascontiguousarray(bits).view(np.int16))
+    return t.to(device).view(torch.bfloat16)
+
+
+def device_weights_from_host(w, device) -> Dict:
+    """synthetic.weights.Bf16Weights -> dict of device bf16 tensors."""
+    return {
+        "embed": upload_bf16(w.embed, device),
+        "lm_head": upload_bf16(w.lm_head, device),
+        "final_norm": upload_bf16(w.final_norm, device),
+        "layers": [{k: upload_bf16(l[k], device) for k in LAYER_TENSORS} for l in w.layers],
+    }
+
+
+def random_device_weights(shape, seed: int, device) -> Dict:
+    """Random-init weights drawn directly on the GPU (bench only; same recipe
+    as synthetic.weights but torch's CUDA generator, so not oracle-reproducible)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    H, D, F, V = shape.hidden, shape.head_dim, shape.ffn_dim, shape.vocab
+    M, Mkv = shape.n_heads, shape.n_kv_heads
+
+    def mat(o, i, std=None):
+        return (torch.randn(o, i, generator=g, device=device) * (std if std else i ** -0.5)).to(torch.bfloat16)
+
+    def norm(n):
+        return (1.0 + (torch.rand(n, generator=g, device=device) - 0.5) * 0.2).to(torch.bfloat16)
+    layers = []
+    for _ in range(shape.n_layers):
+        layers.append({"attn_norm": norm(H), "wq": mat(M * D, H), "wk": mat(Mkv * D, H), "wv": mat(Mkv * D, H),
+                       "wo": mat(H, M * D), "ffn_norm": norm(H), "w_gate": mat(F, H), "w_up": mat(F, H),
+                       "w_down": mat(H, F)})
+    return {"embed": mat(V, H, 1.0), "lm_head": mat(V, H, 2.0 / H ** 0.5), "final_norm": norm(H), "layers": layers}
+
+
+class Instance:
+    """One instance on one GPU. Owns (via torch) the borrowed buffers."""
+
+    def __init__(self, shape, weights: Dict, num_blocks: int, device: int = 0, token_budget: int = 16384,
+                 max_batch: int = 512, max_positions: int = 16384, debug_hidden: bool = False,
+                 free_raw_after_create: bool = False):
+        self.lib = L.load()
+        self.shape = shape
+        self.device = torch.device("cuda", device)
+        self.cshape = c_shape(shape)
+        pool_bytes = self.lib.ecoserve_kv_pool_bytes(C.byref(self.cshape), 64, num_blocks)
+        prep_bytes = self.lib.ecoserve_prepared_weight_bytes(C.byref(self.cshape))
+        if pool_bytes < 0 or prep_bytes < 0:
+            raise L.EcoError(L.ERR_INVALID_ARG, "unsupported shape")
+        self.pool = torch.empty(pool_bytes, dtype=torch.uint8, device=self.device)
+        self.prepared = torch.empty(prep_bytes, dtype=torch.uint8, device=self.device)
+        self.weights = weights
+        ptrs = []
+        for l in weights["layers"]:
+            ptrs += [l[k].data_ptr() for k in LAYER_TENSORS]
+        self._layer_ptrs = (C.c_void_p * len(ptrs))(*ptrs)
+        self.cw = L.Weights(weights["embed"].data_ptr(), weights["lm_head"].data_ptr(),
+                            weights["final_norm"].data_ptr(), C.cast(self._layer_ptrs, C.POINTER(C.c_void_p)))
+        self.ckv = L.KVPool(64, num_blocks, self.pool.data_ptr())
+        self.cfg = L.EngineConfig(token_budget, max_batch, max_positions, 1 if debug_hidden else 0)
+        self.num_blocks = num_blocks
+        h = C.c_void_p()
+        torch.cuda.set_device(self.device)
+        L.check(self.lib.ecoserve_instance_create(C.byref(self.cshape), C.byref(self.ckv), C.byref(self.cw),
+                                                  C.c_void_p(self.prepared.data_ptr()), device, 0, None, None,
+                                                  C.byref(self.cfg), C.byref(h)))
+        self.h = h
+        if free_raw_after_create:  # wq/wk/wv/w_gate/w_up were copied into the prepared buffer
+            for l in weights["layers"]:
+                for k in ("wq", "wk", "wv", "w_gate", "w_up"):
+                    l[k] = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.ecoserve_instance_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ phases
+    def prefill(self, reqs: Sequence[Tuple[int, np.ndarray, int]]) -> np.ndarray:
+        """reqs: (req_id, prompt int32[S], max_new_tokens). Returns first tokens."""
+        n = len(reqs)
+        arr = (L.Request * n)()
+        keep = []
+        for i, (rid, prompt, g) in enumerate(reqs):
+            p = np.ascontiguousarray(prompt, dtype=np.int32)
+            keep.append(p)
+            arr[i] = L.Request(int(rid), p.ctypes.data_as(L.PI32), len(p), int(g))
+        out = np.zeros(n, dtype=np.int32)
+        L.check(self.lib.ecoserve_prefill_phase(self.h, arr, n, out.ctypes.data_as(L.PI32)), self.h)
+        return out
+
+    def decode(self, req_ids: Sequence[int], steps: int):
+        n = len(req_ids)
+        ids = np.ascontiguousarray(req_ids, dtype=np.int64)
+        toks = np.zeros((n, steps), dtype=np.int32)
+        nf = C.c_int32(0)
+        L.check(self.lib.ecoserve_decode_phase(self.h, ids.ctypes.data_as(L.PI64), n, steps,
+                                               toks.ctypes.data_as(L.PI32), C.byref(nf)), self.h)
+        return toks, nf.value
+
+    def release(self, req_ids: Sequence[int]) -> None:
+        ids = np.ascontiguousarray(req_ids, dtype=np.int64)
+        L.check(self.lib.ecoserve_release(self.h, ids.ctypes.data_as(L.PI64), len(ids)), self.h)
+
+    def status(self, cap: int = 4096):
+        st = L.InstanceStatus()
+        rs = (L.ReqStatus * cap)()
+        L.check(self.lib.ecoserve_get_status(self.h, C.byref(st), rs, cap), self.h)
+        reqs = [dict(req_id=r.req_id, prompt_len=r.prompt_len, n_generated=r.n_generated,
+                     finished=bool(r.finished), n_blocks=r.n_blocks) for r in rs[:min(cap, st.n_requests)]]
+        return dict(alive=bool(st.alive), n_requests=st.n_requests, blocks_total=st.blocks_total,
+                    blocks_used=st.blocks_used), reqs
+
+    def hidden(self, req_id: int, layer: int, rows: int) -> np.ndarray:
+        out = np.zeros((rows, self.shape.hidden), dtype=np.float32)
+        L.check(self.lib.ecoserve_debug_hidden(self.h, int(req_id), layer, out.ctypes.data_as(L.PF32)), self.h)
+        return out

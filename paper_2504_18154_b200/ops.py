@@ -1,0 +1,75 @@
+"""Op-level wrappers (include/ecoserve_ops.h) over torch CUDA tensors."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+def _s(stream=None):
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream if stream is None else stream)
+
+
+def gemm(A: torch.Tensor, B: torch.Tensor, out_dtype=torch.float32, bn: int = 256) -> torch.Tensor:
+    m, k = A.shape
+    n = B.shape[0]
+    out = torch.empty(m, n, dtype=out_dtype, device=A.device)
+    L.check(L.load().ecoserve_op_gemm(A.data_ptr(), B.data_ptr(), m, n, k, 0 if out_dtype == torch.float32 else 1,
+                                      out.data_ptr(), bn, _s()))
+    return out
+
+
+def gemm_swap(W: torch.Tensor, X: torch.Tensor, splits: int = 1, bn: int = 64) -> torch.Tensor:
+    m, k = W.shape
+    n = X.shape[0]
+    ws = torch.empty(splits, n, m, dtype=torch.float32, device=W.device)
+    out = torch.empty(n, m, dtype=torch.float32, device=W.device)
+    L.check(L.load().ecoserve_op_gemm_swap(W.data_ptr(), X.data_ptr(), m, n, k, splits, ws.data_ptr(), out.data_ptr(),
+                                           bn, _s()))
+    return out
+
+
+def lm_argmax(W: torch.Tensor, X: torch.Tensor) -> torch.Tensor:
+    V, k = W.shape
+    n = X.shape[0]
+    parts = (V + 127) // 128
+    wv = torch.empty(n, parts, dtype=torch.float32, device=W.device)
+    wi = torch.empty(n, parts, dtype=torch.int32, device=W.device)
+    tok = torch.empty(n, dtype=torch.int32, device=W.device)
+    L.check(L.load().ecoserve_op_lm_argmax(W.data_ptr(), X.data_ptr(), V, n, k, wv.data_ptr(), wi.data_ptr(),
+                                           tok.data_ptr(), _s()))
+    return tok
+
+
+def rmsnorm(x: torch.Tensor, gamma: torch.Tensor, eps: float, rows=None) -> torch.Tensor:
+    n = x.shape[0] if rows is None else rows.shape[0]
+    H = x.shape[1]
+    out = torch.empty(n, H, dtype=torch.bfloat16, device=x.device)
+    L.check(L.load().ecoserve_op_rmsnorm(x.data_ptr(), None if rows is None else rows.data_ptr(), gamma.data_ptr(),
+                                         out.data_ptr(), n, H, eps, _s()))
+    return out
+
+
+def attention_prefill(q, pool, num_blocks, n_heads, n_kv, head_dim, cu_seqlens, block_tables):
+    T = q.shape[0]
+    out = torch.empty(T, n_heads * head_dim, dtype=torch.bfloat16, device=q.device)
+    cu = np.ascontiguousarray(cu_seqlens, dtype=np.int32)
+    n_seq = len(cu) - 1
+    L.check(L.load().ecoserve_op_attention_prefill(q.data_ptr(), pool.data_ptr(), num_blocks, n_heads, n_kv, head_dim,
+                                                   cu.ctypes.data_as(L.PI32), n_seq, block_tables.data_ptr(),
+                                                   block_tables.shape[1], out.data_ptr(), _s()))
+    return out
+
+
+def attention_decode(q, pool, n_heads, n_kv, head_dim, ctx_lens, block_tables, n_splits, blocks_per_split):
+    B = q.shape[0]
+    out = torch.empty(B, n_heads * head_dim, dtype=torch.bfloat16, device=q.device)
+    ws = torch.empty(B * n_heads * n_splits * (head_dim + 2), dtype=torch.float32, device=q.device)
+    L.check(L.load().ecoserve_op_attention_decode(q.data_ptr(), pool.data_ptr(), n_heads, n_kv, head_dim,
+                                                  ctx_lens.data_ptr(), B, block_tables.data_ptr(),
+                                                  block_tables.shape[1], n_splits, blocks_per_split, ws.data_ptr(),
+                                                  out.data_ptr(), _s()))
+    return out

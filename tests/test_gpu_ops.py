@@ -1,0 +1,149 @@
+"""Kernel-by-kernel parity of the CUDA path against the oracle's definitions
+(GPU only). Inputs are seeded and bf16-exact; the oracle side computes in fp64.
+
+Tolerances: GEMMs accumulate bf16 products in fp32
+(error << 1e-4 of the output scale); outputs rounded to bf16 add 2^-9 relative;
+attention additionally rounds P to bf16 before PV (FA2 practice) -> 1e-2 of the
+output scale.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import transformer as T
+from synthetic.weights import bf16_bits_to_f32, f32_to_bf16_bits
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ops():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from paper_2504_18154_b200 import ops as O
+    return O
+
+
+def bf16_rand(rng, shape, scale=1.0):
+    bits = f32_to_bf16_bits(rng.standard_normal(shape).astype(np.float32) * scale)
+    host = bf16_bits_to_f32(bits).astype(np.float64)
+    dev = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.bfloat16)
+    return host, dev
+
+
+def rel_err(got, ref):
+    return float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-30))
+
+
+@pytest.mark.parametrize("m,n,k,bn", [(300, 200, 320, 64), (128, 256, 64, 128), (257, 520, 4096, 256),
+                                      (1, 96, 128, 256), (2048, 4096, 4096, 256)])
+@pytest.mark.parametrize("out", [torch.float32, torch.bfloat16])
+def test_gemm_tcgen05(ops, m, n, k, bn, out):
+    rng = np.random.default_rng(m * 7 + n + k)
+    a, A = bf16_rand(rng, (m, k))
+    b, B = bf16_rand(rng, (n, k), 1.0 / np.sqrt(k))
+    got = ops.gemm(A, B, out, bn).float().cpu().numpy()
+    ref = a @ b.T
+    assert rel_err(got, ref) < (1e-5 if out == torch.float32 else 8e-3)
+
+
+@pytest.mark.parametrize("m,n,k,splits,bn", [(640, 37, 1024, 1, 64), (640, 37, 1024, 3, 64), (4096, 128, 4096, 5, 128),
+                                             (6144, 200, 4096, 2, 256), (250, 3, 192, 8, 64)])
+def test_gemm_swap_splitk(ops, m, n, k, splits, bn):
+    rng = np.random.default_rng(m + n * 3 + splits)
+    w, W = bf16_rand(rng, (m, k), 1.0 / np.sqrt(k))
+    x, X = bf16_rand(rng, (n, k))
+    got = ops.gemm_swap(W, X, splits, bn).cpu().numpy()
+    assert rel_err(got, x @ w.T) < 1e-5
+
+
+@pytest.mark.parametrize("V,n,k", [(1000, 5, 256), (32000, 64, 1024), (4097, 130, 512)])
+def test_lm_argmax(ops, V, n, k):
+    rng = np.random.default_rng(V + n)
+    w, W = bf16_rand(rng, (V, k), 2.0 / np.sqrt(k))
+    x, X = bf16_rand(rng, (n, k))
+    got = ops.lm_argmax(W, X).cpu().numpy()
+    logits = x @ w.T
+    for i in range(n):
+        ref = T.greedy(logits[i])
+        if T.top2_margin(logits[i]) > 1e-3:
+            assert got[i] == ref
+        else:
+            assert logits[i][got[i]] >= logits[i][ref] - 1e-3
+
+
+def test_lm_argmax_ties_lowest_index(ops):
+    rng = np.random.default_rng(3)
+    w, W = bf16_rand(rng, (700, 128))
+    W[650] = W[17]   # exact duplicate rows -> exactly tied logits
+    W[300] = W[17]
+    x, X = bf16_rand(rng, (4, 128))
+    X[:] = W[17]     # make row 17's logit the maximum (|w17|^2)
+    got = ops.lm_argmax(W, X).cpu().numpy()
+    assert (got == 17).all()
+
+
+@pytest.mark.parametrize("n,H", [(1, 256), (37, 4096), (5, 8192)])
+def test_rmsnorm(ops, n, H):
+    rng = np.random.default_rng(H)
+    x = (rng.standard_normal((n, H)) * 3).astype(np.float32)
+    g_bits = f32_to_bf16_bits((1 + rng.uniform(-0.1, 0.1, H)).astype(np.float32))
+    g = bf16_bits_to_f32(g_bits).astype(np.float64)
+    got = ops.rmsnorm(torch.from_numpy(x).cuda(), torch.from_numpy(g_bits.view(np.int16)).cuda().view(torch.bfloat16),
+                      1e-5).float().cpu().numpy()
+    ref = T.rmsnorm(x.astype(np.float64), g, 1e-5)
+    assert rel_err(got, ref) < 8e-3
+
+
+def make_pool(rng, n_blocks, n_kv, D):
+    """single-layer pool [blk][2][Mkv][64][D] with random bf16 K/V"""
+    host, dev = bf16_rand(rng, (n_blocks, 2, n_kv, 64, D))
+    return host, dev.reshape(-1)
+
+
+@pytest.mark.parametrize("D,M,Mkv", [(32, 8, 2), (128, 8, 2), (128, 32, 8), (64, 4, 4)])
+def test_attention_prefill(ops, D, M, Mkv):
+    rng = np.random.default_rng(D + M)
+    lens = [1, 63, 64, 65, 200, 130]
+    nb = [(s + 63) // 64 for s in lens]
+    n_blocks = sum(nb) + 3
+    pool_h, pool_d = make_pool(rng, n_blocks, Mkv, D)
+    perm = rng.permutation(n_blocks)
+    bt = np.zeros((len(lens), max(nb)), dtype=np.int32)
+    k = 0
+    for i, b in enumerate(nb):
+        bt[i, :b] = perm[k:k + b]
+        k += b
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    q_h, q_d = bf16_rand(rng, (cu[-1], M, D))
+    got = ops.attention_prefill(q_d, pool_d, n_blocks, M, Mkv, D, cu, torch.from_numpy(bt).cuda()).float().cpu().numpy()
+    for i, S in enumerate(lens):
+        ks = np.stack([pool_h[bt[i, t // 64], 0, :, t % 64, :] for t in range(S)])
+        vs = np.stack([pool_h[bt[i, t // 64], 1, :, t % 64, :] for t in range(S)])
+        ref = T.attention(q_h[cu[i]:cu[i + 1]], ks, vs, np.arange(S), np.arange(S)).reshape(S, M * D)
+        assert rel_err(got[cu[i]:cu[i + 1]], ref) < 1e-2, (i, S)
+
+
+@pytest.mark.parametrize("D,M,Mkv,splits,bps", [(128, 32, 8, 1, 64), (128, 32, 8, 4, 5), (32, 8, 2, 3, 7),
+                                                 (128, 64, 8, 2, 9), (64, 4, 4, 1, 64)])
+def test_attention_decode(ops, D, M, Mkv, splits, bps):
+    rng = np.random.default_rng(D * 3 + splits)
+    ctx = [1, 64, 65, 300, 1000][: 5]
+    if splits * bps * 64 < max(ctx):
+        ctx = [c for c in ctx if c <= splits * bps * 64]
+    nb = [(c + 63) // 64 for c in ctx]
+    n_blocks = sum(nb) + 2
+    pool_h, pool_d = make_pool(rng, n_blocks, Mkv, D)
+    perm = rng.permutation(n_blocks)
+    bt = np.zeros((len(ctx), max(nb)), dtype=np.int32)
+    k = 0
+    for i, b in enumerate(nb):
+        bt[i, :b] = perm[k:k + b]
+        k += b
+    q_h, q_d = bf16_rand(rng, (len(ctx), M, D))
+    got = ops.attention_decode(q_d, pool_d, M, Mkv, D, torch.tensor(ctx, dtype=torch.int32).cuda(),
+                               torch.from_numpy(bt).cuda(), splits, bps).float().cpu().numpy()
+    for i, c in enumerate(ctx):
+        ks = np.stack([pool_h[bt[i, t // 64], 0, :, t % 64, :] for t in range(c)])
+        vs = np.stack([pool_h[bt[i, t // 64], 1, :, t % 64, :] for t in range(c)])
+        ref = T.attention(q_h[i:i + 1], ks, vs, np.array([c - 1]), np.arange(c)).reshape(M * D)
+        assert rel_err(got[i], ref) < 1e-2, (i, c)
