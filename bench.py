@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""Benchmark of the PaDG instance hot path on B200 (BASELINE.json configs[1]).
+
+One step = one PaDG cycle of one instance per GPU (temporal disaggregation,
+PAPER.md Sec. 3.2.1), i.e. every row of SURVEY 8(a) on the GPU side:
+  * prefill phase: 8 new requests, prompts U{512..2048} (configs[1]), routed by
+    the host macro scheduler (Alg. 1/2) and prefilled in one <= 16384-token batch;
+  * decode phase: 16 decode steps over the running set of 128 requests;
+  * the 8 oldest requests leave (continuous batching keeps B = 128).
+Metric: tokens/s (prompt tokens prefilled + tokens decoded) of the whole job.
+Weights are random-init Llama-3-8B-shape bf16 (synthetic); inputs are larger
+than L2 (16 GB of weights stream every decode step), so no L2 flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Under torchrun each rank runs one independent instance (weak scaling, no data
+path collective: PaDG instances share nothing but host-side control).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "prefill/decode tokens/s per B200; goodput req/s at TTFT/TPOT SLO, 1-8 GPU"
+N_NEW, B_RUN, DEC_STEPS = 8, 128, 16
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev, self.rows, self.proc = dev, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU oracle sample
+def oracle_sample(prefill_len: int = 1024, n_dec: int = 8, dec_ctx: int = 1024, dec_steps: int = 2, seed: int = 0):
+    """Time the fp64 oracle on ONE decoder layer of the 8B shape (bounded sample),
+    extrapolated linearly to the model's 32 layers (embed / LM head excluded).
+    Returns (prefill tok/s, decode tok/s, seconds spent, threads)."""
+    from oracle.transformer import ContiguousKV, Model
+    from synthetic.shapes import get_shape
+    from synthetic.weights import LAYER_TENSORS, _draw, _rng, bf16_bits_to_f32, f32_to_bf16_bits, layer_shapes
+    full = get_shape("8b")
+    shape = full.with_layers(1)
+    shp = layer_shapes(shape)
+    layer = {n: bf16_bits_to_f32(f32_to_bf16_bits(_draw(n, shp[n], _rng(seed, 0, i), shape.hidden))).astype(np.float64)
+             for i, n in enumerate(LAYER_TENSORS)}
+    m = Model(shape, {"layers": [layer]})
+    rng = np.random.default_rng(seed)
+    t0 = time.perf_counter()
+    x = rng.standard_normal((prefill_len, shape.hidden))
+    kv = ContiguousKV.empty(1, shape.n_kv_heads, shape.head_dim)
+    m.layer(0, x, np.arange(prefill_len), kv)
+    t_pre = time.perf_counter() - t0
+    kvs = []
+    for _ in range(n_dec):
+        c = ContiguousKV.empty(1, shape.n_kv_heads, shape.head_dim)
+        c.append(0, rng.standard_normal((dec_ctx, shape.n_kv_heads, shape.head_dim)),
+                 rng.standard_normal((dec_ctx, shape.n_kv_heads, shape.head_dim)))
+        kvs.append(c)
+    t1 = time.perf_counter()
+    for s in range(dec_steps):
+        for c in kvs:
+            m.layer(0, rng.standard_normal((1, shape.hidden)), np.array([dec_ctx + s]), c)
+    t_dec = time.perf_counter() - t1
+    L = full.n_layers
+    threads = len(os.sched_getaffinity(0))
+    return prefill_len / (t_pre * L), n_dec * dec_steps / (t_dec * L), t_pre + t_dec, threads
+
+
+def mix_rate(pre_rate: float, dec_rate: float, pre_tok: float, dec_tok: float) -> float:
+    """tokens/s of a step with the GPU step's token mix, from per-phase rates."""
+    return (pre_tok + dec_tok) / (pre_tok / pre_rate + dec_tok / dec_rate)
+
+
+def run_reference(args, rank: int, world: int):
+    """--impl reference: the oracle as it stands on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    pre_tok, dec_tok = N_NEW * 1280.0, float(B_RUN * DEC_STEPS)
+    times, rates = [], []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        pr, dr, _, thr = oracle_sample(prefill_len=512, n_dec=4, dec_ctx=1024, dec_steps=1, seed=i)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+            rates.append(mix_rate(pr, dr, pre_tok, dec_tok))
+    v = float(np.mean(rates))
+    sample = "1 layer of the 8B shape: prefill 1x512 tokens + decode 4 seqs x 1 step at ctx 1024, fp64 NumPy, " \
+             "extrapolated x32 layers, mixed at the GPU step's prefill/decode token ratio"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "8b-padg-cycle (oracle sample)", "shape": "llama3-8b", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": len(os.sched_getaffinity(0)),
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_gpu(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+    from paper_2504_18154_b200 import build as B
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if rank == 0:
+        B.build(verbose=False)
+    if world > 1:
+        dist.barrier()
+    from paper_2504_18154_b200.instance import Instance, random_device_weights
+    from paper_2504_18154_b200.macro import MacroScheduler, SchedConfig
+    from synthetic.shapes import get_shape
+    from synthetic.traces import make_trace
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    shape = get_shape(args.shape)
+    weights = random_device_weights(shape, seed=1000 + rank, device=dev)
+    stream = torch.cuda.Stream(dev)
+    n_blocks = 6000
+    inst = Instance(shape, weights, n_blocks, local_rank, token_budget=16384, max_batch=256, max_positions=8192,
+                    stream=stream.cuda_stream, free_raw_after_create=True)
+    torch.cuda.empty_cache()
+    # the host macro scheduler of this instance (Alg. 1/2; ShareGPT SLOs)
+    sched = MacroScheduler(SchedConfig(1, 5_000_000_000, 100_000_000, 512, [n_blocks]))
+    n_total = B_RUN + (args.warmup + args.steps) * N_NEW
+    trace = make_trace("8b-cycle", n_total, seed=1 + rank, vocab=shape.vocab)
+    MAX_NEW = 4096   # never reached inside the bench: requests leave by continuous batching
+    t_origin = time.perf_counter_ns()
+
+    def now():
+        return time.perf_counter_ns() - t_origin
+
+    def admit(reqs):
+        for r in reqs:
+            sched.route(r.req_id, now(), r.prompt_len, now())
+        return inst.prefill([(r.req_id, r.prompt, MAX_NEW) for r in reqs])
+
+    # fill the running set (untimed)
+    running = [r.req_id for r in trace[:B_RUN]]
+    for i in range(0, B_RUN, 32):
+        admit(trace[i:i + 32])
+    nxt = B_RUN
+    stats = {"prefill_tokens": 0, "decode_tokens": 0}
+
+    def step():
+        nonlocal nxt, running
+        new = trace[nxt:nxt + N_NEW]
+        nxt += N_NEW
+        admit(new)                                   # prefill phase
+        old, running = running[:N_NEW], running[N_NEW:] + [r.req_id for r in new]
+        inst.release(old)                            # the oldest leave
+        toks, _ = inst.decode(running, DEC_STEPS)    # decode phase
+        st, rs = inst.status()
+        sched.update_status(0, 2, now(), st["blocks_total"],
+                            [(r["req_id"], 0, r["prompt_len"], 0, r["n_generated"], r["finished"]) for r in rs])
+        stats["prefill_tokens"] += sum(r.prompt_len for r in new)
+        stats["decode_tokens"] += len(running) * DEC_STEPS
+
+    for _ in range(args.warmup):
+        step()
+    inst.set_profiling(2)
+    inst.timing(reset=True)
+    stats = {"prefill_tokens": 0, "decode_tokens": 0}
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    if world > 1:
+        dist.barrier()
+    tm = inst.timing(reset=True)
+    dev_ms = tm["prefill_ms"] + tm["decode_ms"]
+    tokens = stats["prefill_tokens"] + stats["decode_tokens"]
+    # max over ranks of the times, sum over ranks of the work
+    vec = torch.tensor([dev_ms, wall, float(tokens), float(stats["prefill_tokens"]), float(stats["decode_tokens"]),
+                        tm["prefill_ms"], tm["decode_ms"]], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = vec.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vec.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    else:
+        mx = sm = vec
+    if rank == 0:
+        P, src = peaks()
+        dev_ms_max, wall_max = float(mx[0]), float(mx[1])
+        tot_tokens = float(sm[2])
+        classes = {
+            "gemm_prefill": (tm["gemm_prefill_ms"], tm["gemm_prefill_flop"], tm["gemm_prefill_launches"], "tensor"),
+            "gemm_decode": (tm["gemm_decode_ms"], tm["gemm_decode_bytes"], tm["gemm_decode_launches"], "hbm"),
+            "attn_prefill": (tm["attn_prefill_ms"], tm["attn_prefill_flop"], tm["attn_prefill_launches"], "tensor"),
+            "attn_decode": (tm["attn_decode_ms"], tm["attn_decode_bytes"], tm["attn_decode_launches"], "hbm"),
+        }
+        breakdown = {}
+        for k, (ms, work, n, bound) in classes.items():
+            if ms <= 0:
+                continue
+            if bound == "tensor":
+                ach, peak, unit = work / (ms * 1e-3) / 1e12, P["bf16_tflops_sustained"], "TFLOP/s"
+            else:
+                ach, peak, unit = work / (ms * 1e-3) / 1e9, P["hbm_gbs"], "GB/s"
+            breakdown[k] = {"bound": bound, "achieved": round(ach, 2), "peak": peak, "unit": unit,
+                            "frac": round(ach / peak, 4), "share_of_step": round(ms / dev_ms, 4),
+                            "launches": n, "avg_launch_us": round(1e3 * ms / max(n, 1), 2)}
+        dom = max(breakdown, key=lambda k: breakdown[k]["share_of_step"])
+        traffic = None
+        tfile = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tfile):
+            traffic = json.load(open(tfile)).get(dom)
+        roof = dict(breakdown[dom])
+        roof.update({"kernel": dom, "traffic": traffic, "peak_source": src +
+                     (" sustained bf16 (kernel timed inside a long step)" if roof["bound"] == "tensor" else " HBM copy")})
+        steps = args.steps
+        line = {
+            "metric": METRIC, "value": round(tot_tokens / (dev_ms_max * 1e-3), 1), "unit": "tokens/s",
+            "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": round(dev_ms_max / steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "8b-padg-cycle", "shape": "llama3-8b (L32 H4096 M32 Mkv8 F14336 V128256)",
+                       "prefill_per_step": f"{N_NEW} new requests, prompts U{{512..2048}}",
+                       "decode_per_step": f"{DEC_STEPS} steps x B={B_RUN}", "token_budget": 16384,
+                       "l2": "inputs larger than L2 (16 GB weights streamed per decode step); no flush",
+                       "parallelism": f"{world} independent PaDG instances (1 per GPU)"},
+            "prefill_tok_s": round(float(sm[3]) / (float(mx[5]) * 1e-3), 1) if float(mx[5]) > 0 else None,
+            "decode_tok_s": round(float(sm[4]) / (float(mx[6]) * 1e-3), 1) if float(mx[6]) > 0 else None,
+            "e2e": {"value": round(tot_tokens / wall_max, 1), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(tm.get("h2d_bytes", 0) // steps),
+                    "d2h_bytes_per_step": int(tm.get("d2h_bytes", 0) // steps)},
+            "gpu_launches": int(tm["launches"]),
+            "roofline": roof, "roofline_breakdown": breakdown, "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            pr, dr, secs, thr = oracle_sample()
+            v = mix_rate(pr, dr, float(sm[3]), float(sm[4]))
+            line["cpu_baseline"] = {
+                "value": round(v, 3), "unit": "tokens/s", "cores": thr, "kind": "oracle",
+                "sample": "1 layer of the 8B shape: prefill 1x1024 tokens + decode 8 seqs x 2 steps at ctx 1024, "
+                          "fp64 NumPy, extrapolated x32 layers, mixed at this run's prefill/decode token ratio "
+                          f"({secs:.1f} s of CPU work)"}
+        print(json.dumps(line), flush=True)
+    inst.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--shape", default="8b")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_gpu(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -160,6 +160,28 @@ ecoserve_status ecoserve_get_status(const ecoserve_instance* inst, ecoserve_inst
  * (decode, last step). */
 ecoserve_status ecoserve_debug_hidden(ecoserve_instance* inst, int64_t req_id, int32_t layer, float* out);
 
+/* Device-side timing of the phase work, measured with CUDA events on the
+ * instance stream: a phase interval starts after its inputs are resident in HBM
+ * (after the host->device copy) and ends before the device->host token copy.
+ * With profiling level 2 every kernel launch is also bracketed by events and
+ * accumulated per kernel class with its algorithmic work. */
+typedef struct {
+  double prefill_ms, decode_ms;
+  int64_t prefill_tokens, decode_tokens;
+  int64_t launches;                          /* kernels launched by the phases */
+  /* level 2 only */
+  double gemm_prefill_ms, gemm_prefill_flop; int64_t gemm_prefill_launches;
+  double gemm_decode_ms, gemm_decode_bytes;  int64_t gemm_decode_launches; /* weight bytes streamed */
+  double attn_prefill_ms, attn_prefill_flop; int64_t attn_prefill_launches;
+  double attn_decode_ms, attn_decode_bytes;  int64_t attn_decode_launches;  /* KV bytes read */
+  double other_ms;                           int64_t other_launches;
+  int64_t h2d_bytes, d2h_bytes;              /* host<->device bytes the phases copied */
+} ecoserve_timing;
+
+/* level 0 off, 1 phase intervals (default), 2 + per-kernel-class events */
+ecoserve_status ecoserve_set_profiling(ecoserve_instance* inst, int32_t level);
+ecoserve_status ecoserve_get_timing(ecoserve_instance* inst, ecoserve_timing* out, int32_t reset);
+
 void ecoserve_instance_destroy(ecoserve_instance* inst);
 const char* ecoserve_last_error(const ecoserve_instance* inst);
 

@@ -57,6 +57,21 @@ class ReqStatus(C.Structure):
                 ("finished", C.c_int32), ("n_blocks", C.c_int32)]
 
 
+class Timing(C.Structure):
+    _fields_ = [("prefill_ms", C.c_double), ("decode_ms", C.c_double), ("prefill_tokens", C.c_int64),
+                ("decode_tokens", C.c_int64), ("launches", C.c_int64),
+                ("gemm_prefill_ms", C.c_double), ("gemm_prefill_flop", C.c_double), ("gemm_prefill_launches", C.c_int64),
+                ("gemm_decode_ms", C.c_double), ("gemm_decode_bytes", C.c_double), ("gemm_decode_launches", C.c_int64),
+                ("attn_prefill_ms", C.c_double), ("attn_prefill_flop", C.c_double),
+                ("attn_prefill_launches", C.c_int64),
+                ("attn_decode_ms", C.c_double), ("attn_decode_bytes", C.c_double), ("attn_decode_launches", C.c_int64),
+                ("other_ms", C.c_double), ("other_launches", C.c_int64), ("h2d_bytes", C.c_int64),
+                ("d2h_bytes", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class MacroConfig(C.Structure):
     _fields_ = [("n_instances", C.c_int32), ("slo_ttft_ns", C.c_int64), ("slo_tpot_ns", C.c_int64),
                 ("reserve_tokens", C.c_int32), ("block_tokens", C.c_int32), ("probe_printed", C.c_int32),
@@ -103,6 +118,8 @@ SIGNATURES = {
     "ecoserve_release": (C.c_int, [P, PI64, I32]),
     "ecoserve_get_status": (C.c_int, [P, C.POINTER(InstanceStatus), C.POINTER(ReqStatus), I32]),
     "ecoserve_debug_hidden": (C.c_int, [P, I64, I32, PF32]),
+    "ecoserve_set_profiling": (C.c_int, [P, I32]),
+    "ecoserve_get_timing": (C.c_int, [P, C.POINTER(Timing), I32]),
     "ecoserve_instance_destroy": (None, [P]),
     "ecoserve_last_error": (C.c_char_p, [P]),
     "ecoserve_macro_create": (C.c_int, [C.POINTER(MacroConfig), C.POINTER(P)]),

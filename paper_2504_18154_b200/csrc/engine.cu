@@ -55,6 +55,68 @@ struct LayerW {
 int bn_index(int bn) { return bn == 64 ? 0 : bn == 128 ? 1 : 2; }
 int pick_bn(int rows) { return rows <= 64 ? 64 : rows <= 128 ? 128 : 256; }
 
+// CUDA-event profiler on the instance stream (ecoserve_get_timing).
+enum ProfClass { P_PREFILL = 0, P_DECODE, P_GEMM_PREFILL, P_GEMM_DECODE, P_ATTN_PREFILL, P_ATTN_DECODE, P_OTHER, P_N };
+
+struct Prof {
+  int level = 1;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  struct Mark {
+    cudaEvent_t a, b;
+    int cls;
+    double work;
+  };
+  std::vector<Mark> marks;
+  double ms[P_N] = {0}, work[P_N] = {0};
+  int64_t count[P_N] = {0};
+  int64_t tokens[2] = {0, 0};
+  int64_t launches = 0;
+  int64_t h2d = 0, d2h = 0;
+
+  cudaEvent_t get() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  // returns the mark index or -1
+  int begin(int cls, cudaStream_t s) {
+    if (level == 0 || (cls >= P_GEMM_PREFILL && level < 2)) return -1;
+    Mark m{get(), get(), cls, 0.0};
+    if (!m.a || !m.b) return -1;
+    cudaEventRecord(m.a, s);
+    marks.push_back(m);
+    return (int)marks.size() - 1;
+  }
+  void end(int idx, double w, cudaStream_t s) {
+    if (idx < 0) return;
+    marks[idx].work = w;
+    cudaEventRecord(marks[idx].b, s);
+  }
+  // after a stream sync
+  void resolve() {
+    for (auto& m : marks) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, m.a, m.b) == cudaSuccess) {
+        ms[m.cls] += t;
+        work[m.cls] += m.work;
+        count[m.cls] += 1;
+      }
+    }
+    marks.clear();
+    used = 0;
+  }
+  void reset() {
+    for (int i = 0; i < P_N; ++i) ms[i] = work[i] = 0, count[i] = 0;
+    tokens[0] = tokens[1] = 0;
+    launches = 0;
+    h2d = d2h = 0;
+  }
+};
+
 }  // namespace
 
 struct ecoserve_instance {
@@ -102,6 +164,7 @@ struct ecoserve_instance {
   float* dbg = nullptr;          // [(L+1)][T_max][H]
   std::unordered_map<int64_t, std::pair<int, int>> dbg_rows;  // req -> (row0, nrows) of the last phase call
   std::unordered_map<int64_t, Req> reqs;
+  Prof prof;
 
   bool fail(const char* what, cudaError_t e) {
     err = std::string(what) + ": " + cudaGetErrorString(e);
@@ -117,6 +180,15 @@ struct ecoserve_instance {
       inst->fail(#expr, _e);                                      \
       return ECOSERVE_ERR_CUDA;                                   \
     }                                                             \
+  } while (0)
+
+// launch `expr` (which launches `nk` kernels) under profiler class `cls` with algorithmic work `w`
+#define LAUNCH(cls, w, nk, expr)                                  \
+  do {                                                            \
+    const int _m = inst->prof.begin((cls), inst->stream);         \
+    CK(expr);                                                     \
+    inst->prof.end(_m, (w), inst->stream);                        \
+    inst->prof.launches += (nk);                                  \
   } while (0)
 
 static bool shape_ok(const ecoserve_model_shape* s) {
@@ -163,6 +235,7 @@ void ecoserve_instance_destroy(ecoserve_instance* inst) {
     if (p) cudaFree(p);
   if (inst->h_meta) cudaFreeHost(inst->h_meta);
   if (inst->h_tokens) cudaFreeHost(inst->h_tokens);
+  for (cudaEvent_t e : inst->prof.pool) cudaEventDestroy(e);
   if (inst->own_stream && inst->stream) cudaStreamDestroy(inst->stream);
   delete inst;
 }
@@ -378,22 +451,23 @@ cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const 
 
 static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const int* d_ids, const int* d_pos,
                                           const int* d_slot, const int* d_cu, const int* d_bt, int bt_ld,
-                                          const int* d_tiles, int n_tiles) {
+                                          const int* d_tiles, int n_tiles, double attn_flop) {
   cudaStream_t st = inst->stream;
   const int L = inst->L, H = inst->H, M = inst->M, D = inst->D, F = inst->F;
   const float eps = inst->shape.rms_eps;
-  CK(embed_launch(d_ids, inst->embed, inst->x, T, H, st));
+  LAUNCH(P_OTHER, 0, 1, embed_launch(d_ids, inst->embed, inst->x, T, H, st));
   if (inst->debug) CK(cudaMemcpyAsync(inst->dbg, inst->x, sizeof(float) * (int64_t)T * H, cudaMemcpyDeviceToDevice, st));
   for (int l = 0; l < L; ++l) {
     LayerW& w = inst->lw[l];
-    CK(rmsnorm_launch(inst->x, H, nullptr, w.attn_norm, inst->h, T, H, eps, st));
+    LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.attn_norm, inst->h, T, H, eps, st));
     GemmEpi e = epi_base(inst);
     e.mode = EPI_QKV;
     e.pos = d_pos;
     e.slot = d_slot;
     e.k_cache = k_layer(inst, l);
     e.v_cache = v_layer(inst, l);
-    CK(gemm_launch(&inst->m_h.a, &w.qkv_b, T, inst->QKV, H, BN_PREFILL, 1, e, inst->num_sms, st));
+    LAUNCH(P_GEMM_PREFILL, 2.0 * T * inst->QKV * H, 1,
+           gemm_launch(&inst->m_h.a, &w.qkv_b, T, inst->QKV, H, BN_PREFILL, 1, e, inst->num_sms, st));
     PrefillAttnArgs a;
     a.q = inst->q;
     a.k_cache = k_layer(inst, l);
@@ -408,23 +482,26 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
     a.n_heads = M;
     a.n_kv = inst->Mkv;
     a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
-    CK(attn_prefill_launch(a, D, st));
+    LAUNCH(P_ATTN_PREFILL, attn_flop, 1, attn_prefill_launch(a, D, st));
     GemmEpi eo = epi_base(inst);
     eo.mode = EPI_RESID;
     eo.resid = inst->x;
     eo.ldr = H;
-    CK(gemm_launch(&inst->m_ao.a, &w.o_b, T, H, M * D, BN_PREFILL, 1, eo, inst->num_sms, st));
-    CK(rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, T, H, eps, st));
+    LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * M * D, 1,
+           gemm_launch(&inst->m_ao.a, &w.o_b, T, H, M * D, BN_PREFILL, 1, eo, inst->num_sms, st));
+    LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, T, H, eps, st));
     GemmEpi eg = epi_base(inst);
     eg.mode = EPI_SILU;
     eg.out = inst->act;
     eg.ldo = F;
-    CK(gemm_launch(&inst->m_h.a, &w.gu_b, T, 2 * F, H, BN_PREFILL, 1, eg, inst->num_sms, st));
+    LAUNCH(P_GEMM_PREFILL, 2.0 * T * 2 * F * H, 1,
+           gemm_launch(&inst->m_h.a, &w.gu_b, T, 2 * F, H, BN_PREFILL, 1, eg, inst->num_sms, st));
     GemmEpi ed = epi_base(inst);
     ed.mode = EPI_RESID;
     ed.resid = inst->x;
     ed.ldr = H;
-    CK(gemm_launch(&inst->m_act.a, &w.d_b, T, H, F, BN_PREFILL, 1, ed, inst->num_sms, st));
+    LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * F, 1,
+           gemm_launch(&inst->m_act.a, &w.d_b, T, H, F, BN_PREFILL, 1, ed, inst->num_sms, st));
     if (inst->debug)
       CK(cudaMemcpyAsync(inst->dbg + (int64_t)(l + 1) * inst->T_max * H, inst->x, sizeof(float) * (int64_t)T * H,
                          cudaMemcpyDeviceToDevice, st));
@@ -434,11 +511,11 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
 
 static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const int* d_ids, const int* d_pos,
                                          const int* d_slot, const int* d_ctx, const int* d_bt, int bt_ld,
-                                         int max_blocks) {
+                                         int max_blocks, double kv_bytes) {
   cudaStream_t st = inst->stream;
   const int L = inst->L, H = inst->H, M = inst->M, D = inst->D, F = inst->F;
   const float eps = inst->shape.rms_eps;
-  CK(embed_launch(d_ids, inst->embed, inst->x, B, H, st));
+  LAUNCH(P_OTHER, 0, 1, embed_launch(d_ids, inst->embed, inst->x, B, H, st));
   if (inst->debug) CK(cudaMemcpyAsync(inst->dbg, inst->x, sizeof(float) * (int64_t)B * H, cudaMemcpyDeviceToDevice, st));
   // split the context so that B x Mkv x splits fills the SMs about twice
   int n_splits = std::max(1, (2 * inst->num_sms + B * inst->Mkv - 1) / (B * inst->Mkv));
@@ -448,13 +525,13 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
   if ((int64_t)B * M * n_splits * (D + 2) > inst->attn_ws_elems) return ECOSERVE_ERR_INVALID_ARG;
   for (int l = 0; l < L; ++l) {
     LayerW& w = inst->lw[l];
-    CK(rmsnorm_launch(inst->x, H, nullptr, w.attn_norm, inst->h, B, H, eps, st));
+    LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.attn_norm, inst->h, B, H, eps, st));
     GemmEpi e = epi_base(inst);
     e.pos = d_pos;
     e.slot = d_slot;
     e.k_cache = k_layer(inst, l);
     e.v_cache = v_layer(inst, l);
-    CK(decode_gemm(inst, w.qkv_a, inst->m_h, inst->QKV, H, B, RED_QKV, e));
+    LAUNCH(P_GEMM_DECODE, 2.0 * inst->QKV * H, 2, decode_gemm(inst, w.qkv_a, inst->m_h, inst->QKV, H, B, RED_QKV, e));
     DecodeAttnArgs a;
     a.q = inst->q;
     a.k_cache = k_layer(inst, l);
@@ -472,20 +549,20 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     a.part_ml = inst->attn_ws + (int64_t)B * M * n_splits * D;
     a.out = inst->ao;
     a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
-    CK(attn_decode_launch(a, D, st));
+    LAUNCH(P_ATTN_DECODE, kv_bytes, n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
     GemmEpi eo = epi_base(inst);
     eo.resid = inst->x;
     eo.ldr = H;
-    CK(decode_gemm(inst, w.o_a, inst->m_ao, H, M * D, B, RED_RESID, eo));
-    CK(rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, B, H, eps, st));
+    LAUNCH(P_GEMM_DECODE, 2.0 * H * M * D, 2, decode_gemm(inst, w.o_a, inst->m_ao, H, M * D, B, RED_RESID, eo));
+    LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, B, H, eps, st));
     GemmEpi eg = epi_base(inst);
     eg.out = inst->act;
     eg.ldo = F;
-    CK(decode_gemm(inst, w.gu_a, inst->m_h, 2 * F, H, B, RED_SILU, eg));
+    LAUNCH(P_GEMM_DECODE, 2.0 * 2 * F * H, 2, decode_gemm(inst, w.gu_a, inst->m_h, 2 * F, H, B, RED_SILU, eg));
     GemmEpi ed = epi_base(inst);
     ed.resid = inst->x;
     ed.ldr = H;
-    CK(decode_gemm(inst, w.d_a, inst->m_act, H, F, B, RED_RESID, ed));
+    LAUNCH(P_GEMM_DECODE, 2.0 * H * F, 2, decode_gemm(inst, w.d_a, inst->m_act, H, F, B, RED_RESID, ed));
     if (inst->debug)
       CK(cudaMemcpyAsync(inst->dbg + (int64_t)(l + 1) * inst->T_max * H, inst->x, sizeof(float) * (int64_t)B * H,
                          cudaMemcpyDeviceToDevice, st));
@@ -494,10 +571,10 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
 }
 
 // final RMSNorm of the selected rows + LM head + greedy argmax -> h_tokens[0..n)
-static ecoserve_status lm_head_argmax(ecoserve_instance* inst, const int* d_rows, int n) {
+static ecoserve_status lm_head_argmax(ecoserve_instance* inst, const int* d_rows, int n, int gemm_cls) {
   cudaStream_t st = inst->stream;
   const int H = inst->H;
-  CK(rmsnorm_launch(inst->x, H, d_rows, inst->final_norm, inst->hl, n, H, inst->shape.rms_eps, st));
+  LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, d_rows, inst->final_norm, inst->hl, n, H, inst->shape.rms_eps, st));
   GemmEpi e;
   memset(&e, 0, sizeof(e));
   e.mode = EPI_SWAP_ARGMAX;
@@ -505,9 +582,10 @@ static ecoserve_status lm_head_argmax(ecoserve_instance* inst, const int* d_rows
   e.am_idx = inst->am_idx;
   e.am_ld = inst->am_ld;
   const int bn = pick_bn(n);
-  CK(gemm_launch(&inst->lm_a, &inst->m_hl.b[bn_index(bn)], inst->V, n, H, bn, 1, e, inst->num_sms, st));
-  CK(argmax_reduce_launch(inst->am_val, inst->am_idx, n, inst->am_ld, inst->am_ld, inst->d_tokens, inst->d_nan, st));
-  CK(cudaMemcpyAsync(inst->h_tokens, inst->d_tokens, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+  LAUNCH(gemm_cls, gemm_cls == P_GEMM_DECODE ? 2.0 * inst->V * H : 2.0 * inst->V * H * n, 1,
+         gemm_launch(&inst->lm_a, &inst->m_hl.b[bn_index(bn)], inst->V, n, H, bn, 1, e, inst->num_sms, st));
+  LAUNCH(P_OTHER, 0, 1,
+         argmax_reduce_launch(inst->am_val, inst->am_idx, n, inst->am_ld, inst->am_ld, inst->d_tokens, inst->d_nan, st));
   return ECOSERVE_OK;
 }
 
@@ -612,12 +690,21 @@ ecoserve_status ecoserve_prefill_phase(ecoserve_instance* inst, const ecoserve_r
     cudaStream_t st = inst->stream;
     CK(cudaMemcpyAsync(inst->d_meta, hm, sizeof(int) * used, cudaMemcpyHostToDevice, st));
     int* d = inst->d_meta;
+    double attn_flop = 0;  // causal QK^T + PV: 2 * 2 * M * D * S(S+1)/2 per sequence
+    for (int i = i0; i < i1; ++i) attn_flop += 2.0 * inst->M * inst->D * (double)rs[i]->S * (rs[i]->S + 1);
+    const int pm = inst->prof.begin(P_PREFILL, st);
     ecoserve_status s = run_layers_prefill(inst, tok, d, d + (pos - hm), d + (slot - hm), d + (cu - hm),
-                                           d + (bt - hm), bt_ld, d + (tl - hm), (int)tiles.size());
+                                           d + (bt - hm), bt_ld, d + (tl - hm), (int)tiles.size(), attn_flop);
     if (s != ECOSERVE_OK) return s;
-    s = lm_head_argmax(inst, d + (rows - hm), ns);
+    s = lm_head_argmax(inst, d + (rows - hm), ns, P_OTHER);
     if (s != ECOSERVE_OK) return s;
+    inst->prof.end(pm, tok, st);
+    CK(cudaMemcpyAsync(inst->h_tokens, inst->d_tokens, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    inst->prof.resolve();
+    inst->prof.tokens[0] += tok;
+    inst->prof.h2d += sizeof(int) * used;
+    inst->prof.d2h += sizeof(int) * ns;
     for (int i = i0; i < i1; ++i) {
       Req* r = rs[i];
       r->last_token = inst->h_tokens[i - i0];
@@ -697,12 +784,22 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
     cudaStream_t st = inst->stream;
     CK(cudaMemcpyAsync(inst->d_meta, hm, sizeof(int) * used, cudaMemcpyHostToDevice, st));
     int* d = inst->d_meta;
-    ecoserve_status es =
-        run_layers_decode(inst, B, d, d + (pos - hm), d + (slot - hm), d + (ctx - hm), d + (bt - hm), bt_ld, max_blocks);
+    double kv_tokens = 0;
+    for (int k = 0; k < B; ++k) kv_tokens += ctx[k];
+    const double kv_bytes = kv_tokens * 2.0 * inst->Mkv * inst->D * 2.0;  // K and V, one layer
+    const int pm = inst->prof.begin(P_DECODE, st);
+    ecoserve_status es = run_layers_decode(inst, B, d, d + (pos - hm), d + (slot - hm), d + (ctx - hm), d + (bt - hm),
+                                           bt_ld, max_blocks, kv_bytes);
     if (es != ECOSERVE_OK) return es;
-    es = lm_head_argmax(inst, d + (rows - hm), B);
+    es = lm_head_argmax(inst, d + (rows - hm), B, P_GEMM_DECODE);
     if (es != ECOSERVE_OK) return es;
+    inst->prof.end(pm, B, st);
+    CK(cudaMemcpyAsync(inst->h_tokens, inst->d_tokens, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    inst->prof.resolve();
+    inst->prof.tokens[1] += B;
+    inst->prof.h2d += sizeof(int) * used;
+    inst->prof.d2h += sizeof(int) * B;
     for (int k = 0; k < B; ++k) {
       Req* r = rs[live[k]];
       r->last_token = inst->h_tokens[k];
@@ -716,6 +813,41 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
     for (int i = 0; i < n; ++i) c += rs[i]->finished ? 1 : 0;
     *n_finished = c;
   }
+  return ECOSERVE_OK;
+}
+
+ecoserve_status ecoserve_set_profiling(ecoserve_instance* inst, int32_t level) {
+  if (!inst || level < 0 || level > 2) return ECOSERVE_ERR_INVALID_ARG;
+  inst->prof.level = level;
+  return ECOSERVE_OK;
+}
+
+ecoserve_status ecoserve_get_timing(ecoserve_instance* inst, ecoserve_timing* out, int32_t reset) {
+  if (!inst || !out) return ECOSERVE_ERR_INVALID_ARG;
+  const Prof& p = inst->prof;
+  memset(out, 0, sizeof(*out));
+  out->prefill_ms = p.ms[P_PREFILL];
+  out->decode_ms = p.ms[P_DECODE];
+  out->prefill_tokens = p.tokens[0];
+  out->decode_tokens = p.tokens[1];
+  out->launches = p.launches;
+  out->gemm_prefill_ms = p.ms[P_GEMM_PREFILL];
+  out->gemm_prefill_flop = p.work[P_GEMM_PREFILL];
+  out->gemm_prefill_launches = p.count[P_GEMM_PREFILL];
+  out->gemm_decode_ms = p.ms[P_GEMM_DECODE];
+  out->gemm_decode_bytes = p.work[P_GEMM_DECODE];
+  out->gemm_decode_launches = p.count[P_GEMM_DECODE];
+  out->attn_prefill_ms = p.ms[P_ATTN_PREFILL];
+  out->attn_prefill_flop = p.work[P_ATTN_PREFILL];
+  out->attn_prefill_launches = p.count[P_ATTN_PREFILL];
+  out->attn_decode_ms = p.ms[P_ATTN_DECODE];
+  out->attn_decode_bytes = p.work[P_ATTN_DECODE];
+  out->attn_decode_launches = p.count[P_ATTN_DECODE];
+  out->other_ms = p.ms[P_OTHER];
+  out->other_launches = p.count[P_OTHER];
+  out->h2d_bytes = p.h2d;
+  out->d2h_bytes = p.d2h;
+  if (reset) inst->prof.reset();
   return ECOSERVE_OK;
 }
 

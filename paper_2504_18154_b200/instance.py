@@ -64,7 +64,7 @@ class Instance:
 
     def __init__(self, shape, weights: Dict, num_blocks: int, device: int = 0, token_budget: int = 16384,
                  max_batch: int = 512, max_positions: int = 16384, debug_hidden: bool = False,
-                 free_raw_after_create: bool = False):
+                 free_raw_after_create: bool = False, stream: Optional[int] = None):
         self.lib = L.load()
         self.shape = shape
         self.device = torch.device("cuda", device)
@@ -88,7 +88,8 @@ class Instance:
         h = C.c_void_p()
         torch.cuda.set_device(self.device)
         L.check(self.lib.ecoserve_instance_create(C.byref(self.cshape), C.byref(self.ckv), C.byref(self.cw),
-                                                  C.c_void_p(self.prepared.data_ptr()), device, 0, None, None,
+                                                  C.c_void_p(self.prepared.data_ptr()), device, 0, None,
+                                                  C.c_void_p(stream) if stream else None,
                                                   C.byref(self.cfg), C.byref(h)))
         self.h = h
         if free_raw_after_create:  # wq/wk/wv/w_gate/w_up were copied into the prepared buffer
@@ -142,6 +143,14 @@ class Instance:
                      finished=bool(r.finished), n_blocks=r.n_blocks) for r in rs[:min(cap, st.n_requests)]]
         return dict(alive=bool(st.alive), n_requests=st.n_requests, blocks_total=st.blocks_total,
                     blocks_used=st.blocks_used), reqs
+
+    def set_profiling(self, level: int) -> None:
+        L.check(self.lib.ecoserve_set_profiling(self.h, level), self.h)
+
+    def timing(self, reset: bool = False) -> Dict:
+        t = L.Timing()
+        L.check(self.lib.ecoserve_get_timing(self.h, C.byref(t), 1 if reset else 0), self.h)
+        return t.as_dict()
 
     def hidden(self, req_id: int, layer: int, rows: int) -> np.ndarray:
         out = np.zeros((rows, self.shape.hidden), dtype=np.float32)
