@@ -15,7 +15,8 @@ extern "C" {
 
 /* D = A B^T on tcgen05 (Table 2 projections). A [m][k], B [n][k] bf16
  * row-major, k % 64 == 0 is not required (TMA zero-fills). out_mode 0: out f32
- * [m][n]; 1: out bf16 [m][n]. bn in {64, 128, 256}. */
+ * [m][n]; 1: out bf16 [m][n]. bn in {64, 128, 256}: one CTA per 128 x bn tile;
+ * bn = 2: the CTA-pair (cta_group::2) kernel with 256 x 256 tiles. */
 ecoserve_status ecoserve_op_gemm(const void* A, const void* B, int32_t m, int32_t n, int32_t k, int32_t out_mode,
                                  void* out, int32_t bn, void* stream);
 
@@ -24,6 +25,14 @@ ecoserve_status ecoserve_op_gemm(const void* A, const void* B, int32_t m, int32_
  * caller's workspace f32 [splits][n][m], then a fixed-order reduction. */
 ecoserve_status ecoserve_op_gemm_swap(const void* W, const void* X, int32_t m, int32_t n, int32_t k, int32_t splits,
                                       float* workspace, float* out, int32_t bn, void* stream);
+
+/* The decode-phase form of the same GEMM: in-kernel split-K reduction (the last
+ * CTA of each tile sums the f32 partials of all splits in split order) and an
+ * in-kernel epilogue writing out bf16 [n][m]. part: f32 [splits][n][m];
+ * counters: int32 [ceil(m/128) * ceil(n/bn)], zero on entry, zero on return. */
+ecoserve_status ecoserve_op_gemm_swap_bf16(const void* W, const void* X, int32_t m, int32_t n, int32_t k,
+                                           int32_t splits, float* part, int32_t* counters, void* out, int32_t bn,
+                                           void* stream);
 
 /* Greedy LM head (rows a12/a16): tokens[i] = argmax_v (X [n][k] W[v][k]^T), lowest
  * v on ties, logits never materialised. workspace: f32 [n][ceil(V/128)] and

@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "launch.cuh"
 
 namespace eco {
 
@@ -53,6 +54,8 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(PrefillAttnArgs a) {
   bf16* sQ = reinterpret_cast<bf16*>(sm);
   bf16* sK = sQ + 64 * D;  // [2][64][D]
   bf16* sV = sK + 2 * 64 * D;
+  pdl_trigger();
+  pdl_wait();
 
   const int tile = blockIdx.x, h = blockIdx.y;
   const int seq = a.tiles[2 * tile], q_start = a.tiles[2 * tile + 1];
@@ -217,6 +220,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a) {
   bf16* sV = sK + DEC_STAGES * 64 * D;
   bf16* sQ = sV + DEC_STAGES * 64 * D;                     // [16][D]
   float* red = reinterpret_cast<float*>(sm);               // reused after the main loop
+  pdl_trigger();
+  pdl_wait();
 
   const int b = blockIdx.x, kvh = blockIdx.y, split = blockIdx.z;
   const int G = a.n_heads / a.n_kv;
@@ -381,6 +386,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a) {
 
 template <int D>
 __global__ void attn_combine_kernel(DecodeAttnArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x, h = blockIdx.y;
   const int64_t p0 = ((int64_t)b * a.n_heads + h) * a.n_splits;
   float M = -INFINITY;
@@ -408,8 +415,7 @@ static cudaError_t prefill_d(const PrefillAttnArgs& a, cudaStream_t s) {
     cfg = true;
   }
   if (a.n_tiles == 0) return cudaSuccess;
-  attn_prefill_kernel<D><<<dim3(a.n_tiles, a.n_heads), 128, smem, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(attn_prefill_kernel<D>, dim3(a.n_tiles, a.n_heads), dim3(128), smem, s, a);
 }
 
 cudaError_t attn_prefill_launch(const PrefillAttnArgs& a, int head_dim, cudaStream_t s) {
@@ -434,11 +440,9 @@ static cudaError_t decode_d(const DecodeAttnArgs& a, cudaStream_t s) {
   }
   if (a.B == 0) return cudaSuccess;
   if (a.n_heads / a.n_kv > 16) return cudaErrorInvalidValue;
-  attn_decode_kernel<D><<<dim3(a.B, a.n_kv, a.n_splits), 128, smem, s>>>(a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(attn_decode_kernel<D>, dim3(a.B, a.n_kv, a.n_splits), dim3(128), smem, s, a);
   if (e != cudaSuccess || a.n_splits == 1) return e;
-  attn_combine_kernel<D><<<dim3(a.B, a.n_heads), D, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(attn_combine_kernel<D>, dim3(a.B, a.n_heads), dim3(D), 0, s, a);
 }
 
 cudaError_t attn_decode_launch(const DecodeAttnArgs& a, int head_dim, cudaStream_t s) {

@@ -149,6 +149,7 @@ struct ecoserve_instance {
   ActMaps m_h, m_ao, m_act, m_hl;
   float* part = nullptr;         // split-K partials
   int64_t part_elems = 0;
+  int* counters = nullptr;       // split-K tile arrival counters
   float* attn_ws = nullptr;      // decode attention partials
   int64_t attn_ws_elems = 0;
   float* am_val = nullptr;
@@ -229,7 +230,8 @@ void ecoserve_instance_destroy(ecoserve_instance* inst) {
   if (!inst) return;
   cudaSetDevice(inst->device);
   if (inst->stream) cudaStreamSynchronize(inst->stream);
-  void* dev[] = {inst->x, inst->h, inst->q, inst->ao, inst->act, inst->hl, inst->part, inst->attn_ws, inst->am_val,
+  void* dev[] = {inst->x, inst->h, inst->q, inst->ao, inst->act, inst->hl, inst->part, inst->counters, inst->attn_ws,
+                 inst->am_val,
                  inst->am_idx, inst->d_tokens, inst->d_nan, inst->rope_cos, inst->rope_sin, inst->d_meta, inst->dbg};
   for (void* p : dev)
     if (p) cudaFree(p);
@@ -367,6 +369,8 @@ ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, cons
   const int nmax = std::max(QKV, std::max(2 * F, H));
   inst->part_elems = 8LL * inst->B_max * nmax;
   CK(cudaMalloc(&inst->part, sizeof(float) * inst->part_elems));
+  CK(cudaMalloc(&inst->counters, sizeof(int) * 16384));
+  CK(cudaMemsetAsync(inst->counters, 0, sizeof(int) * 16384, st));
   const int max_blocks_seq = (inst->P_max + BLOCK - 1) / BLOCK;
   inst->attn_ws_elems = (int64_t)inst->B_max * M * 64 * (D + 2);
   CK(cudaMalloc(&inst->attn_ws, sizeof(float) * inst->attn_ws_elems));
@@ -418,6 +422,7 @@ GemmEpi epi_base(ecoserve_instance* inst) {
   memset(&e, 0, sizeof(e));
   e.rope_cos = inst->rope_cos;
   e.rope_sin = inst->rope_sin;
+  e.indep = 2;  // prefill: the weights are the B operand
   e.n_heads = inst->M;
   e.n_kv = inst->Mkv;
   e.head_dim = inst->D;
@@ -429,22 +434,46 @@ GemmEpi epi_base(ecoserve_instance* inst) {
 bf16* k_layer(ecoserve_instance* inst, int l) { return inst->pool + (int64_t)l * 2 * inst->Mkv * BLOCK * inst->D; }
 bf16* v_layer(ecoserve_instance* inst, int l) { return k_layer(inst, l) + (int64_t)inst->Mkv * BLOCK * inst->D; }
 
-// Skinny decode GEMM: part = W x^T split-K, then the fixed-order reduce + epilogue.
+// Prefill projection: CTA-pair 256 x 256 tiles (cta_group::2) unless ECOSERVE_GEMM2=0,
+// then the 1-CTA 128 x 256 kernel. w128 / w256: the weight's tensor maps with 128 / 256-row boxes.
+bool use_gemm2() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_GEMM2");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+cudaError_t prefill_gemm(ecoserve_instance* inst, const CUtensorMap& amap, const CUtensorMap& w128,
+                         const CUtensorMap& w256, int T, int N, int K, const GemmEpi& e) {
+  if (use_gemm2()) return gemm2_launch(&amap, &w128, T, N, K, e, inst->num_sms, inst->stream);
+  return gemm_launch(&amap, &w256, T, N, K, BN_PREFILL, 1, e, inst->num_sms, inst->stream);
+}
+
+// Skinny decode GEMM (swap-AB): weights on the MMA M side, the B tokens on N, K split so
+// the grid fills the SMs; the epilogue (and the split reduction) run inside the kernel.
 cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const ActMaps& xm, int n_out, int K, int B,
-                        int red_mode, GemmEpi e) {
-  const int bn = pick_bn(B);
-  const int m_tiles = (n_out + 127) / 128, n_tiles = (B + bn - 1) / bn;
-  int splits = (inst->num_sms + m_tiles * n_tiles - 1) / (m_tiles * n_tiles);
-  splits = std::min(splits, 8);
-  splits = gemm_effective_splits(K, splits);
-  GemmEpi ge;
-  memset(&ge, 0, sizeof(ge));
+                        int mode, GemmEpi e, int* nk) {
+  const int bn = B <= 64 ? 64 : 128;  // B > 128: several 128-token tiles; weight re-reads hit L2
+  const int splits = gemm_decode_splits(n_out, K, inst->num_sms);
+  e.indep = 1;  // weights (A) prefetch before the PDL wait
+  if (splits == 1) {  // epilogue in the GEMM
+    e.mode = mode;
+    *nk = 1;
+    return gemm_launch(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, 1, e, inst->num_sms, inst->stream);
+  }
+  // split-K: f32 partials, then one fixed-order reduction kernel applying the epilogue
+  GemmEpi ge = e;
   ge.mode = EPI_SWAP_F32;
   ge.out = inst->part;
   ge.ldo = n_out;
   cudaError_t r = gemm_launch(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, splits, ge, inst->num_sms, inst->stream);
   if (r != cudaSuccess) return r;
-  return splitk_reduce_launch(red_mode, inst->part, splits, B, n_out, n_out, e, inst->stream);
+  const int red = mode == EPI_SWAP_QKV ? RED_QKV : mode == EPI_SWAP_SILU ? RED_SILU
+                : mode == EPI_SWAP_RESID ? RED_RESID : RED_BF16;
+  *nk = 2;
+  return splitk_reduce_launch(red, inst->part, splits, B, n_out, n_out, e, inst->stream);
 }
 
 }  // namespace
@@ -467,7 +496,7 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
     e.k_cache = k_layer(inst, l);
     e.v_cache = v_layer(inst, l);
     LAUNCH(P_GEMM_PREFILL, 2.0 * T * inst->QKV * H, 1,
-           gemm_launch(&inst->m_h.a, &w.qkv_b, T, inst->QKV, H, BN_PREFILL, 1, e, inst->num_sms, st));
+           prefill_gemm(inst, inst->m_h.a, w.qkv_a, w.qkv_b, T, inst->QKV, H, e));
     PrefillAttnArgs a;
     a.q = inst->q;
     a.k_cache = k_layer(inst, l);
@@ -488,20 +517,20 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
     eo.resid = inst->x;
     eo.ldr = H;
     LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * M * D, 1,
-           gemm_launch(&inst->m_ao.a, &w.o_b, T, H, M * D, BN_PREFILL, 1, eo, inst->num_sms, st));
+           prefill_gemm(inst, inst->m_ao.a, w.o_a, w.o_b, T, H, M * D, eo));
     LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, T, H, eps, st));
     GemmEpi eg = epi_base(inst);
     eg.mode = EPI_SILU;
     eg.out = inst->act;
     eg.ldo = F;
     LAUNCH(P_GEMM_PREFILL, 2.0 * T * 2 * F * H, 1,
-           gemm_launch(&inst->m_h.a, &w.gu_b, T, 2 * F, H, BN_PREFILL, 1, eg, inst->num_sms, st));
+           prefill_gemm(inst, inst->m_h.a, w.gu_a, w.gu_b, T, 2 * F, H, eg));
     GemmEpi ed = epi_base(inst);
     ed.mode = EPI_RESID;
     ed.resid = inst->x;
     ed.ldr = H;
     LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * F, 1,
-           gemm_launch(&inst->m_act.a, &w.d_b, T, H, F, BN_PREFILL, 1, ed, inst->num_sms, st));
+           prefill_gemm(inst, inst->m_act.a, w.d_a, w.d_b, T, H, F, ed));
     if (inst->debug)
       CK(cudaMemcpyAsync(inst->dbg + (int64_t)(l + 1) * inst->T_max * H, inst->x, sizeof(float) * (int64_t)T * H,
                          cudaMemcpyDeviceToDevice, st));
@@ -531,7 +560,9 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     e.slot = d_slot;
     e.k_cache = k_layer(inst, l);
     e.v_cache = v_layer(inst, l);
-    LAUNCH(P_GEMM_DECODE, 2.0 * inst->QKV * H, 2, decode_gemm(inst, w.qkv_a, inst->m_h, inst->QKV, H, B, RED_QKV, e));
+    int nk = 0;
+    LAUNCH(P_GEMM_DECODE, 2.0 * inst->QKV * H, nk,
+           decode_gemm(inst, w.qkv_a, inst->m_h, inst->QKV, H, B, EPI_SWAP_QKV, e, &nk));
     DecodeAttnArgs a;
     a.q = inst->q;
     a.k_cache = k_layer(inst, l);
@@ -553,16 +584,18 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     GemmEpi eo = epi_base(inst);
     eo.resid = inst->x;
     eo.ldr = H;
-    LAUNCH(P_GEMM_DECODE, 2.0 * H * M * D, 2, decode_gemm(inst, w.o_a, inst->m_ao, H, M * D, B, RED_RESID, eo));
+    LAUNCH(P_GEMM_DECODE, 2.0 * H * M * D, nk,
+           decode_gemm(inst, w.o_a, inst->m_ao, H, M * D, B, EPI_SWAP_RESID, eo, &nk));
     LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, B, H, eps, st));
     GemmEpi eg = epi_base(inst);
     eg.out = inst->act;
     eg.ldo = F;
-    LAUNCH(P_GEMM_DECODE, 2.0 * 2 * F * H, 2, decode_gemm(inst, w.gu_a, inst->m_h, 2 * F, H, B, RED_SILU, eg));
+    LAUNCH(P_GEMM_DECODE, 2.0 * 2 * F * H, nk,
+           decode_gemm(inst, w.gu_a, inst->m_h, 2 * F, H, B, EPI_SWAP_SILU, eg, &nk));
     GemmEpi ed = epi_base(inst);
     ed.resid = inst->x;
     ed.ldr = H;
-    LAUNCH(P_GEMM_DECODE, 2.0 * H * F, 2, decode_gemm(inst, w.d_a, inst->m_act, H, F, B, RED_RESID, ed));
+    LAUNCH(P_GEMM_DECODE, 2.0 * H * F, nk, decode_gemm(inst, w.d_a, inst->m_act, H, F, B, EPI_SWAP_RESID, ed, &nk));
     if (inst->debug)
       CK(cudaMemcpyAsync(inst->dbg + (int64_t)(l + 1) * inst->T_max * H, inst->x, sizeof(float) * (int64_t)B * H,
                          cudaMemcpyDeviceToDevice, st));
@@ -578,6 +611,7 @@ static ecoserve_status lm_head_argmax(ecoserve_instance* inst, const int* d_rows
   GemmEpi e;
   memset(&e, 0, sizeof(e));
   e.mode = EPI_SWAP_ARGMAX;
+  e.indep = 1;
   e.am_val = inst->am_val;
   e.am_idx = inst->am_idx;
   e.am_ld = inst->am_ld;

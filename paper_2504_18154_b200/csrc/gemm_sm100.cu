@@ -15,6 +15,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "launch.cuh"
 
 namespace eco {
 
@@ -97,8 +98,15 @@ __device__ __forceinline__ void epi_rows(const GemmEpi& e, int m, int n0, int n_
         const bool is_q = n0 < qd;
         const int head = is_q ? n0 / D : (n0 - qd) / D;
         const int j0 = (n0 % D) / 2;  // pair index of f[0]
-        const float* cs = e.rope_cos + (int64_t)p * half + j0;
-        const float* sn = e.rope_sin + (int64_t)p * half + j0;
+        const float4* cs4 = reinterpret_cast<const float4*>(e.rope_cos + (int64_t)p * half + j0);
+        const float4* sn4 = reinterpret_cast<const float4*>(e.rope_sin + (int64_t)p * half + j0);
+        float cs[16], sn[16];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 c = __ldg(cs4 + q4), s = __ldg(sn4 + q4);
+          cs[4 * q4] = c.x; cs[4 * q4 + 1] = c.y; cs[4 * q4 + 2] = c.z; cs[4 * q4 + 3] = c.w;
+          sn[4 * q4] = s.x; sn[4 * q4 + 1] = s.y; sn[4 * q4 + 2] = s.z; sn[4 * q4 + 3] = s.w;
+        }
         uint32_t lo[8], hi[8];
 #pragma unroll
         for (int j = 0; j < 16; j += 2) {
@@ -134,6 +142,74 @@ __device__ __forceinline__ void epi_rows(const GemmEpi& e, int m, int n0, int n_
   }
 }
 
+// Swapped (decode) epilogue: this thread owns feature `m` (TMEM lane), tokens n0..n0+31
+// in f[]. Pair-interleaved rows (RoPE, SiLU) sit in adjacent lanes: exchange by shuffle,
+// so every lane executes the shuffles before any bounds check.
+__device__ __forceinline__ void epi_swap(const GemmEpi& e, int m, int m_rows, int n0, int n_rows, int lane,
+                                         const float (&f)[32]) {
+  const bool mv = m < m_rows;
+  const int ncols = min(32, n_rows - n0);
+  switch (e.mode) {
+    case EPI_SWAP_BF16: {
+      bf16* o = reinterpret_cast<bf16*>(e.out);
+      if (mv)
+        for (int i = 0; i < ncols; ++i) o[(int64_t)(n0 + i) * e.ldo + m] = __float2bfloat16_rn(f[i]);
+    } break;
+    case EPI_SWAP_RESID: {
+      if (mv)
+        for (int i = 0; i < ncols; ++i) e.resid[(int64_t)(n0 + i) * e.ldr + m] += f[i];
+    } break;
+    case EPI_SWAP_SILU: {
+      bf16* o = reinterpret_cast<bf16*>(e.out);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float up = __shfl_xor_sync(0xffffffffu, f[i], 1);
+        if (mv && !(lane & 1) && i < ncols) o[(int64_t)(n0 + i) * e.ldo + m / 2] = __float2bfloat16_rn(silu_f(f[i]) * up);
+      }
+    } break;
+    case EPI_SWAP_QKV: {
+      const int D = e.head_dim, half = D / 2;
+      const int qd = e.n_heads * D, kd = e.n_kv * D;
+      const bool odd = lane & 1;
+      if (m < qd + kd) {  // warp-uniform: 32 rows never straddle the q/k | v boundary (D % 32 == 0)
+        const bool is_q = m < qd;
+        const int head = is_q ? m / D : (m - qd) / D;
+        const int j = (m % D) / 2;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float other = __shfl_xor_sync(0xffffffffu, f[i], 1);
+          if (mv && i < ncols) {
+            const int n = n0 + i;
+            const int p = e.pos[n];
+            const float c = e.rope_cos[(int64_t)p * half + j], s = e.rope_sin[(int64_t)p * half + j];
+            // even lane holds x_j (a), odd lane holds x_{j+D/2} (b)
+            const float a = odd ? other : f[i], b = odd ? f[i] : other;
+            const float y = odd ? (b * c + a * s) : (a * c - b * s);
+            bf16* dst;
+            if (is_q) {
+              dst = e.q_out + ((int64_t)n * e.n_heads + head) * D;
+            } else {
+              const int sl = e.slot[n];
+              dst = e.k_cache + (int64_t)(sl >> 6) * e.blk_stride + ((int64_t)head * 64 + (sl & 63)) * D;
+            }
+            dst[odd ? j + half : j] = __float2bfloat16_rn(y);
+          }
+        }
+      } else if (mv) {
+        const int c = m - qd - kd;
+        const int head = c / D, d = c % D;
+        for (int i = 0; i < ncols; ++i) {
+          const int sl = e.slot[n0 + i];
+          e.v_cache[(int64_t)(sl >> 6) * e.blk_stride + ((int64_t)head * 64 + (sl & 63)) * D + d] =
+              __float2bfloat16_rn(f[i]);
+        }
+      }
+    } break;
+    default:
+      break;
+  }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int m_rows,
@@ -148,6 +224,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint32_t* tmem_base_ptr = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   __shared__ float am_v[4][BN];
   __shared__ int am_i[4][BN];
+  __shared__ int s_last;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int m_tiles = (m_rows + BM - 1) / BM;
@@ -176,26 +253,59 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_ptr;
+  // prologue done (smem, barriers, TMEM, descriptor prefetch): let the next kernel launch.
+  // Threads wait for the previous kernel (PDL) right before their first dependent access.
+  pdl_trigger();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-        const int ks = w % splits;
-        const int t = w / splits;
-        const int mt = t / n_tiles, nt = t % n_tiles;
-        const int kb0 = ks * kb_per, kb1 = min(kb_total, kb0 + kb_per);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
+      // iteration cursor over this CTA's (work unit, K block) sequence
+      int w = blockIdx.x, kb = -1, kb1 = 0, mt = 0, nt = 0;
+      auto next = [&]() -> bool {
+        if (kb >= 0 && kb + 1 < kb1) { ++kb; return true; }
+        if (kb >= 0) w += gridDim.x;
+        if (w >= n_work) return false;
+        const int ks = w % splits, t = w / splits;
+        mt = t / n_tiles;
+        nt = t % n_tiles;
+        kb = ks * kb_per;
+        kb1 = min(kb_total, kb + kb_per);
+        return true;
+      };
+      // 1) the operand that does not depend on the previous kernel (the weights) is
+      //    streamed into the first stages before the PDL wait
+      int pre_mt[8], pre_nt[8], pre_kb[8], npre = 0;
+      const int indep = epi.indep;
+      if (indep != 0) {
+        while (npre < C::STAGES && next()) {
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
-          uint8_t* sb = sa + C::A_BYTES;
           mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
-          tma_load_2d(sa, &mapA, &full_bar[stage], kb * BK, mt * BM);
-          tma_load_2d(sb, &mapB, &full_bar[stage], kb * BK, nt * BN);
+          if (indep == 1) tma_load_2d(sa, &mapA, &full_bar[stage], kb * BK, mt * BM);
+          else tma_load_2d(sa + C::A_BYTES, &mapB, &full_bar[stage], kb * BK, nt * BN);
+          pre_mt[npre] = mt; pre_nt[npre] = nt; pre_kb[npre] = kb;
+          ++npre;
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
+      }
+      pdl_wait();
+      // 2) their dependent operand
+      for (int i = 0; i < npre; ++i) {
+        uint8_t* sa = smem + i * C::STAGE_BYTES;
+        if (indep == 1) tma_load_2d(sa + C::A_BYTES, &mapB, &full_bar[i], pre_kb[i] * BK, pre_nt[i] * BN);
+        else tma_load_2d(sa, &mapA, &full_bar[i], pre_kb[i] * BK, pre_mt[i] * BM);
+      }
+      // 3) steady state
+      while (next()) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * C::STAGE_BYTES;
+        uint8_t* sb = sa + C::A_BYTES;
+        mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+        tma_load_2d(sa, &mapA, &full_bar[stage], kb * BK, mt * BM);
+        tma_load_2d(sb, &mapB, &full_bar[stage], kb * BK, nt * BN);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -232,6 +342,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
+    pdl_wait();              // the epilogue reads/writes buffers of the previous kernels
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int ep_tid = (warp - 2) * 32 + lane;
     int acc = 0;
@@ -301,6 +412,68 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      } else if (epi.mode >= EPI_SWAP_BF16) {
+        if (splits == 1) {
+          for (int c0 = 0; c0 < BN; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(tbase + c0, v);
+            tc_wait_ld();
+            float f[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+            epi_swap(epi, m, m_rows, nt * BN + c0, n_rows, lane, f);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+        } else {
+          // 1) this split's partial -> workspace (coalesced over the lanes = features)
+          const int64_t plane = (int64_t)n_rows * m_rows;
+          float* mine = epi.part + (int64_t)ks * plane;
+          for (int c0 = 0; c0 < BN; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(tbase + c0, v);
+            tc_wait_ld();
+            if (m < m_rows) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const int n = nt * BN + c0 + i;
+                if (n < n_rows) mine[(int64_t)n * m_rows + m] = __uint_as_float(v[i]);
+              }
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+          // 2) the last CTA to finish a split of this tile reduces all splits in split order
+          __threadfence();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (ep_tid == 0) {
+            const int old = atomicAdd(&epi.counters[t], 1);
+            s_last = (old == splits - 1) ? 1 : 0;
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (s_last) {
+            __threadfence();
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+              float f[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) f[i] = 0.f;
+              if (m < m_rows) {
+                for (int s = 0; s < splits; ++s) {
+                  const float* ps = epi.part + (int64_t)s * plane;
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) {
+                    const int n = nt * BN + c0 + i;
+                    if (n < n_rows) f[i] += __ldcg(ps + (int64_t)n * m_rows + m);
+                  }
+                }
+              }
+              epi_swap(epi, m, m_rows, nt * BN + c0, n_rows, lane, f);
+            }
+            if (ep_tid == 0) epi.counters[t] = 0;
+          }
+        }
       } else {
         for (int c0 = 0; c0 < BN; c0 += 32) {
           uint32_t v[32];
@@ -323,6 +496,189 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     __syncwarp();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
+}
+
+// ---------------------------------------------------------------- CTA-pair GEMM
+// cta_group::2 variant for the prefill projections: a cluster of 2 CTAs computes a
+// 256 x 256 tile with one tcgen05.mma.cta_group::2 M=256 N=256 per 16-wide K step,
+// issued by the even CTA. CTA r stages A rows [r*128, r*128+128) and B rows
+// [r*128, r*128+128) of the tile (half the B traffic of a 1-CTA 128 x 256 tile per
+// SM) and owns accumulator rows r*128.. in its TMEM (2 x 256 columns, double buffered).
+// TMA completions land on the even CTA's full barriers; MMA completions are
+// multicast to both CTAs' empty / tmem-full barriers; both CTAs' epilogues release
+// the accumulator on the even CTA's tmem-empty barrier.
+struct Gemm2Cfg {
+  static constexpr int BN = 256;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = 6;
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int m_rows,
+                    int n_rows, int K, GemmEpi epi) {
+  using C = Gemm2Cfg;
+  constexpr int BN = C::BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + C::STAGES;
+  uint64_t* tfull_bar = empty_bar + C::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_base_ptr = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int rank = (int)cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+  const int m_tiles = (m_rows + 2 * BM - 1) / (2 * BM);
+  const int n_tiles = (n_rows + BN - 1) / BN;
+  const int kb_total = (K + BK - 1) / BK;
+  const int n_work = m_tiles * n_tiles;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapB);
+  }
+  if (warp == 1) tmem_alloc2(tmem_base_ptr, C::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_ptr;
+  pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int w = cid, kb = -1, mt = 0, nt = 0;
+      auto next = [&]() -> bool {
+        if (kb >= 0 && kb + 1 < kb_total) { ++kb; return true; }
+        if (kb >= 0) w += ncl;
+        if (w >= n_work) return false;
+        mt = w / n_tiles;
+        nt = w % n_tiles;
+        kb = 0;
+        return true;
+      };
+      const int arow = rank * BM, brow = rank * (BN / 2);
+      int pre_mt[C::STAGES], pre_nt[C::STAGES], pre_kb[C::STAGES], npre = 0;
+      const int indep = epi.indep;
+      if (indep != 0) {
+        while (npre < C::STAGES && next()) {
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
+          if (indep == 1) tma_load_2d_pair(sa, &mapA, &full_bar[stage], kb * BK, mt * 2 * BM + arow);
+          else tma_load_2d_pair(sa + C::A_BYTES, &mapB, &full_bar[stage], kb * BK, nt * BN + brow);
+          pre_mt[npre] = mt; pre_nt[npre] = nt; pre_kb[npre] = kb;
+          ++npre;
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+      pdl_wait();
+      for (int i = 0; i < npre; ++i) {
+        uint8_t* sa = smem + i * C::STAGE_BYTES;
+        if (indep == 1) tma_load_2d_pair(sa + C::A_BYTES, &mapB, &full_bar[i], pre_kb[i] * BK, pre_nt[i] * BN + brow);
+        else tma_load_2d_pair(sa, &mapA, &full_bar[i], pre_kb[i] * BK, pre_mt[i] * 2 * BM + arow);
+      }
+      while (next()) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * C::STAGE_BYTES;
+        if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
+        tma_load_2d_pair(sa, &mapA, &full_bar[stage], kb * BK, mt * 2 * BM + arow);
+        tma_load_2d_pair(sa + C::A_BYTES, &mapB, &full_bar[stage], kb * BK, nt * BN + brow);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int w = cid; w < n_work; w += ncl) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kb_total; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + C::A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            tc_mma_f16_pair(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          tc_commit_pair(&empty_bar[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit_pair(&tfull_bar[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    pdl_wait();
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int w = cid; w < n_work; w += ncl) {
+      const int mt = w / n_tiles, nt = w % n_tiles;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int m = mt * 2 * BM + rank * BM + q * 32 + lane;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(tbase + c0, v);
+        tc_wait_ld();
+        const int n0 = nt * BN + c0;
+        if (m < m_rows && n0 < n_rows) epi_rows(epi, m, n0, n_rows, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_peer0(&tempty_bar[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 1) {
+    __syncwarp();
+    tmem_dealloc2(tmem_base, C::TMEM_COLS);
+  }
+}
+
+cudaError_t gemm2_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K,
+                         const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+  if (epi.mode >= EPI_SWAP_F32) return cudaErrorInvalidValue;  // prefill (non-swapped) epilogues only
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int work = ((m_rows + 255) / 256) * ((n_rows + 255) / 256);
+  int clusters = num_sms / 2;
+  if (work < clusters) clusters = work;
+  if (clusters <= 0) return cudaSuccess;
+  return launch_k(gemm_tc2_kernel, dim3(2 * clusters), dim3(GEMM_THREADS), Gemm2Cfg::SMEM, stream, *mapA, *mapB,
+                  m_rows, n_rows, K, epi);
 }
 
 // ---------------------------------------------------------------- host side
@@ -360,6 +716,34 @@ int gemm_effective_splits(int K, int splits) {
   return (kb_total + kb_per - 1) / kb_per;
 }
 
+int gemm_choose_splits(int m_rows, int n_rows, int K, int bn, int num_sms, int max_splits) {
+  const int tiles = ((m_rows + BM - 1) / BM) * ((n_rows + bn - 1) / bn);
+  const int kb_total = (K + BK - 1) / BK;
+  int best = 1;
+  double best_cost = 1e30;
+  for (int s = 1; s <= max_splits; ++s) {
+    const int eff = gemm_effective_splits(K, s);
+    if (eff != s && s > 1) continue;
+    const int kb_per = (kb_total + eff - 1) / eff;
+    const int waves = (tiles * eff + num_sms - 1) / num_sms;
+    // K blocks streamed by the busiest CTA, plus ~1 block-equivalent per split for the reduction
+    const double cost = (double)waves * kb_per + (eff > 1 ? 0.5 * eff : 0.0);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = eff;
+    }
+  }
+  return best;
+}
+
+int gemm_decode_splits(int m_rows, int K, int num_sms) {
+  const int tiles = (m_rows + BM - 1) / BM;
+  if (4 * tiles >= 3 * num_sms) return 1;
+  int s = (num_sms + tiles / 2) / tiles;
+  s = s < 2 ? 2 : s > 4 ? 4 : s;
+  return gemm_effective_splits(K, s);
+}
+
 int gemm_smem_bytes(int bn) {
   switch (bn) {
     case 64: return GemmCfg<64>::SMEM;
@@ -382,13 +766,15 @@ static cudaError_t launch_bn(const CUtensorMap* mapA, const CUtensorMap* mapB, i
   const int work = m_tiles * n_tiles * splits;
   const int grid = work < num_sms ? work : num_sms;
   if (grid <= 0) return cudaSuccess;
-  gemm_tc_kernel<BN><<<grid, GEMM_THREADS, GemmCfg<BN>::SMEM, stream>>>(*mapA, *mapB, m_rows, n_rows, K, splits, epi);
-  return cudaGetLastError();
+  return launch_k(gemm_tc_kernel<BN>, dim3(grid), dim3(GEMM_THREADS), GemmCfg<BN>::SMEM, stream, *mapA, *mapB, m_rows,
+                  n_rows, K, splits, epi);
 }
 
 cudaError_t gemm_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K, int bn,
                         int splits, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
-  if (splits < 1 || (splits > 1 && epi.mode != EPI_SWAP_F32)) return cudaErrorInvalidValue;
+  if (splits < 1) return cudaErrorInvalidValue;
+  if (splits > 1 && epi.mode != EPI_SWAP_F32 && epi.mode < EPI_SWAP_BF16) return cudaErrorInvalidValue;
+  if (splits > 1 && epi.mode >= EPI_SWAP_BF16 && (!epi.part || !epi.counters)) return cudaErrorInvalidValue;
   splits = gemm_effective_splits(K, splits);
   switch (bn) {
     case 64: return launch_bn<64>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);

@@ -22,6 +22,13 @@ enum EpiMode : int {
   EPI_QKV = 4,          // RoPE on pair-interleaved q/k heads, q -> q_out, k/v -> paged pool
   EPI_SWAP_F32 = 5,     // out f32 [split][n][ldo] (ldo = padded m), partial sums of a K split
   EPI_SWAP_ARGMAX = 6,  // per token n, per 128-row m tile: (max, lowest argmax) -> am_val/am_idx [n][am_ld]
+  // swapped (decode) epilogues applied in-kernel; with splits > 1 every split writes
+  // its f32 partial to `part` and the last-arriving CTA of a tile (per-tile counter)
+  // sums the partials in split order (deterministic) and applies the epilogue
+  EPI_SWAP_BF16 = 7,    // out bf16 [n][ldo] at m
+  EPI_SWAP_RESID = 8,   // resid f32 [n][ldr] at m += acc
+  EPI_SWAP_SILU = 9,    // out bf16 [n][ldo] at m/2: silu(acc[m even]) * acc[m + 1]
+  EPI_SWAP_QKV = 10,    // RoPE on pair-interleaved q/k rows (lanes 2j, 2j+1), KV to the pool
 };
 
 struct GemmEpi {
@@ -44,7 +51,19 @@ struct GemmEpi {
   float* am_val;
   int* am_idx;
   int am_ld;
+  // split-K workspace of the in-kernel reduction (swapped modes 7..10)
+  float* part;             // [splits][n_rows][m_rows] f32
+  int* counters;           // [m_tiles * n_tiles], zero on entry, left zero on exit
+  // which operand does not depend on the previous kernel on the stream (0 none,
+  // 1 A, 2 B): it is prefetched into the first smem stages before the PDL wait
+  int indep;
 };
+
+// Split count for a decode GEMM: minimises waves x K-blocks per CTA (+ a per-split reduction cost).
+int gemm_choose_splits(int m_rows, int n_rows, int K, int bn, int num_sms, int max_splits);
+// Split count of the engine's decode GEMMs (measured on B200, tools/gemm_decode_sweep.py):
+// no split once the weight tiles cover most SMs, else ~SMs/tiles (2..4) splits.
+int gemm_decode_splits(int m_rows, int K, int num_sms);
 
 // Creates a 2D bf16 tensor map (rows x cols, row-major, 128B swizzle, box 64 x box_rows).
 int make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int box_rows);
@@ -53,6 +72,10 @@ int make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols
 cudaError_t gemm_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K, int bn,
                         int splits, const GemmEpi& epi, int num_sms, cudaStream_t stream);
 int gemm_smem_bytes(int bn);
+// CTA-pair (cta_group::2) 256 x 256-tile variant for the non-swapped (prefill) epilogues.
+// mapA box 128 rows (A), mapB box 128 rows (half of the 256 B rows of a tile).
+cudaError_t gemm2_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K,
+                         const GemmEpi& epi, int num_sms, cudaStream_t stream);
 // The number of K splits gemm_launch actually runs for a requested count (every
 // split owns >= 1 K block); the reduction must use the same number.
 int gemm_effective_splits(int K, int splits);

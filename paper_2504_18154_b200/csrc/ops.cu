@@ -29,9 +29,9 @@ extern "C" {
 ecoserve_status ecoserve_op_gemm(const void* A, const void* B, int32_t m, int32_t n, int32_t k, int32_t out_mode,
                                  void* out, int32_t bn, void* stream) {
   if (!A || !B || !out || m < 1 || n < 1 || k < 1 || k % 8 || (out_mode != 0 && out_mode != 1)) return ECOSERVE_ERR_INVALID_ARG;
-  if (bn != 64 && bn != 128 && bn != 256) return ECOSERVE_ERR_INVALID_ARG;
+  if (bn != 2 && bn != 64 && bn != 128 && bn != 256) return ECOSERVE_ERR_INVALID_ARG;
   CUtensorMap ma, mb;
-  if (make_tmap_bf16(&ma, A, m, k, 128) || make_tmap_bf16(&mb, B, n, k, bn)) return ECOSERVE_ERR_CUDA;
+  if (make_tmap_bf16(&ma, A, m, k, 128) || make_tmap_bf16(&mb, B, n, k, bn == 2 ? 128 : bn)) return ECOSERVE_ERR_CUDA;
   GemmEpi e;
   memset(&e, 0, sizeof(e));
   e.mode = out_mode == 0 ? EPI_F32 : EPI_BF16;
@@ -39,7 +39,10 @@ ecoserve_status ecoserve_op_gemm(const void* A, const void* B, int32_t m, int32_
   e.ldo = n;
   if (out_mode == 1 && n % 8) return ECOSERVE_ERR_INVALID_ARG;
   if (out_mode == 0 && n % 4) return ECOSERVE_ERR_INVALID_ARG;
-  OPCK(gemm_launch(&ma, &mb, m, n, k, bn, 1, e, num_sms(), (cudaStream_t)stream));
+  if (bn == 2)
+    OPCK(gemm2_launch(&ma, &mb, m, n, k, e, num_sms(), (cudaStream_t)stream));
+  else
+    OPCK(gemm_launch(&ma, &mb, m, n, k, bn, 1, e, num_sms(), (cudaStream_t)stream));
   return ECOSERVE_OK;
 }
 
@@ -62,6 +65,25 @@ ecoserve_status ecoserve_op_gemm_swap(const void* W, const void* X, int32_t m, i
   r.out = out;
   r.ldo = m;
   OPCK(splitk_reduce_launch(RED_F32, workspace, eff, n, m, m, r, (cudaStream_t)stream));
+  return ECOSERVE_OK;
+}
+
+ecoserve_status ecoserve_op_gemm_swap_bf16(const void* W, const void* X, int32_t m, int32_t n, int32_t k,
+                                           int32_t splits, float* part, int32_t* counters, void* out, int32_t bn,
+                                           void* stream) {
+  if (!W || !X || !out || m < 1 || n < 1 || k < 1 || k % 8 || splits < 1 || (splits > 1 && (!part || !counters)))
+    return ECOSERVE_ERR_INVALID_ARG;
+  if (bn != 64 && bn != 128 && bn != 256) return ECOSERVE_ERR_INVALID_ARG;
+  CUtensorMap ma, mb;
+  if (make_tmap_bf16(&ma, W, m, k, 128) || make_tmap_bf16(&mb, X, n, k, bn)) return ECOSERVE_ERR_CUDA;
+  GemmEpi e;
+  memset(&e, 0, sizeof(e));
+  e.mode = EPI_SWAP_BF16;
+  e.out = out;
+  e.ldo = m;
+  e.part = part;
+  e.counters = counters;
+  OPCK(gemm_launch(&ma, &mb, m, n, k, bn, gemm_effective_splits(k, splits), e, num_sms(), (cudaStream_t)stream));
   return ECOSERVE_OK;
 }
 

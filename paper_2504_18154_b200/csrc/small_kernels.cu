@@ -8,10 +8,13 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "launch.cuh"
 
 namespace eco {
 
 __global__ void embed_kernel(const int* __restrict__ ids, const bf16* __restrict__ E, float* __restrict__ x, int H) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   const bf16* src = E + (int64_t)ids[t] * H;
   float* dst = x + (int64_t)t * H;
@@ -26,13 +29,14 @@ __global__ void embed_kernel(const int* __restrict__ ids, const bf16* __restrict
 
 cudaError_t embed_launch(const int* ids, const bf16* E, float* x, int n, int H, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  embed_kernel<<<n, 128, 0, s>>>(ids, E, x, H);
-  return cudaGetLastError();
+  return launch_k(embed_kernel, dim3(n), dim3(128), 0, s, ids, E, x, H);
 }
 
 // out[i] = bf16( x[row_i] * rsqrt(mean(x[row_i]^2) + eps) * gamma ), row_i = rows ? rows[i] : i
 __global__ void rmsnorm_kernel(const float* __restrict__ x, int64_t ldx, const int* __restrict__ rows,
                                const bf16* __restrict__ gamma, bf16* __restrict__ out, int H, float eps) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x;
   const int r = rows ? rows[i] : i;
   const float* src = x + (int64_t)r * ldx;
@@ -70,8 +74,7 @@ cudaError_t rmsnorm_launch(const float* x, int64_t ldx, const int* rows, const b
   if (n == 0) return cudaSuccess;
   if (H % 4) return cudaErrorInvalidValue;
   const int threads = H >= 4096 ? 512 : (H >= 1024 ? 256 : 128);
-  rmsnorm_kernel<<<n, threads, 0, s>>>(x, ldx, rows, gamma, out, H, eps);
-  return cudaGetLastError();
+  return launch_k(rmsnorm_kernel, dim3(n), dim3(threads), 0, s, x, ldx, rows, gamma, out, H, eps);
 }
 
 __global__ void row_gather_kernel(const bf16* __restrict__ s0, const bf16* __restrict__ s1,
@@ -95,6 +98,8 @@ cudaError_t row_gather_launch(const bf16* s0, const bf16* s1, const bf16* s2, co
 // tokens[i] = argmax over parts of (val, idx): largest value, lowest index on ties.
 __global__ void argmax_reduce_kernel(const float* __restrict__ val, const int* __restrict__ idx, int parts, int ld,
                                      int* __restrict__ tokens, int* __restrict__ nan_flag) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x;
   float bv = -INFINITY;
   int bi = 0x7fffffff;
@@ -130,8 +135,7 @@ __global__ void argmax_reduce_kernel(const float* __restrict__ val, const int* _
 cudaError_t argmax_reduce_launch(const float* val, const int* idx, int n, int parts, int ld, int* tokens, int* nan_flag,
                                  cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  argmax_reduce_kernel<<<n, 128, 0, s>>>(val, idx, parts, ld, tokens, nan_flag);
-  return cudaGetLastError();
+  return launch_k(argmax_reduce_kernel, dim3(n), dim3(128), 0, s, val, idx, parts, ld, tokens, nan_flag);
 }
 
 __device__ __forceinline__ float silu_r(float z) { return z / (1.f + __expf(-z)); }
@@ -139,6 +143,8 @@ __device__ __forceinline__ float silu_r(float z) { return z / (1.f + __expf(-z))
 // part [split][row][ld_part] f32; one thread per (row, column pair).
 __global__ void splitk_reduce_kernel(int mode, const float* __restrict__ part, int splits, int rows, int cols,
                                      int64_t ld_part, GemmEpi e) {
+  pdl_trigger();
+  pdl_wait();
   const int pairs = cols / 2;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)rows * pairs) return;

@@ -32,6 +32,21 @@ def gemm_swap(W: torch.Tensor, X: torch.Tensor, splits: int = 1, bn: int = 64) -
     return out
 
 
+def gemm_swap_bf16(W: torch.Tensor, X: torch.Tensor, splits: int = 1, bn: int = 64,
+                   check_counters: bool = False) -> torch.Tensor:
+    """out bf16 [n][m] = X W^T through the in-kernel split-K reduction path."""
+    m, k = W.shape
+    n = X.shape[0]
+    part = torch.empty(splits, n, m, dtype=torch.float32, device=W.device)
+    cnt = torch.zeros(((m + 127) // 128) * ((n + bn - 1) // bn), dtype=torch.int32, device=W.device)
+    out = torch.empty(n, m, dtype=torch.bfloat16, device=W.device)
+    L.check(L.load().ecoserve_op_gemm_swap_bf16(W.data_ptr(), X.data_ptr(), m, n, k, splits, part.data_ptr(),
+                                                cnt.data_ptr(), out.data_ptr(), bn, _s()))
+    if check_counters:
+        assert int(cnt.abs().sum()) == 0, "split-K counters must be left at zero"
+    return out
+
+
 def lm_argmax(W: torch.Tensor, X: torch.Tensor) -> torch.Tensor:
     V, k = W.shape
     n = X.shape[0]

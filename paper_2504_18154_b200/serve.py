@@ -1,0 +1,249 @@
+"""Live PaDG serving of one macro instance over real GPU instances
+(SURVEY 8(a) rows a1-a4 and a18 in live mode).
+
+* One worker thread per GPU instance runs the intra-instance policy (temporal
+  disaggregation): after every decode step, if the
+  macro forwarded requests, it switches to a prefill phase that drains them FIFO
+  in <= token_budget batches (A16), then switches back to decode; it stamps
+  t_first / t_decode_begin / t_done with the host clock and pushes its status
+  (decode progress, memory use) to the macro after every phase call.
+* The dispatcher thread replays the trace in real time (Poisson arrivals)
+  and routes every arrival with the C++ macro scheduler (Alg. 1/2),
+  deferring when no instance passes CheckConstraints; rolling activation
+  emerges from the routing.
+* Metrics per Sec. 3.3: reported TTFT includes the phase-switch
+  wait; TPOT is measured from the first decode step after the switch.
+
+The ctypes calls into libecoserve.so release the GIL, so N instances on N GPUs
+run concurrently from one process.
+"""
+from __future__ import annotations
+
+import queue
+import threading
+import time
+from collections import deque
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from .macro import MacroScheduler, SchedConfig
+
+IDLE, PREFILL, DECODE = 0, 1, 2
+
+
+@dataclass
+class LiveReq:
+    req_id: int
+    arrival_ns: int
+    prompt: np.ndarray
+    G: int
+    inst: int = -1
+    t_first_ns: int = -1
+    t_decode_begin_ns: int = -1
+    t_done_ns: int = -1
+    n_gen: int = 0
+    tokens: List[int] = field(default_factory=list)
+
+    @property
+    def S(self) -> int:
+        return len(self.prompt)
+
+
+class Clock:
+    def __init__(self):
+        self.t0 = time.perf_counter_ns()
+
+    def now(self) -> int:
+        return time.perf_counter_ns() - self.t0
+
+
+class Worker(threading.Thread):
+    def __init__(self, idx: int, inst, clock: Clock, status_q: "queue.Queue", token_budget: int,
+                 decode_steps_per_poll: int = 1, max_batch: int = 256):
+        super().__init__(daemon=True)
+        self.idx, self.inst, self.clock = idx, inst, clock
+        self.inbox: "queue.Queue" = queue.Queue()
+        self.status_q = status_q
+        self.budget = token_budget
+        self.k = decode_steps_per_poll
+        self.max_batch = max_batch
+        self.stop_flag = threading.Event()
+        self.phase, self.t_switch = IDLE, 0
+        self.pending: deque = deque()
+        self.waiting: List[LiveReq] = []
+        self.running: List[LiveReq] = []
+        self.finished: List[LiveReq] = []
+        self.timeline: List[tuple] = []
+        self.error: Optional[BaseException] = None
+
+    def push_status(self, fin: Sequence[LiveReq] = ()):
+        live = list(self.pending) + self.waiting + self.running
+        recs = [(r.req_id, r.arrival_ns, r.S, r.t_first_ns, r.n_gen, False) for r in live]
+        recs += [(r.req_id, r.arrival_ns, r.S, r.t_first_ns, r.n_gen, True) for r in fin]
+        self.status_q.put((self.idx, self.phase, self.t_switch, recs))
+
+    def _drain_inbox(self, block: bool):
+        try:
+            r = self.inbox.get(timeout=0.002) if block else self.inbox.get_nowait()
+            self.pending.append(r)
+            while True:
+                self.pending.append(self.inbox.get_nowait())
+        except queue.Empty:
+            pass
+
+    def run(self):
+        try:
+            self._loop()
+        except BaseException as e:  # surfaced by the server
+            self.error = e
+
+    def _loop(self):
+        while not self.stop_flag.is_set():
+            self._drain_inbox(block=False)
+            if self.pending:
+                if self.phase != PREFILL:
+                    self.phase, self.t_switch = PREFILL, self.clock.now()
+                batch, tok = [], 0
+                while self.pending and len(batch) < self.max_batch and \
+                        (not batch or tok + self.pending[0].S <= self.budget):
+                    r = self.pending.popleft()
+                    batch.append(r)
+                    tok += r.S
+                t0 = self.clock.now()
+                first = self.inst.prefill([(r.req_id, r.prompt, r.G) for r in batch])
+                t = self.clock.now()
+                self.timeline.append((t0, t, "prefill", len(batch)))
+                fin = []
+                for r, f in zip(batch, first):
+                    r.t_first_ns, r.n_gen = t, 1
+                    r.tokens.append(int(f))
+                    if r.G <= 1:
+                        r.t_decode_begin_ns = r.t_done_ns = t
+                        fin.append(r)
+                    else:
+                        self.waiting.append(r)
+                self._finish(fin)
+                self.push_status(fin)
+            elif self.waiting or self.running:
+                if self.phase != DECODE:
+                    self.phase, self.t_switch = DECODE, self.clock.now()
+                    for r in self.waiting:
+                        r.t_decode_begin_ns = self.t_switch
+                    self.running += self.waiting
+                    self.waiting = []
+                t0 = self.clock.now()
+                toks, _ = self.inst.decode([r.req_id for r in self.running], self.k)
+                t = self.clock.now()
+                self.timeline.append((t0, t, "decode", len(self.running)))
+                fin, keep = [], []
+                for i, r in enumerate(self.running):
+                    for s in range(self.k):
+                        if toks[i, s] >= 0:
+                            r.tokens.append(int(toks[i, s]))
+                            r.n_gen += 1
+                    if r.n_gen >= r.G:
+                        r.t_done_ns = t
+                        fin.append(r)
+                    else:
+                        keep.append(r)
+                self.running = keep
+                self._finish(fin)
+                self.push_status(fin)
+            else:
+                self._drain_inbox(block=True)
+
+    def _finish(self, fin):
+        if fin:
+            self.inst.release([r.req_id for r in fin])
+            self.finished += fin
+
+
+def profile_prefill(inst, lens=(128, 256, 512, 1024, 2048, 4096, 8192), vocab: int = 1000, reps: int = 2):
+    """On-box prefill profile (P:513 'predicted in advance by profiling sequences
+    of various lengths'; reading A13): median ns of a single-request prefill phase."""
+    rng = np.random.default_rng(0)
+    out_l, out_ns = [], []
+    rid = -1_000_000
+    for S in lens:
+        ts = []
+        for _ in range(reps + 1):
+            p = rng.integers(0, vocab, S).astype(np.int32)
+            t0 = time.perf_counter_ns()
+            inst.prefill([(rid, p, 1)])
+            ts.append(time.perf_counter_ns() - t0)
+            inst.release([rid])
+            rid -= 1
+        out_l.append(S)
+        out_ns.append(int(np.median(ts[1:])))
+    return out_l, out_ns
+
+
+class PaDGServer:
+    """A macro instance of len(instances) GPU instances under rolling activation."""
+
+    def __init__(self, instances: Sequence, slo_ttft_ns: int, slo_tpot_ns: int, reserve_tokens: int,
+                 predictor_table=None, token_budget: int = 16384, decode_steps_per_poll: int = 1,
+                 probe_printed: bool = False):
+        self.clock = Clock()
+        self.status_q: "queue.Queue" = queue.Queue()
+        self.workers = [Worker(i, inst, self.clock, self.status_q, token_budget, decode_steps_per_poll)
+                        for i, inst in enumerate(instances)]
+        blocks = [inst.num_blocks for inst in instances]
+        self.macro = MacroScheduler(SchedConfig(len(instances), slo_ttft_ns, slo_tpot_ns, reserve_tokens, blocks,
+                                                probe_printed=probe_printed, table=predictor_table))
+        self.route_log: List[tuple] = []
+        self.reqs: Dict[int, LiveReq] = {}
+
+    def _apply_statuses(self):
+        n = 0
+        while True:
+            try:
+                idx, phase, t_switch, recs = self.status_q.get_nowait()
+            except queue.Empty:
+                break
+            self.macro.update_status(idx, phase, t_switch, self.workers[idx].inst.num_blocks, recs)
+            n += 1
+        if n:
+            for rid, i in self.macro.drain_deferred(self.clock.now()):
+                self._send(self.reqs[rid], i)
+
+    def _send(self, r: LiveReq, i: int):
+        r.inst = i
+        self.route_log.append((self.clock.now(), r.req_id, i))
+        self.workers[i].inbox.put(r)
+
+    def run(self, trace, timeout_s: float = 600.0) -> Dict[int, LiveReq]:
+        """Replay `trace` (synthetic.traces.Request with prompts) in real time."""
+        for w in self.workers:
+            w.start()
+        reqs = sorted(trace, key=lambda r: (r.arrival_ns, r.req_id))
+        t_start = self.clock.now()
+        for r in reqs:
+            lr = LiveReq(r.req_id, t_start + r.arrival_ns, np.asarray(r.prompt, np.int32), r.output_len)
+            self.reqs[r.req_id] = lr
+        pending = deque(self.reqs[r.req_id] for r in reqs)
+        deadline = time.perf_counter() + timeout_s
+        while time.perf_counter() < deadline:
+            self._apply_statuses()
+            now = self.clock.now()
+            while pending and pending[0].arrival_ns <= now:
+                lr = pending.popleft()
+                i, _ = self.macro.route(lr.req_id, lr.arrival_ns, lr.S, now)
+                if i < 0:
+                    self.route_log.append((now, lr.req_id, -1))
+                    self.macro.defer(lr.req_id, lr.arrival_ns, lr.S)
+                else:
+                    self._send(lr, i)
+            for w in self.workers:
+                if w.error is not None:
+                    raise RuntimeError(f"instance {w.idx} failed") from w.error
+            if not pending and all(r.t_done_ns >= 0 for r in self.reqs.values()):
+                break
+            time.sleep(0.0005)
+        for w in self.workers:
+            w.stop_flag.set()
+        for w in self.workers:
+            w.join(timeout=30)
+        return self.reqs
