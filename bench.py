@@ -237,15 +237,9 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     dev_ms = tm["prefill_ms"] + tm["decode_ms"]
     tokens = stats["prefill_tokens"] + stats["decode_tokens"]
     # max over ranks of the times, sum over ranks of the work
-    vec = torch.tensor([dev_ms, wall, float(tokens), float(stats["prefill_tokens"]), float(stats["decode_tokens"]),
-                        tm["prefill_ms"], tm["decode_ms"]], dtype=torch.float64, device=dev)
-    if world > 1:
-        mx = vec.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = vec.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-    else:
-        mx = sm = vec
+    from paper_2504_18154_b200.dist import reduce_max_sum
+    mx, sm = reduce_max_sum([dev_ms, wall, float(tokens), float(stats["prefill_tokens"]),
+                             float(stats["decode_tokens"]), tm["prefill_ms"], tm["decode_ms"]], device=dev)
     if rank == 0:
         P, src = peaks()
         dev_ms_max, wall_max = float(mx[0]), float(mx[1])

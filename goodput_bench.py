@@ -1,0 +1,114 @@
+#!/usr/bin/env python
+"""Goodput under SLO of a live PaDG macro instance on real B200 instances
+(the second half of BASELINE.json's metric: "goodput req/s at TTFT/TPOT SLO, 1-8 GPU").
+
+One process, one worker thread per GPU instance (ctypes calls release the GIL),
+the C++ macro scheduler routing in real time (Alg. 1/2 with the on-box prefill
+profile as predictor, reading A13). Each probe replays a fresh Poisson trace
+ shaped like ShareGPT (Table 4; prompts <= 4096 as P:660, outputs
+capped at --max-out), measures joint TTFT/TPOT attainment (Sec. 3.3), and the
+rate is bisected for the largest one meeting the percentile.
+
+  python goodput_bench.py --gpus N [--shape 8b] [--p 0.9] [--n-req 300]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--instances-per-gpu", type=int, default=1)
+    ap.add_argument("--shape", default="8b")
+    ap.add_argument("--preset", default="sharegpt")
+    ap.add_argument("--slo-ttft", type=float, default=5.0)
+    ap.add_argument("--slo-tpot", type=float, default=0.1)
+    ap.add_argument("--p", type=float, default=0.9)
+    ap.add_argument("--n-req", type=int, default=300)
+    ap.add_argument("--max-out", type=int, default=1024)
+    ap.add_argument("--lo", type=float, default=4.0)
+    ap.add_argument("--hi", type=float, default=160.0)
+    ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--blocks", type=int, default=8000)
+    ap.add_argument("--rates", type=str, default="", help="comma list: fixed probes instead of bisection")
+    args = ap.parse_args()
+
+    import torch
+
+    from paper_2504_18154_b200 import build as B
+    B.build(verbose=False)
+    from paper_2504_18154_b200 import metrics as MX
+    from paper_2504_18154_b200.instance import Instance, random_device_weights
+    from paper_2504_18154_b200.serve import PaDGServer, profile_prefill
+    from synthetic.shapes import get_shape
+    from synthetic.traces import make_trace
+
+    shape = get_shape(args.shape)
+    n_gpu = min(args.gpus, torch.cuda.device_count())
+    insts = []
+    for g in range(n_gpu):
+        dev = torch.device("cuda", g)
+        torch.cuda.set_device(dev)
+        w = random_device_weights(shape, seed=100 + g, device=dev)
+        for _ in range(args.instances_per_gpu):
+            insts.append(Instance(shape, w, args.blocks, g, token_budget=16384, max_batch=512,
+                                  max_positions=8192, free_raw_after_create=(args.instances_per_gpu == 1)))
+    lens, ns = profile_prefill(insts[0], vocab=shape.vocab)
+    slo_ttft, slo_tpot = int(args.slo_ttft * 1e9), int(args.slo_tpot * 1e9)
+    probes = []
+    rid0 = [0]
+
+    def attain_at(rate: float) -> float:
+        trace = make_trace(args.preset, args.n_req, seed=int(rate * 1000) % 100003, rate_per_s=rate,
+                           vocab=shape.vocab)
+        for r in trace:
+            r.output_len = min(r.output_len, args.max_out)
+            r.req_id += rid0[0]
+        rid0[0] += args.n_req
+        srv = PaDGServer(insts, slo_ttft, slo_tpot, reserve_tokens=237, predictor_table=(lens, ns))
+        t0 = time.perf_counter()
+        out = srv.run(trace, timeout_s=900)
+        wall = time.perf_counter() - t0
+        recs = [MX.request_ok(r.arrival_ns, r.t_first_ns, r.t_decode_begin_ns, r.t_done_ns, r.G, slo_ttft, slo_tpot)
+                for r in out.values()]
+        att = MX.attainment(recs)
+        fin = [x for x in recs if x["finished"]]
+        toks = sum(r.G for r in out.values() if r.t_done_ns >= 0)
+        per_inst = [sum(1 for r in out.values() if r.inst == i) for i in range(len(insts))]
+        probes.append({"rate": round(rate, 3), "attainment": round(att, 4), "wall_s": round(wall, 2),
+                       "ttft_p90_s": round(float(np.percentile([x["ttft_ns"] for x in fin], 90)) / 1e9, 4) if fin else None,
+                       "tpot_p90_ms": round(float(np.percentile([x["tpot_ns"] for x in fin], 90)) / 1e6, 3) if fin else None,
+                       "out_tok_s": round(toks / wall, 1), "per_instance": per_inst,
+                       "deferred": sum(1 for x in srv.route_log if x[2] < 0)})
+        print(json.dumps({"probe": probes[-1]}), flush=True)
+        return att
+
+    if args.rates:
+        for r in [float(x) for x in args.rates.split(",")]:
+            attain_at(r)
+        ok = [p["rate"] for p in probes if p["attainment"] >= args.p]
+        gp = max(ok) if ok else 0.0
+    else:
+        gp = MX.bisect_goodput(attain_at, args.p, args.lo, args.hi, args.iters)
+    line = {"metric": "goodput req/s at TTFT/TPOT SLO", "value": gp, "unit": "req/s", "n_gpus": n_gpu,
+            "instances": len(insts), "p": args.p, "slo": {"ttft_s": args.slo_ttft, "tpot_s": args.slo_tpot},
+            "config": {"workload": f"{args.preset} Poisson, {args.n_req} req/probe, outputs <= {args.max_out}",
+                       "shape": args.shape, "macro": f"{len(insts)} instances, rolling activation (Alg. 1/2)"},
+            "predictor": {"lens": lens, "ns": ns}, "probes": probes}
+    print(json.dumps(line), flush=True)
+    for i in insts:
+        i.close()
+
+
+if __name__ == "__main__":
+    main()

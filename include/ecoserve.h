@@ -52,7 +52,8 @@ typedef struct {
   int32_t vocab;      /* V */
   float rope_theta;   /* reading A3 */
   float rms_eps;      /* reading A4 */
-  int32_t tp_size;    /* 1 (TP=2 pairs: ECOSERVE_ERR_UNSUPPORTED in this build) */
+  int32_t tp_size;    /* 1, or 2: a TP pair splitting heads, kv heads and FFN
+                         columns; every size query and buffer below is then per rank */
 } ecoserve_model_shape;
 
 /* Paged KV pool (PagedAttention). Layout, block-major so a
@@ -113,6 +114,9 @@ typedef struct {
 
 typedef struct ecoserve_instance ecoserve_instance;
 
+/* Writes a fresh NCCL unique id (128 bytes) to host `out` for a TP pair. */
+ecoserve_status ecoserve_nccl_unique_id(void* out);
+
 /* Bytes of the KV pool for `num_blocks` blocks (layout above). <0 on bad args. */
 int64_t ecoserve_kv_pool_bytes(const ecoserve_model_shape* shape, int32_t block_tokens, int64_t num_blocks);
 /* Bytes of the caller-allocated prepared-weight buffer (fused, re-laid-out QKV
@@ -121,8 +125,15 @@ int64_t ecoserve_prepared_weight_bytes(const ecoserve_model_shape* shape);
 
 /* Create an instance on `device`. `prepared` is a caller-allocated device buffer
  * of ecoserve_prepared_weight_bytes(); `cuda_stream` is a borrowed cudaStream_t
- * (NULL = the library creates its own). tp_rank must be 0 and nccl_unique_id
- * NULL in this build. */
+ * (NULL = the library creates its own).
+ * TP=2 (shape->tp_size == 2): each rank of the pair (one process
+ * per GPU) calls create concurrently with tp_rank 0/1 and the same 128-byte
+ * nccl_unique_id (from ecoserve_nccl_unique_id on one rank, broadcast by the
+ * caller). `raw` then holds the rank's shard: wq/wk/wv/w_gate/w_up rows and
+ * wo/w_down columns of heads [r*M/2, (r+1)*M/2), kv heads [r*Mkv/2, ..) and FFN
+ * columns [r*F/2, ..); embed, LM head and norms are replicated. The residual
+ * stream is all-reduced (fp32 sum) after the O and down projections; both ranks
+ * return identical tokens. tp_size 1 requires tp_rank 0 and nccl_unique_id NULL. */
 ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, const ecoserve_kv_pool* kv,
                                          const ecoserve_weights* raw, void* prepared, int32_t device,
                                          int32_t tp_rank, const void* nccl_unique_id, void* cuda_stream,

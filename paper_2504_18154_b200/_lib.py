@@ -109,6 +109,7 @@ PI32, PI64, PF32 = C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_flo
 
 # name -> (restype, argtypes); every symbol include/*.h declares
 SIGNATURES = {
+    "ecoserve_nccl_unique_id": (C.c_int, [P]),
     "ecoserve_kv_pool_bytes": (I64, [C.POINTER(ModelShape), I32, I64]),
     "ecoserve_prepared_weight_bytes": (I64, [C.POINTER(ModelShape)]),
     "ecoserve_instance_create": (C.c_int, [C.POINTER(ModelShape), C.POINTER(KVPool), C.POINTER(Weights), P, I32,

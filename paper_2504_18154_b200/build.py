@@ -15,6 +15,15 @@ LIB = os.path.join(PKG, "libecoserve.so")
 SOURCES = ["gemm_sm100.cu", "attention.cu", "small_kernels.cu", "engine.cu", "ops.cu", "sched.cpp"]
 HEADERS = ["common.cuh", "kernels.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dir():
+    import site
+    for sp in site.getsitepackages():
+        d = os.path.join(sp, "nvidia", "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("nccl.h not found (nvidia-nccl wheel)")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "--expt-relaxed-constexpr"]
 
@@ -35,12 +44,14 @@ def build(force: bool = False, verbose: bool = True) -> str:
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
+    nccl = _nccl_dir()
+    incs = ["-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include")]
     for src in SOURCES:
         obj = os.path.join(objdir, src + ".o")
-        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *incs, "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cpp"):
-            cmd = [NVCC, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
-                   "-c", os.path.join(CSRC, src), "-o", obj]
+            cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
+                   *incs, "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
         objs.append(obj)
     failed = False
@@ -54,8 +65,9 @@ def build(force: bool = False, verbose: bool = True) -> str:
     if failed:
         raise RuntimeError("building libecoserve.so failed")
     tmp = LIB + ".tmp"
+    libdir = os.path.join(nccl, "lib")
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs,
-                           "-lcudart"])
+                           "-lcudart", "-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath={libdir}"])
     os.replace(tmp, LIB)
     return LIB
 

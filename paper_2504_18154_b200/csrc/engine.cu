@@ -20,6 +20,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <nccl.h>
+
 #include "../../include/ecoserve.h"
 #include "kernels.h"
 
@@ -123,6 +125,8 @@ struct ecoserve_instance {
   ecoserve_model_shape shape{};
   int L = 0, H = 0, M = 0, Mkv = 0, D = 0, F = 0, V = 0, QKV = 0;
   int device = 0, num_sms = 148;
+  int tp = 1, tp_rank = 0;
+  ncclComm_t comm = nullptr;     // TP=2 pair (a17): all-reduce of the residual after O and down
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   bool dead = false;
@@ -183,6 +187,22 @@ struct ecoserve_instance {
     }                                                             \
   } while (0)
 
+// TP=2: in-place fp32 sum of the residual stream over the pair (NCCL over NVLink)
+#define ALLREDUCE_X(rows)                                                                              \
+  do {                                                                                                 \
+    if (inst->tp > 1) {                                                                                \
+      const int _m = inst->prof.begin(P_OTHER, inst->stream);                                          \
+      ncclResult_t _r = ncclAllReduce(inst->x, inst->x, (size_t)(rows) * inst->H, ncclFloat, ncclSum,  \
+                                      inst->comm, inst->stream);                                       \
+      inst->prof.end(_m, 0, inst->stream);                                                             \
+      if (_r != ncclSuccess) {                                                                         \
+        inst->err = std::string("ncclAllReduce: ") + ncclGetErrorString(_r);                           \
+        inst->dead = true;                                                                             \
+        return ECOSERVE_ERR_NCCL;                                                                      \
+      }                                                                                                \
+    }                                                                                                  \
+  } while (0)
+
 // launch `expr` (which launches `nk` kernels) under profiler class `cls` with algorithmic work `w`
 #define LAUNCH(cls, w, nk, expr)                                  \
   do {                                                            \
@@ -192,13 +212,27 @@ struct ecoserve_instance {
     inst->prof.launches += (nk);                                  \
   } while (0)
 
+// The per-rank shape of a TP group (heads and FFN columns are split over
+// the tp ranks; hidden size, vocabulary and layer count are not).
+static ecoserve_model_shape local_shape(const ecoserve_model_shape* s) {
+  ecoserve_model_shape l = *s;
+  const int tp = s->tp_size > 0 ? s->tp_size : 1;
+  l.n_heads = s->n_heads / tp;
+  l.n_kv_heads = s->n_kv_heads / tp;
+  l.ffn_dim = s->ffn_dim / tp;
+  return l;
+}
+
 static bool shape_ok(const ecoserve_model_shape* s) {
   if (!s) return false;
-  if (s->n_layers < 1 || s->hidden < 64 || s->hidden % 64 || s->n_heads < 1 || s->n_kv_heads < 1) return false;
-  if (s->n_heads % s->n_kv_heads || s->n_heads / s->n_kv_heads > 16) return false;
-  if (!(s->head_dim == 32 || s->head_dim == 64 || s->head_dim == 128)) return false;
-  if (s->ffn_dim < 64 || s->ffn_dim % 64 || s->vocab < 1) return false;
-  if ((s->n_heads * s->head_dim) % 64) return false;
+  if (s->tp_size != 1 && s->tp_size != 2) return false;
+  if (s->n_heads % s->tp_size || s->n_kv_heads % s->tp_size || s->ffn_dim % s->tp_size) return false;
+  const ecoserve_model_shape l = local_shape(s);
+  if (l.n_layers < 1 || l.hidden < 64 || l.hidden % 64 || l.n_heads < 1 || l.n_kv_heads < 1) return false;
+  if (l.n_heads % l.n_kv_heads || l.n_heads / l.n_kv_heads > 16) return false;
+  if (!(l.head_dim == 32 || l.head_dim == 64 || l.head_dim == 128)) return false;
+  if (l.ffn_dim < 64 || l.ffn_dim % 64 || l.vocab < 1) return false;
+  if ((l.n_heads * l.head_dim) % 64) return false;
   return true;
 }
 
@@ -206,14 +240,24 @@ extern "C" {
 
 int64_t ecoserve_kv_pool_bytes(const ecoserve_model_shape* s, int32_t block_tokens, int64_t num_blocks) {
   if (!shape_ok(s) || block_tokens != BLOCK || num_blocks < 1) return -1;
-  return num_blocks * (int64_t)s->n_layers * 2 * s->n_kv_heads * BLOCK * s->head_dim * 2;
+  const ecoserve_model_shape l = local_shape(s);
+  return num_blocks * (int64_t)l.n_layers * 2 * l.n_kv_heads * BLOCK * l.head_dim * 2;
 }
 
 int64_t ecoserve_prepared_weight_bytes(const ecoserve_model_shape* s) {
   if (!shape_ok(s)) return -1;
-  const int64_t qkv = (int64_t)(s->n_heads + 2 * s->n_kv_heads) * s->head_dim * s->hidden;
-  const int64_t gu = 2LL * s->ffn_dim * s->hidden;
-  return (int64_t)s->n_layers * (qkv + gu) * 2;
+  const ecoserve_model_shape l = local_shape(s);
+  const int64_t qkv = (int64_t)(l.n_heads + 2 * l.n_kv_heads) * l.head_dim * l.hidden;
+  const int64_t gu = 2LL * l.ffn_dim * l.hidden;
+  return (int64_t)l.n_layers * (qkv + gu) * 2;
+}
+
+ecoserve_status ecoserve_nccl_unique_id(void* out) {
+  if (!out) return ECOSERVE_ERR_INVALID_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return ECOSERVE_ERR_NCCL;
+  memcpy(out, &id, sizeof(id));
+  return ECOSERVE_OK;
 }
 
 const char* ecoserve_last_error(const ecoserve_instance* inst) { return inst ? inst->err.c_str() : "null instance"; }
@@ -238,6 +282,7 @@ void ecoserve_instance_destroy(ecoserve_instance* inst) {
   if (inst->h_meta) cudaFreeHost(inst->h_meta);
   if (inst->h_tokens) cudaFreeHost(inst->h_tokens);
   for (cudaEvent_t e : inst->prof.pool) cudaEventDestroy(e);
+  if (inst->comm) ncclCommDestroy(inst->comm);
   if (inst->own_stream && inst->stream) cudaStreamDestroy(inst->stream);
   delete inst;
 }
@@ -251,17 +296,22 @@ ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, cons
   if (!shape_ok(shape) || !kv || !raw || !prepared || !kv->pool || kv->block_tokens != BLOCK || kv->num_blocks < 1 ||
       !raw->embed || !raw->lm_head || !raw->final_norm || !raw->layers)
     return ECOSERVE_ERR_INVALID_ARG;
-  if (shape->tp_size != 1 || tp_rank != 0 || nccl_unique_id) return ECOSERVE_ERR_UNSUPPORTED;
+  if (shape->tp_size == 1 && (tp_rank != 0 || nccl_unique_id)) return ECOSERVE_ERR_INVALID_ARG;
+  if (shape->tp_size == 2 && (tp_rank < 0 || tp_rank > 1 || !nccl_unique_id)) return ECOSERVE_ERR_INVALID_ARG;
   std::unique_ptr<ecoserve_instance> holder(new ecoserve_instance());
   ecoserve_instance* inst = holder.get();
   inst->shape = *shape;
-  inst->L = shape->n_layers;
-  inst->H = shape->hidden;
-  inst->M = shape->n_heads;
-  inst->Mkv = shape->n_kv_heads;
-  inst->D = shape->head_dim;
-  inst->F = shape->ffn_dim;
-  inst->V = shape->vocab;
+  inst->tp = shape->tp_size;
+  inst->tp_rank = tp_rank;
+  // every per-head / per-FFN-column dimension below is this rank's shard
+  const ecoserve_model_shape ls = local_shape(shape);
+  inst->L = ls.n_layers;
+  inst->H = ls.hidden;
+  inst->M = ls.n_heads;
+  inst->Mkv = ls.n_kv_heads;
+  inst->D = ls.head_dim;
+  inst->F = ls.ffn_dim;
+  inst->V = ls.vocab;
   inst->QKV = (inst->M + 2 * inst->Mkv) * inst->D;
   if (cfg) {
     if (cfg->token_budget > 0) inst->T_max = cfg->token_budget;
@@ -402,6 +452,15 @@ ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, cons
   if (inst->debug) CK(cudaMalloc(&inst->dbg, sizeof(float) * (int64_t)(L + 1) * T * H));
   CK(cudaStreamSynchronize(st));
   cudaFree(d_map);
+  if (inst->tp > 1) {  // both ranks of the pair call create concurrently (one process per GPU)
+    ncclUniqueId id;
+    memcpy(&id, nccl_unique_id, sizeof(id));
+    const ncclResult_t r = ncclCommInitRank(&inst->comm, inst->tp, id, tp_rank);
+    if (r != ncclSuccess) {
+      inst->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+      return ECOSERVE_ERR_NCCL;
+    }
+  }
   *out = holder.release();
   return ECOSERVE_OK;
 }
@@ -430,6 +489,21 @@ GemmEpi epi_base(ecoserve_instance* inst) {
   e.q_out = inst->q;
   return e;
 }
+
+// Residual update after the O / down projection. TP=1: x += acc. TP=2 (row a17,
+// P:276-283): rank 0 writes x + acc_0, rank 1 writes acc_1, and one NCCL all-reduce
+// (sum, fp32, in place) forms x + acc_0 + acc_1 -- bitwise identical on both ranks,
+// so the replicated LM head takes the same argmax without another collective.
+GemmEpi resid_epi(ecoserve_instance* inst) {
+  GemmEpi e = epi_base(inst);
+  e.resid = inst->x;
+  e.ldr = inst->H;
+  e.out = inst->x;
+  e.ldo = inst->H;
+  return e;
+}
+int resid_mode_prefill(const ecoserve_instance* inst) { return inst->tp_rank == 0 ? EPI_RESID : EPI_F32; }
+int resid_mode_decode(const ecoserve_instance* inst) { return inst->tp_rank == 0 ? EPI_SWAP_RESID : EPI_SWAP_STORE; }
 
 bf16* k_layer(ecoserve_instance* inst, int l) { return inst->pool + (int64_t)l * 2 * inst->Mkv * BLOCK * inst->D; }
 bf16* v_layer(ecoserve_instance* inst, int l) { return k_layer(inst, l) + (int64_t)inst->Mkv * BLOCK * inst->D; }
@@ -471,7 +545,7 @@ cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const 
   cudaError_t r = gemm_launch(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, splits, ge, inst->num_sms, inst->stream);
   if (r != cudaSuccess) return r;
   const int red = mode == EPI_SWAP_QKV ? RED_QKV : mode == EPI_SWAP_SILU ? RED_SILU
-                : mode == EPI_SWAP_RESID ? RED_RESID : RED_BF16;
+                : mode == EPI_SWAP_RESID ? RED_RESID : mode == EPI_SWAP_STORE ? RED_F32 : RED_BF16;
   *nk = 2;
   return splitk_reduce_launch(red, inst->part, splits, B, n_out, n_out, e, inst->stream);
 }
@@ -512,12 +586,11 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
     a.n_kv = inst->Mkv;
     a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
     LAUNCH(P_ATTN_PREFILL, attn_flop, 1, attn_prefill_launch(a, D, st));
-    GemmEpi eo = epi_base(inst);
-    eo.mode = EPI_RESID;
-    eo.resid = inst->x;
-    eo.ldr = H;
+    GemmEpi eo = resid_epi(inst);
+    eo.mode = resid_mode_prefill(inst);
     LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * M * D, 1,
            prefill_gemm(inst, inst->m_ao.a, w.o_a, w.o_b, T, H, M * D, eo));
+    ALLREDUCE_X(T);
     LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, T, H, eps, st));
     GemmEpi eg = epi_base(inst);
     eg.mode = EPI_SILU;
@@ -525,12 +598,11 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
     eg.ldo = F;
     LAUNCH(P_GEMM_PREFILL, 2.0 * T * 2 * F * H, 1,
            prefill_gemm(inst, inst->m_h.a, w.gu_a, w.gu_b, T, 2 * F, H, eg));
-    GemmEpi ed = epi_base(inst);
-    ed.mode = EPI_RESID;
-    ed.resid = inst->x;
-    ed.ldr = H;
+    GemmEpi ed = resid_epi(inst);
+    ed.mode = resid_mode_prefill(inst);
     LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * F, 1,
            prefill_gemm(inst, inst->m_act.a, w.d_a, w.d_b, T, H, F, ed));
+    ALLREDUCE_X(T);
     if (inst->debug)
       CK(cudaMemcpyAsync(inst->dbg + (int64_t)(l + 1) * inst->T_max * H, inst->x, sizeof(float) * (int64_t)T * H,
                          cudaMemcpyDeviceToDevice, st));
@@ -581,21 +653,20 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     a.out = inst->ao;
     a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
     LAUNCH(P_ATTN_DECODE, kv_bytes, n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
-    GemmEpi eo = epi_base(inst);
-    eo.resid = inst->x;
-    eo.ldr = H;
+    GemmEpi eo = resid_epi(inst);
     LAUNCH(P_GEMM_DECODE, 2.0 * H * M * D, nk,
-           decode_gemm(inst, w.o_a, inst->m_ao, H, M * D, B, EPI_SWAP_RESID, eo, &nk));
+           decode_gemm(inst, w.o_a, inst->m_ao, H, M * D, B, resid_mode_decode(inst), eo, &nk));
+    ALLREDUCE_X(B);
     LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, B, H, eps, st));
     GemmEpi eg = epi_base(inst);
     eg.out = inst->act;
     eg.ldo = F;
     LAUNCH(P_GEMM_DECODE, 2.0 * 2 * F * H, nk,
            decode_gemm(inst, w.gu_a, inst->m_h, 2 * F, H, B, EPI_SWAP_SILU, eg, &nk));
-    GemmEpi ed = epi_base(inst);
-    ed.resid = inst->x;
-    ed.ldr = H;
-    LAUNCH(P_GEMM_DECODE, 2.0 * H * F, nk, decode_gemm(inst, w.d_a, inst->m_act, H, F, B, EPI_SWAP_RESID, ed, &nk));
+    GemmEpi ed = resid_epi(inst);
+    LAUNCH(P_GEMM_DECODE, 2.0 * H * F, nk,
+           decode_gemm(inst, w.d_a, inst->m_act, H, F, B, resid_mode_decode(inst), ed, &nk));
+    ALLREDUCE_X(B);
     if (inst->debug)
       CK(cudaMemcpyAsync(inst->dbg + (int64_t)(l + 1) * inst->T_max * H, inst->x, sizeof(float) * (int64_t)B * H,
                          cudaMemcpyDeviceToDevice, st));

@@ -159,6 +159,10 @@ __device__ __forceinline__ void epi_swap(const GemmEpi& e, int m, int m_rows, in
       if (mv)
         for (int i = 0; i < ncols; ++i) e.resid[(int64_t)(n0 + i) * e.ldr + m] += f[i];
     } break;
+    case EPI_SWAP_STORE: {
+      if (mv)
+        for (int i = 0; i < ncols; ++i) e.resid[(int64_t)(n0 + i) * e.ldr + m] = f[i];
+    } break;
     case EPI_SWAP_SILU: {
       bf16* o = reinterpret_cast<bf16*>(e.out);
 #pragma unroll

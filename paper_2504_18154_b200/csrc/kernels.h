@@ -29,6 +29,7 @@ enum EpiMode : int {
   EPI_SWAP_RESID = 8,   // resid f32 [n][ldr] at m += acc
   EPI_SWAP_SILU = 9,    // out bf16 [n][ldo] at m/2: silu(acc[m even]) * acc[m + 1]
   EPI_SWAP_QKV = 10,    // RoPE on pair-interleaved q/k rows (lanes 2j, 2j+1), KV to the pool
+  EPI_SWAP_STORE = 11,  // resid f32 [n][ldr] at m = acc (TP ranks > 0: partial sum before the all-reduce)
 };
 
 struct GemmEpi {

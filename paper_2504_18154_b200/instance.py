@@ -59,16 +59,46 @@ def random_device_weights(shape, seed: int, device) -> Dict:
     return {"embed": mat(V, H, 1.0), "lm_head": mat(V, H, 2.0 / H ** 0.5), "final_norm": norm(H), "layers": layers}
 
 
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    L.check(L.load().ecoserve_nccl_unique_id(buf))
+    return buf.raw
+
+
+def shard_weights(w: Dict, shape, tp: int, rank: int) -> Dict:
+    """TP shard of full weights: heads [r*M/tp, (r+1)*M/tp), kv heads
+    [r*Mkv/tp, ..), FFN columns [r*F/tp, ..); embed / LM head / norms replicated."""
+    D = shape.head_dim
+    mq, mk, f = shape.n_heads // tp * D, shape.n_kv_heads // tp * D, shape.ffn_dim // tp
+    out = {k: w[k] for k in ("embed", "lm_head", "final_norm")}
+    out["layers"] = []
+    for l in w["layers"]:
+        out["layers"].append({
+            "attn_norm": l["attn_norm"], "ffn_norm": l["ffn_norm"],
+            "wq": l["wq"][rank * mq:(rank + 1) * mq].contiguous(),
+            "wk": l["wk"][rank * mk:(rank + 1) * mk].contiguous(),
+            "wv": l["wv"][rank * mk:(rank + 1) * mk].contiguous(),
+            "wo": l["wo"][:, rank * mq:(rank + 1) * mq].contiguous(),
+            "w_gate": l["w_gate"][rank * f:(rank + 1) * f].contiguous(),
+            "w_up": l["w_up"][rank * f:(rank + 1) * f].contiguous(),
+            "w_down": l["w_down"][:, rank * f:(rank + 1) * f].contiguous()})
+    return out
+
+
 class Instance:
     """One instance on one GPU. Owns (via torch) the borrowed buffers."""
 
     def __init__(self, shape, weights: Dict, num_blocks: int, device: int = 0, token_budget: int = 16384,
                  max_batch: int = 512, max_positions: int = 16384, debug_hidden: bool = False,
-                 free_raw_after_create: bool = False, stream: Optional[int] = None):
+                 free_raw_after_create: bool = False, stream: Optional[int] = None, tp_size: int = 1,
+                 tp_rank: int = 0, nccl_id: Optional[bytes] = None):
+        """tp_size 2: `weights` hold this rank's shard (see shard_weights); all
+        ranks of the pair construct concurrently with the same nccl_id."""
         self.lib = L.load()
         self.shape = shape
         self.device = torch.device("cuda", device)
-        self.cshape = c_shape(shape)
+        self.cshape = c_shape(shape, tp_size)
+        self._nccl_id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         pool_bytes = self.lib.ecoserve_kv_pool_bytes(C.byref(self.cshape), 64, num_blocks)
         prep_bytes = self.lib.ecoserve_prepared_weight_bytes(C.byref(self.cshape))
         if pool_bytes < 0 or prep_bytes < 0:
@@ -88,8 +118,8 @@ class Instance:
         h = C.c_void_p()
         torch.cuda.set_device(self.device)
         L.check(self.lib.ecoserve_instance_create(C.byref(self.cshape), C.byref(self.ckv), C.byref(self.cw),
-                                                  C.c_void_p(self.prepared.data_ptr()), device, 0, None,
-                                                  C.c_void_p(stream) if stream else None,
+                                                  C.c_void_p(self.prepared.data_ptr()), device, tp_rank,
+                                                  self._nccl_id, C.c_void_p(stream) if stream else None,
                                                   C.byref(self.cfg), C.byref(h)))
         self.h = h
         if free_raw_after_create:  # wq/wk/wv/w_gate/w_up were copied into the prepared buffer

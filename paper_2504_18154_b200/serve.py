@@ -160,7 +160,7 @@ class Worker(threading.Thread):
             self.finished += fin
 
 
-def profile_prefill(inst, lens=(128, 256, 512, 1024, 2048, 4096, 8192), vocab: int = 1000, reps: int = 2):
+def profile_prefill(inst, lens=(128, 256, 512, 1024, 2048, 4096), vocab: int = 1000, reps: int = 2):
     """On-box prefill profile (P:513 'predicted in advance by profiling sequences
     of various lengths'; reading A13): median ns of a single-request prefill phase."""
     rng = np.random.default_rng(0)

@@ -52,11 +52,16 @@ def test_create_rejects_bad_args_without_touching_gpu(lib):
     out = ctypes.c_void_p()
     assert lib.ecoserve_instance_create(ctypes.byref(s), None, None, None, 0, 0, None, None, None,
                                         ctypes.byref(out)) == 1
-    s2 = ModelShape(2, 256, 8, 8, 32, 768, 1024, 1e4, 1e-5, 2)      # TP=2 not in this build
+    s2 = ModelShape(2, 256, 8, 8, 32, 768, 1024, 1e4, 1e-5, 2)      # TP=2 needs an NCCL id
     kv = KVPool(64, 4, 1)
     w = Weights(1, 1, 1, ctypes.cast(ctypes.c_void_p(1), ctypes.POINTER(ctypes.c_void_p)))
     assert lib.ecoserve_instance_create(ctypes.byref(s2), ctypes.byref(kv), ctypes.byref(w), ctypes.c_void_p(1), 0, 0,
-                                        None, None, None, ctypes.byref(out)) == 4
+                                        None, None, None, ctypes.byref(out)) == 1
+    s3 = ModelShape(2, 256, 8, 8, 32, 768, 1024, 1e4, 1e-5, 4)      # only TP 1 or 2
+    assert lib.ecoserve_prepared_weight_bytes(ctypes.byref(s3)) < 0
+    # TP=2 sizes are per rank: half the kv heads, half the QKV/gate-up rows
+    assert lib.ecoserve_kv_pool_bytes(ctypes.byref(s2), 64, 1) * 2 == \
+        lib.ecoserve_kv_pool_bytes(ctypes.byref(ModelShape(2, 256, 8, 8, 32, 768, 1024, 1e4, 1e-5, 1)), 64, 1)
 
 
 def test_product_does_not_import_oracle():

@@ -82,6 +82,26 @@ def test_live_serving_completes_and_rolls(S):
     assert sorted(x[1] for x in routed) == sorted(out)
 
 
+def test_product_metrics_match_oracle_definition():
+    import random
+    from oracle import metrics as OM
+    from paper_2504_18154_b200 import metrics as MX
+    rng = random.Random(4)
+    for _ in range(2000):
+        arr = rng.randint(0, 10 ** 9)
+        tf = -1 if rng.random() < 0.05 else arr + rng.randint(0, 2 * 10 ** 9)
+        db = tf + rng.randint(0, 10 ** 8) if tf >= 0 else -1
+        G = rng.randint(1, 50)
+        td = db + rng.randint(0, (G - 1) * 2 * 10 ** 8) if tf >= 0 else -1
+        slo = (rng.choice([10 ** 9, 5 * 10 ** 8]), rng.choice([10 ** 8, 5 * 10 ** 7]))
+        a = MX.request_ok(arr, tf, db, td, G, *slo)
+        b = OM.request_metrics(arr, tf, db, td, G, *slo)
+        assert a["ok"] == b.ok and a["finished"] == b.finished
+        if b.finished:
+            assert a["ttft_ok"] == b.ttft_ok and a["tpot_ok"] == b.tpot_ok
+    assert MX.bisect_goodput(lambda r: 1.0 if r <= 13.0 else 0.0, 0.9, 1, 100, 20) == pytest.approx(13.0, abs=1e-3)
+
+
 def test_worker_prefers_prefill_after_decode_step(S):
     """Intra-instance policy: a request arriving during decoding is
     prefilled right after the in-flight decode step (non-preemptive, A15)."""
