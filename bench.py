@@ -291,11 +291,11 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
             "roofline": roof, "roofline_breakdown": breakdown, "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
-            pr, dr, secs, thr = oracle_sample()
+            pr, dr, secs, thr = oracle_sample(prefill_len=4096, n_dec=8, dec_ctx=1024, dec_steps=16)
             v = mix_rate(pr, dr, float(sm[3]), float(sm[4]))
             line["cpu_baseline"] = {
                 "value": round(v, 3), "unit": "tokens/s", "cores": thr, "kind": "oracle",
-                "sample": "1 layer of the 8B shape: prefill 1x1024 tokens + decode 8 seqs x 2 steps at ctx 1024, "
+                "sample": "1 layer of the 8B shape: prefill 1x4096 tokens + decode 8 seqs x 16 steps at ctx 1024, "
                           "fp64 NumPy, extrapolated x32 layers, mixed at this run's prefill/decode token ratio "
                           f"({secs:.1f} s of CPU work)"}
         print(json.dumps(line), flush=True)

@@ -34,6 +34,12 @@ ecoserve_status ecoserve_op_gemm_swap_bf16(const void* W, const void* X, int32_t
                                            int32_t splits, float* part, int32_t* counters, void* out, int32_t bn,
                                            void* stream);
 
+/* The engine's decode GEMM: out f32 [n][m] = X W^T with r (1 or 2) 128-row weight
+ * tiles per CTA sharing one activation tile; splits == 1: written by the GEMM
+ * epilogue; splits > 1: f32 partials in `ws` [splits][n][m] + fixed-order reduction. */
+ecoserve_status ecoserve_op_gemm_decode(const void* W, const void* X, int32_t m, int32_t n, int32_t k, int32_t r,
+                                        int32_t splits, float* ws, float* out, int32_t bn, void* stream);
+
 /* Greedy LM head (rows a12/a16): tokens[i] = argmax_v (X [n][k] W[v][k]^T), lowest
  * v on ties, logits never materialised. workspace: f32 [n][ceil(V/128)] and
  * i32 [n][ceil(V/128)]. */

@@ -527,23 +527,46 @@ cudaError_t prefill_gemm(ecoserve_instance* inst, const CUtensorMap& amap, const
 
 // Skinny decode GEMM (swap-AB): weights on the MMA M side, the B tokens on N, K split so
 // the grid fills the SMs; the epilogue (and the split reduction) run inside the kernel.
+int decode_variant() {  // 1: 1-CTA/SM GEMM (default); 3: lean (co-resident with the next kernel)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_DEC_VARIANT");
+    v = e ? atoi(e) : 1;
+    if (v != 1 && v != 3) v = 1;
+  }
+  return v;
+}
+
+// norm_gamma / norm_out (optional): when the projection is a residual add split over K,
+// its reduction is fused with the following RMSNorm (one kernel: x += sum of partials,
+// out = rmsnorm(x) * gamma); *fused reports whether that happened.
 cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const ActMaps& xm, int n_out, int K, int B,
-                        int mode, GemmEpi e, int* nk) {
+                        int mode, GemmEpi e, int* nk, const bf16* norm_gamma = nullptr, bf16* norm_out = nullptr,
+                        bool* fused = nullptr) {
   const int bn = B <= 64 ? 64 : 128;  // B > 128: several 128-token tiles; weight re-reads hit L2
   const int splits = gemm_decode_splits(n_out, K, inst->num_sms);
+  const int var = decode_variant();
+  if (fused) *fused = false;
   e.indep = 1;  // weights (A) prefetch before the PDL wait
   if (splits == 1) {  // epilogue in the GEMM
     e.mode = mode;
     *nk = 1;
-    return gemm_launch(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, 1, e, inst->num_sms, inst->stream);
+    return gemm_launch_r(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, var, 1, e, inst->num_sms, inst->stream);
   }
   // split-K: f32 partials, then one fixed-order reduction kernel applying the epilogue
   GemmEpi ge = e;
   ge.mode = EPI_SWAP_F32;
   ge.out = inst->part;
   ge.ldo = n_out;
-  cudaError_t r = gemm_launch(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, splits, ge, inst->num_sms, inst->stream);
+  cudaError_t r =
+      gemm_launch_r(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, var, splits, ge, inst->num_sms, inst->stream);
   if (r != cudaSuccess) return r;
+  if (norm_gamma && mode == EPI_SWAP_RESID && n_out == inst->H) {
+    *nk = 2;
+    if (fused) *fused = true;
+    return splitk_resid_rmsnorm_launch(inst->part, splits, B, inst->x, norm_gamma, norm_out, inst->H,
+                                       inst->shape.rms_eps, inst->stream);
+  }
   const int red = mode == EPI_SWAP_QKV ? RED_QKV : mode == EPI_SWAP_SILU ? RED_SILU
                 : mode == EPI_SWAP_RESID ? RED_RESID : mode == EPI_SWAP_STORE ? RED_F32 : RED_BF16;
   *nk = 2;
@@ -612,7 +635,7 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
 
 static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const int* d_ids, const int* d_pos,
                                          const int* d_slot, const int* d_ctx, const int* d_bt, int bt_ld,
-                                         int max_blocks, double kv_bytes) {
+                                         int max_blocks, double kv_bytes, bool* final_normed) {
   cudaStream_t st = inst->stream;
   const int L = inst->L, H = inst->H, M = inst->M, D = inst->D, F = inst->F;
   const float eps = inst->shape.rms_eps;
@@ -624,9 +647,14 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
   const int bps = (max_blocks + n_splits - 1) / n_splits;
   n_splits = (max_blocks + bps - 1) / bps;
   if ((int64_t)B * M * n_splits * (D + 2) > inst->attn_ws_elems) return ECOSERVE_ERR_INVALID_ARG;
+  // RMSNorms fused into the split-K reduction of the preceding O / down projection (TP=1)
+  const bool can_fuse = inst->tp == 1;
+  bool h_ready = false, fused = false;
+  *final_normed = false;
   for (int l = 0; l < L; ++l) {
     LayerW& w = inst->lw[l];
-    LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.attn_norm, inst->h, B, H, eps, st));
+    if (!h_ready) LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.attn_norm, inst->h, B, H, eps, st));
+    h_ready = false;
     GemmEpi e = epi_base(inst);
     e.pos = d_pos;
     e.slot = d_slot;
@@ -655,18 +683,26 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     LAUNCH(P_ATTN_DECODE, kv_bytes, n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
     GemmEpi eo = resid_epi(inst);
     LAUNCH(P_GEMM_DECODE, 2.0 * H * M * D, nk,
-           decode_gemm(inst, w.o_a, inst->m_ao, H, M * D, B, resid_mode_decode(inst), eo, &nk));
+           decode_gemm(inst, w.o_a, inst->m_ao, H, M * D, B, resid_mode_decode(inst), eo, &nk,
+                       can_fuse ? w.ffn_norm : nullptr, inst->h, &fused));
     ALLREDUCE_X(B);
-    LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, B, H, eps, st));
+    if (!fused) LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, B, H, eps, st));
     GemmEpi eg = epi_base(inst);
     eg.out = inst->act;
     eg.ldo = F;
     LAUNCH(P_GEMM_DECODE, 2.0 * 2 * F * H, nk,
            decode_gemm(inst, w.gu_a, inst->m_h, 2 * F, H, B, EPI_SWAP_SILU, eg, &nk));
+    // the down projection's reduction also applies the next RMSNorm: the next layer's
+    // attention norm, or after the last layer the final norm (into the LM-head input)
+    const bool last = l + 1 == L;
     GemmEpi ed = resid_epi(inst);
     LAUNCH(P_GEMM_DECODE, 2.0 * H * F, nk,
-           decode_gemm(inst, w.d_a, inst->m_act, H, F, B, resid_mode_decode(inst), ed, &nk));
+           decode_gemm(inst, w.d_a, inst->m_act, H, F, B, resid_mode_decode(inst), ed, &nk,
+                       can_fuse ? (last ? inst->final_norm : inst->lw[l + 1].attn_norm) : nullptr,
+                       last ? inst->hl : inst->h, &fused));
     ALLREDUCE_X(B);
+    h_ready = fused && !last;
+    if (last) *final_normed = fused;
     if (inst->debug)
       CK(cudaMemcpyAsync(inst->dbg + (int64_t)(l + 1) * inst->T_max * H, inst->x, sizeof(float) * (int64_t)B * H,
                          cudaMemcpyDeviceToDevice, st));
@@ -675,10 +711,13 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
 }
 
 // final RMSNorm of the selected rows + LM head + greedy argmax -> h_tokens[0..n)
-static ecoserve_status lm_head_argmax(ecoserve_instance* inst, const int* d_rows, int n, int gemm_cls) {
+static ecoserve_status lm_head_argmax(ecoserve_instance* inst, const int* d_rows, int n, int gemm_cls,
+                                      bool normed = false) {
   cudaStream_t st = inst->stream;
   const int H = inst->H;
-  LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, d_rows, inst->final_norm, inst->hl, n, H, inst->shape.rms_eps, st));
+  if (!normed)  // (decode: usually already fused into the last down projection's reduction)
+    LAUNCH(P_OTHER, 0, 1,
+           rmsnorm_launch(inst->x, H, d_rows, inst->final_norm, inst->hl, n, H, inst->shape.rms_eps, st));
   GemmEpi e;
   memset(&e, 0, sizeof(e));
   e.mode = EPI_SWAP_ARGMAX;
@@ -893,10 +932,11 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
     for (int k = 0; k < B; ++k) kv_tokens += ctx[k];
     const double kv_bytes = kv_tokens * 2.0 * inst->Mkv * inst->D * 2.0;  // K and V, one layer
     const int pm = inst->prof.begin(P_DECODE, st);
+    bool final_normed = false;
     ecoserve_status es = run_layers_decode(inst, B, d, d + (pos - hm), d + (slot - hm), d + (ctx - hm), d + (bt - hm),
-                                           bt_ld, max_blocks, kv_bytes);
+                                           bt_ld, max_blocks, kv_bytes, &final_normed);
     if (es != ECOSERVE_OK) return es;
-    es = lm_head_argmax(inst, d + (rows - hm), B, P_GEMM_DECODE);
+    es = lm_head_argmax(inst, d + (rows - hm), B, P_GEMM_DECODE, final_normed);
     if (es != ECOSERVE_OK) return es;
     inst->prof.end(pm, B, st);
     CK(cudaMemcpyAsync(inst->h_tokens, inst->d_tokens, sizeof(int) * B, cudaMemcpyDeviceToHost, st));

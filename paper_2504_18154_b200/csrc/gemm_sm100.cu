@@ -23,14 +23,24 @@ static constexpr int BM = 128;
 static constexpr int BK = 64;
 static constexpr int GEMM_THREADS = 192;
 
-template <int BN>
+// R = 128-row A tiles per work unit sharing one B tile (R = 2 in the decode GEMMs:
+// two weight tiles per CTA stream behind one activation tile, so 2/3 of the staged
+// bytes are weights instead of 1/2 -- more weight bytes in flight per SM).
+// R = 3 selects the "lean" single-tile variant: 3 smem stages (< 114 KB of smem) so a
+// CTA of the next kernel on the stream can be resident beside it -- with PDL its
+// prologue and weight prefetch then overlap this kernel's tail.
+template <int BN, int R = 1>
 struct GemmCfg {
-  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int RT = R == 3 ? 1 : R;  // A tiles per unit
+  static constexpr int A_BYTES = RT * BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
-  static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
+  static constexpr int STAGES = R == 3 ? 3 : (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int ACC_COLS = RT * BN;  // one accumulator stage
+  static constexpr int TMEM_COLS = (2 * ACC_COLS) <= 32 ? 32 : (2 * ACC_COLS) <= 64 ? 64 : (2 * ACC_COLS) <= 128 ? 128
+                                 : (2 * ACC_COLS) <= 256 ? 256 : 512;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(2 * ACC_COLS <= 512, "two accumulator stages must fit the 512 TMEM columns");
 };
 
 __device__ __forceinline__ float silu_f(float z) { return z / (1.f + __expf(-z)); }
@@ -214,11 +224,12 @@ __device__ __forceinline__ void epi_swap(const GemmEpi& e, int m, int m_rows, in
   }
 }
 
-template <int BN>
+template <int BN, int RV>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int m_rows,
                    int n_rows, int K, int splits, GemmEpi epi) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, RV>;
+  constexpr int R = C::RT;  // 128-row A tiles per work unit
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
@@ -231,7 +242,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __shared__ int s_last;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int m_tiles = (m_rows + BM - 1) / BM;
+  const int m_tiles = (m_rows + BM * R - 1) / (BM * R);  // work units of R x 128 rows
   const int n_tiles = (n_rows + BN - 1) / BN;
   const int kb_total = (K + BK - 1) / BK;
   const int kb_per = (kb_total + splits - 1) / splits;
@@ -287,7 +298,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         while (npre < C::STAGES && next()) {
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
-          if (indep == 1) tma_load_2d(sa, &mapA, &full_bar[stage], kb * BK, mt * BM);
+          if (indep == 1) tma_load_2d(sa, &mapA, &full_bar[stage], kb * BK, mt * BM * R);
           else tma_load_2d(sa + C::A_BYTES, &mapB, &full_bar[stage], kb * BK, nt * BN);
           pre_mt[npre] = mt; pre_nt[npre] = nt; pre_kb[npre] = kb;
           ++npre;
@@ -299,7 +310,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int i = 0; i < npre; ++i) {
         uint8_t* sa = smem + i * C::STAGE_BYTES;
         if (indep == 1) tma_load_2d(sa + C::A_BYTES, &mapB, &full_bar[i], pre_kb[i] * BK, pre_nt[i] * BN);
-        else tma_load_2d(sa, &mapA, &full_bar[i], pre_kb[i] * BK, pre_mt[i] * BM);
+        else tma_load_2d(sa, &mapA, &full_bar[i], pre_kb[i] * BK, pre_mt[i] * BM * R);
       }
       // 3) steady state
       while (next()) {
@@ -307,7 +318,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         uint8_t* sa = smem + stage * C::STAGE_BYTES;
         uint8_t* sb = sa + C::A_BYTES;
         mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
-        tma_load_2d(sa, &mapA, &full_bar[stage], kb * BK, mt * BM);
+        tma_load_2d(sa, &mapA, &full_bar[stage], kb * BK, mt * BM * R);
         tma_load_2d(sb, &mapB, &full_bar[stage], kb * BK, nt * BN);
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
@@ -325,17 +336,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int kb0 = ks * kb_per, kb1 = min(kb_total, kb0 + kb_per);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t sb = sa + C::A_BYTES;
-          const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sb);
+          const uint64_t db = umma_desc_sw128(sb);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // advance 16 bf16 = 32 B along K inside the 128 B swizzle row: +2 in 16-byte units
-            tc_mma_f16(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          for (int r = 0; r < R; ++r) {
+            const uint64_t da = umma_desc_sw128(sa + r * BM * BK * 2);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              // advance 16 bf16 = 32 B along K inside the 128 B swizzle row: +2 in 16-byte units
+              tc_mma_f16(d_tmem + r * BN, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
           }
           tc_commit(&empty_bar[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -358,8 +373,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row = q * 32 + lane;  // accumulator row (TMEM lane)
-      const int m = mt * BM + row;
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      const int m = mt * BM * R + row;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::ACC_COLS;
       if (epi.mode == EPI_SWAP_ARGMAX) {
         for (int c0 = 0; c0 < BN; c0 += 32) {
           uint32_t v[32];
@@ -401,15 +416,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         asm volatile("bar.sync 1, 128;" ::: "memory");
       } else if (epi.mode == EPI_SWAP_F32) {
         float* out = reinterpret_cast<float*>(epi.out) + (int64_t)ks * n_rows * epi.ldo;
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32(tbase + c0, v);
-          tc_wait_ld();
-          if (m < m_rows) {
+#pragma unroll 1
+        for (int r = 0; r < R; ++r) {
+          const int mr = m + r * BM;
+          for (int c0 = 0; c0 < BN; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(tbase + r * BN + c0, v);
+            tc_wait_ld();
+            if (mr < m_rows) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const int n = nt * BN + c0 + i;
-              if (n < n_rows) out[(int64_t)n * epi.ldo + m] = __uint_as_float(v[i]);
+              for (int i = 0; i < 32; ++i) {
+                const int n = nt * BN + c0 + i;
+                if (n < n_rows) out[(int64_t)n * epi.ldo + mr] = __uint_as_float(v[i]);
+              }
             }
           }
         }
@@ -418,14 +437,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (lane == 0) mbar_arrive(&tempty_bar[acc]);
       } else if (epi.mode >= EPI_SWAP_BF16) {
         if (splits == 1) {
-          for (int c0 = 0; c0 < BN; c0 += 32) {
-            uint32_t v[32];
-            tmem_ld32(tbase + c0, v);
-            tc_wait_ld();
-            float f[32];
+#pragma unroll 1
+          for (int r = 0; r < R; ++r) {
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+              uint32_t v[32];
+              tmem_ld32(tbase + r * BN + c0, v);
+              tc_wait_ld();
+              float f[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-            epi_swap(epi, m, m_rows, nt * BN + c0, n_rows, lane, f);
+              for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+              epi_swap(epi, m + r * BM, m_rows, nt * BN + c0, n_rows, lane, f);
+            }
           }
           tc_fence_before();
           __syncwarp();
@@ -750,42 +772,64 @@ int gemm_decode_splits(int m_rows, int K, int num_sms) {
 
 int gemm_smem_bytes(int bn) {
   switch (bn) {
-    case 64: return GemmCfg<64>::SMEM;
-    case 128: return GemmCfg<128>::SMEM;
-    default: return GemmCfg<256>::SMEM;
+    case 64: return GemmCfg<64, 1>::SMEM;
+    case 128: return GemmCfg<128, 1>::SMEM;
+    default: return GemmCfg<256, 1>::SMEM;
   }
 }
 
-template <int BN>
+template <int BN, int R>
 static cudaError_t launch_bn(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K,
                              int splits, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+  using C = GemmCfg<BN, R>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         GemmCfg<BN>::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int m_tiles = (m_rows + BM - 1) / BM, n_tiles = (n_rows + BN - 1) / BN;
+  const int m_tiles = (m_rows + BM * C::RT - 1) / (BM * C::RT), n_tiles = (n_rows + BN - 1) / BN;
   const int work = m_tiles * n_tiles * splits;
   const int grid = work < num_sms ? work : num_sms;
   if (grid <= 0) return cudaSuccess;
-  return launch_k(gemm_tc_kernel<BN>, dim3(grid), dim3(GEMM_THREADS), GemmCfg<BN>::SMEM, stream, *mapA, *mapB, m_rows,
+  return launch_k(gemm_tc_kernel<BN, R>, dim3(grid), dim3(GEMM_THREADS), C::SMEM, stream, *mapA, *mapB, m_rows,
                   n_rows, K, splits, epi);
 }
 
-cudaError_t gemm_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K, int bn,
-                        int splits, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+cudaError_t gemm_launch_r(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K, int bn,
+                          int r, int splits, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
   if (splits < 1) return cudaErrorInvalidValue;
   if (splits > 1 && epi.mode != EPI_SWAP_F32 && epi.mode < EPI_SWAP_BF16) return cudaErrorInvalidValue;
   if (splits > 1 && epi.mode >= EPI_SWAP_BF16 && (!epi.part || !epi.counters)) return cudaErrorInvalidValue;
   splits = gemm_effective_splits(K, splits);
+  if (r == 2) {
+    // two weight tiles per unit: swapped epilogues without the in-kernel split reduction
+    if (epi.mode != EPI_SWAP_F32 && !(epi.mode >= EPI_SWAP_BF16 && splits == 1)) return cudaErrorInvalidValue;
+    switch (bn) {
+      case 64: return launch_bn<64, 2>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
+      case 128: return launch_bn<128, 2>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  if (r == 3) {  // lean single-tile variant (co-resident with the next kernel's CTA)
+    switch (bn) {
+      case 64: return launch_bn<64, 3>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
+      case 128: return launch_bn<128, 3>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  if (r != 1) return cudaErrorInvalidValue;
   switch (bn) {
-    case 64: return launch_bn<64>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
-    case 128: return launch_bn<128>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
-    case 256: return launch_bn<256>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
+    case 64: return launch_bn<64, 1>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
+    case 128: return launch_bn<128, 1>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
+    case 256: return launch_bn<256, 1>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t gemm_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K, int bn,
+                        int splits, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+  return gemm_launch_r(mapA, mapB, m_rows, n_rows, K, bn, 1, splits, epi, num_sms, stream);
 }
 
 }  // namespace eco

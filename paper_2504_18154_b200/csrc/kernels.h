@@ -72,6 +72,10 @@ int make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols
 // Launch; tile width bn in {64, 128, 256}; splits > 1 only with EPI_SWAP_F32.
 cudaError_t gemm_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K, int bn,
                         int splits, const GemmEpi& epi, int num_sms, cudaStream_t stream);
+// r = 128-row A tiles per work unit (1 or 2; 2 needs an A tensor map with a 256-row box
+// and a swapped epilogue without the in-kernel split reduction).
+cudaError_t gemm_launch_r(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K, int bn,
+                          int r, int splits, const GemmEpi& epi, int num_sms, cudaStream_t stream);
 int gemm_smem_bytes(int bn);
 // CTA-pair (cta_group::2) 256 x 256-tile variant for the non-swapped (prefill) epilogues.
 // mapA box 128 rows (A), mapB box 128 rows (half of the 256 B rows of a tile).
@@ -124,6 +128,9 @@ cudaError_t rmsnorm_launch(const float* x, int64_t ldx, const int* rows, const b
 // dst[r] = src_sel[r][row[r]] (row copy of `cols` bf16), sel in {0,1,2} -> s0/s1/s2.
 cudaError_t row_gather_launch(const bf16* s0, const bf16* s1, const bf16* s2, const int* sel, const int* row, bf16* dst,
                               int nrows, int cols, cudaStream_t s);
+// x[row] += sum_s part[s][row] (split order); out[row] = bf16(rmsnorm(x[row]) * gamma). part plane = rows x H.
+cudaError_t splitk_resid_rmsnorm_launch(const float* part, int splits, int rows, float* x, const bf16* gamma,
+                                        bf16* out, int H, float eps, cudaStream_t s);
 cudaError_t argmax_reduce_launch(const float* val, const int* idx, int n, int parts, int ld, int* tokens,
                                  int* nan_flag, cudaStream_t s);
 // Decode epilogues (after a split-K swap GEMM): sum partial[split][row][col] in fixed split order, then

@@ -87,6 +87,36 @@ ecoserve_status ecoserve_op_gemm_swap_bf16(const void* W, const void* X, int32_t
   return ECOSERVE_OK;
 }
 
+ecoserve_status ecoserve_op_gemm_decode(const void* W, const void* X, int32_t m, int32_t n, int32_t k, int32_t r,
+                                        int32_t splits, float* ws, float* out, int32_t bn, void* stream) {
+  if (!W || !X || !out || m < 1 || n < 1 || k < 1 || k % 8 || m % 2 || splits < 1 || r < 1 || r > 3 ||
+      (splits > 1 && !ws))
+    return ECOSERVE_ERR_INVALID_ARG;
+  if (bn != 64 && bn != 128) return ECOSERVE_ERR_INVALID_ARG;
+  CUtensorMap ma, mb;
+  if (make_tmap_bf16(&ma, W, m, k, r == 2 ? 256 : 128) || make_tmap_bf16(&mb, X, n, k, bn)) return ECOSERVE_ERR_CUDA;
+  const int eff = gemm_effective_splits(k, splits);
+  GemmEpi e;
+  memset(&e, 0, sizeof(e));
+  if (eff == 1) {
+    e.mode = EPI_SWAP_STORE;
+    e.resid = out;
+    e.ldr = m;
+    OPCK(gemm_launch_r(&ma, &mb, m, n, k, bn, r, 1, e, num_sms(), (cudaStream_t)stream));
+    return ECOSERVE_OK;
+  }
+  e.mode = EPI_SWAP_F32;
+  e.out = ws;
+  e.ldo = m;
+  OPCK(gemm_launch_r(&ma, &mb, m, n, k, bn, r, eff, e, num_sms(), (cudaStream_t)stream));
+  GemmEpi red;
+  memset(&red, 0, sizeof(red));
+  red.out = out;
+  red.ldo = m;
+  OPCK(splitk_reduce_launch(RED_F32, ws, eff, n, m, m, red, (cudaStream_t)stream));
+  return ECOSERVE_OK;
+}
+
 ecoserve_status ecoserve_op_lm_argmax(const void* W, const void* X, int32_t V, int32_t n, int32_t k, float* ws_val,
                                       int32_t* ws_idx, int32_t* tokens, void* stream) {
   if (!W || !X || !ws_val || !ws_idx || !tokens || V < 1 || n < 1 || k < 1 || k % 8) return ECOSERVE_ERR_INVALID_ARG;

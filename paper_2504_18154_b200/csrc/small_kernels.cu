@@ -138,6 +138,67 @@ cudaError_t argmax_reduce_launch(const float* val, const int* idx, int n, int pa
   return launch_k(argmax_reduce_kernel, dim3(n), dim3(128), 0, s, val, idx, parts, ld, tokens, nan_flag);
 }
 
+// Decode O / down projection tail fused with the next RMSNorm: per row,
+//   x += sum_s part[s][row][:]  (fixed split order)  ;  out = bf16(rmsnorm(x) * gamma)
+// One CTA per row; each thread keeps its <= 4 float4 of the row in registers.
+__global__ void splitk_resid_rmsnorm_kernel(const float* __restrict__ part, int splits, int rows,
+                                            float* __restrict__ x, const bf16* __restrict__ gamma,
+                                            bf16* __restrict__ out, int H, float eps) {
+  pdl_trigger();
+  pdl_wait();
+  const int row = blockIdx.x;
+  const int64_t plane = (int64_t)rows * H;
+  float4 v[4];
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = (threadIdx.x + j * blockDim.x) * 4;
+    if (c < H) {
+      float4 a = *reinterpret_cast<const float4*>(x + (int64_t)row * H + c);
+      for (int s = 0; s < splits; ++s) {
+        const float4 p = *reinterpret_cast<const float4*>(part + s * plane + (int64_t)row * H + c);
+        a.x += p.x; a.y += p.y; a.z += p.z; a.w += p.w;
+      }
+      *reinterpret_cast<float4*>(x + (int64_t)row * H + c) = a;
+      ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+      v[j] = a;
+    }
+  }
+  __shared__ float red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / H + eps);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = (threadIdx.x + j * blockDim.x) * 4;
+    if (c < H) {
+      const uint2 gv = *reinterpret_cast<const uint2*>(gamma + c);
+      uint2 o;
+      o.x = pack_bf16x2(v[j].x * inv * bf16_lo(gv.x), v[j].y * inv * bf16_hi(gv.x));
+      o.y = pack_bf16x2(v[j].z * inv * bf16_lo(gv.y), v[j].w * inv * bf16_hi(gv.y));
+      *reinterpret_cast<uint2*>(out + (int64_t)row * H + c) = o;
+    }
+  }
+}
+
+cudaError_t splitk_resid_rmsnorm_launch(const float* part, int splits, int rows, float* x, const bf16* gamma,
+                                        bf16* out, int H, float eps, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  const int threads = H > 4096 ? 512 : (H >= 1024 ? 256 : 64);
+  if (H % 4 || H > threads * 16) return cudaErrorInvalidValue;
+  return launch_k(splitk_resid_rmsnorm_kernel, dim3(rows), dim3(threads), 0, s, part, splits, rows, x, gamma, out, H,
+                  eps);
+}
+
 __device__ __forceinline__ float silu_r(float z) { return z / (1.f + __expf(-z)); }
 
 // part [split][row][ld_part] f32; one thread per (row, column pair).

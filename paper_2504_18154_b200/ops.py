@@ -47,6 +47,17 @@ def gemm_swap_bf16(W: torch.Tensor, X: torch.Tensor, splits: int = 1, bn: int = 
     return out
 
 
+def gemm_decode(W: torch.Tensor, X: torch.Tensor, r: int = 2, splits: int = 1, bn: int = 128) -> torch.Tensor:
+    """out f32 [n][m] = X W^T through the engine's decode-GEMM configuration."""
+    m, k = W.shape
+    n = X.shape[0]
+    ws = torch.empty(max(splits, 1), n, m, dtype=torch.float32, device=W.device) if splits > 1 else None
+    out = torch.empty(n, m, dtype=torch.float32, device=W.device)
+    L.check(L.load().ecoserve_op_gemm_decode(W.data_ptr(), X.data_ptr(), m, n, k, r, splits,
+                                             ws.data_ptr() if ws is not None else None, out.data_ptr(), bn, _s()))
+    return out
+
+
 def lm_argmax(W: torch.Tensor, X: torch.Tensor) -> torch.Tensor:
     V, k = W.shape
     n = X.shape[0]

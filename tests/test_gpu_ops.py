@@ -72,6 +72,18 @@ def test_gemm_swap_inkernel_reduction(ops, m, n, k, splits, bn):
     assert np.array_equal(got, again)
 
 
+@pytest.mark.parametrize("m,n,k,r,splits,bn", [(640, 37, 1024, 2, 1, 64), (640, 37, 1024, 2, 3, 64),
+                                               (6144, 128, 4096, 2, 6, 128), (28672, 128, 4096, 2, 1, 128),
+                                               (4096, 100, 14336, 2, 8, 128), (300, 5, 192, 2, 2, 64),
+                                               (4096, 128, 4096, 1, 4, 128)])
+def test_gemm_decode_dual_tile(ops, m, n, k, r, splits, bn):
+    rng = np.random.default_rng(m + n + k + r + splits)
+    w, W = bf16_rand(rng, (m, k), 1.0 / np.sqrt(k))
+    x, X = bf16_rand(rng, (n, k))
+    got = ops.gemm_decode(W, X, r, splits, bn).cpu().numpy()
+    assert rel_err(got, x @ w.T) < 1e-5
+
+
 @pytest.mark.parametrize("V,n,k",[(1000, 5, 256), (32000, 64, 1024), (4097, 130, 512)])
 def test_lm_argmax(ops, V, n, k):
     rng = np.random.default_rng(V + n)
