@@ -269,6 +269,41 @@ int32_t ecoserve_macro_prev_idx(const ecoserve_macro* m);
 int64_t ecoserve_macro_predict_prefill_ns(const ecoserve_macro* m, int32_t prompt_len);
 void ecoserve_macro_destroy(ecoserve_macro* m);
 
+/* ------------------------------------------------------------------------
+ * Mitosis scaling (Sec. 3.5).
+ * ------------------------------------------------------------------------ */
+enum {
+  ECOSERVE_MITOSIS_CREATE = 0,       /* first macro created (a1 = index) */
+  ECOSERVE_MITOSIS_ADD = 1,          /* one instance added to macro a1 */
+  ECOSERVE_MITOSIS_ADD_SPLIT = 2,    /* added to a1, which then split off a new macro a2 of N_l */
+  ECOSERVE_MITOSIS_REMOVE = 3,       /* one instance removed from macro a1 */
+  ECOSERVE_MITOSIS_REMOVE_MERGE = 4, /* one removed from a1, then macros a1 and a2 merged */
+  ECOSERVE_MITOSIS_REMOVE_MACRO = 5  /* the last instance of the only macro removed */
+};
+/* One expansion (expand = 1) or contraction (0) step over the macro sizes
+ * (host array sizes[*n_macros], creation order, capacity cap) with bounds
+ * N_l <= N_u (Fig. 7: expansion fills the first macro below N_u, splitting off a
+ * new macro of N_l when all are full; contraction shrinks the smallest macro to
+ * N_l, then its partner, merging the pair into N_u - 1 once they total N_u).
+ * action (host [3]) = {kind, a1, a2}. */
+ecoserve_status ecoserve_mitosis_step(int32_t* sizes, int32_t* n_macros, int32_t cap, int32_t n_l, int32_t n_u,
+                                      int32_t expand, int32_t* action);
+
+/* InstanceHandler: the serializable proxy of an instance handed from
+ * one macro scheduler to another (no re-initialisation, no KV movement). */
+typedef struct {
+  int64_t actor_id;
+  int32_t device;
+  int32_t tp_size;
+  int32_t tp_rank;
+  int64_t kv_blocks;
+  char address[64];    /* e.g. "host:port/gpu" (NUL-terminated) */
+} ecoserve_instance_handler;
+/* Returns the encoded size (> 0) written to out, or -(needed bytes) if cap is too small. */
+int32_t ecoserve_handler_serialize(const ecoserve_instance_handler* h, uint8_t* out, int32_t cap);
+/* ECOSERVE_ERR_UNSUPPORTED on an unknown wire version, INVALID_ARG on a malformed buffer. */
+ecoserve_status ecoserve_handler_deserialize(const uint8_t* in, int32_t n, ecoserve_instance_handler* h);
+
 /* Virtual-clock discrete-event simulation of a macro instance of n identical
  * instances under the integer cost model (decision-parity mode):
  * prefill batch = sum of predicted prefill ns; decode step =

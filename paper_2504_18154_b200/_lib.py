@@ -103,6 +103,11 @@ class DesConfig(C.Structure):
                 ("token_budget", C.c_int32)]
 
 
+class InstanceHandler(C.Structure):
+    _fields_ = [("actor_id", C.c_int64), ("device", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32),
+                ("kv_blocks", C.c_int64), ("address", C.c_char * 64)]
+
+
 P = C.c_void_p
 I32, I64, F32 = C.c_int32, C.c_int64, C.c_float
 PI32, PI64, PF32 = C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_float)
@@ -132,6 +137,9 @@ SIGNATURES = {
     "ecoserve_macro_prev_idx": (I32, [P]),
     "ecoserve_macro_predict_prefill_ns": (I64, [P, I32]),
     "ecoserve_macro_destroy": (None, [P]),
+    "ecoserve_mitosis_step": (C.c_int, [PI32, PI32, I32, I32, I32, I32, PI32]),
+    "ecoserve_handler_serialize": (I32, [C.POINTER(InstanceHandler), C.POINTER(C.c_uint8), I32]),
+    "ecoserve_handler_deserialize": (C.c_int, [C.POINTER(C.c_uint8), I32, C.POINTER(InstanceHandler)]),
     "ecoserve_des_run": (C.c_int, [C.POINTER(MacroConfig), C.POINTER(DesConfig), PI64, PI32, PI32, I32, PI32,
                                    PI64, PI64, PI64, PI64, I32, PI32]),
     "ecoserve_op_gemm": (C.c_int, [P, P, I32, I32, I32, I32, P, I32, P]),

@@ -219,6 +219,132 @@ ecoserve_status ecoserve_macro_drain_deferred(ecoserve_macro* m, int64_t now_ns,
   return ECOSERVE_OK;
 }
 
+// ------------------------------------------------------------------ mitosis (N1)
+// PAPER.md Sec. 3.5.1 (Fig. 7). Expansion: add to the first macro below N_u
+// (creation order); if all are full the last one takes N_u + 1 and splits off a new
+// macro of N_l. Contraction: shrink the smallest macro (last on ties) down to N_l;
+// then shrink its partner (the other partial macro, else the last full one) until
+// the pair totals N_u; the next removal merges the pair into one macro of N_u - 1.
+ecoserve_status ecoserve_mitosis_step(int32_t* sizes, int32_t* n_macros, int32_t cap, int32_t n_l, int32_t n_u,
+                                      int32_t expand, int32_t* action) {
+  if (!sizes || !n_macros || !action || n_l < 1 || n_u < n_l || *n_macros < 0 || *n_macros > cap)
+    return ECOSERVE_ERR_INVALID_ARG;
+  int n = *n_macros;
+  action[0] = action[1] = action[2] = -1;
+  if (expand) {
+    if (n == 0) {
+      if (cap < 1) return ECOSERVE_ERR_INVALID_ARG;
+      sizes[0] = 1;
+      *n_macros = 1;
+      action[0] = ECOSERVE_MITOSIS_CREATE;
+      action[1] = 0;
+      return ECOSERVE_OK;
+    }
+    for (int i = 0; i < n; ++i)
+      if (sizes[i] < n_u) {
+        ++sizes[i];
+        action[0] = ECOSERVE_MITOSIS_ADD;
+        action[1] = i;
+        return ECOSERVE_OK;
+      }
+    if (n + 1 > cap) return ECOSERVE_ERR_INVALID_ARG;
+    sizes[n - 1] = n_u + 1 - n_l;
+    sizes[n] = n_l;
+    *n_macros = n + 1;
+    action[0] = ECOSERVE_MITOSIS_ADD_SPLIT;
+    action[1] = n - 1;
+    action[2] = n;
+    return ECOSERVE_OK;
+  }
+  if (n == 0) return ECOSERVE_ERR_STATE;
+  if (n == 1) {
+    if (sizes[0] == 1) {
+      *n_macros = 0;
+      action[0] = ECOSERVE_MITOSIS_REMOVE_MACRO;
+      action[1] = 0;
+    } else {
+      --sizes[0];
+      action[0] = ECOSERVE_MITOSIS_REMOVE;
+      action[1] = 0;
+    }
+    return ECOSERVE_OK;
+  }
+  int small = 0;
+  for (int i = 1; i < n; ++i)
+    if (sizes[i] <= sizes[small]) small = i;  // smallest, last on ties
+  if (sizes[small] > n_l) {
+    --sizes[small];
+    action[0] = ECOSERVE_MITOSIS_REMOVE;
+    action[1] = small;
+    return ECOSERVE_OK;
+  }
+  int p = -1;
+  for (int i = 0; i < n; ++i)
+    if (i != small && sizes[i] < n_u) p = i;  // last partial macro
+  if (p < 0)
+    for (int i = 0; i < n; ++i)
+      if (i != small) p = i;  // last full macro
+  const int total = sizes[small] + sizes[p];
+  if (total > n_u) {
+    --sizes[p];
+    action[0] = ECOSERVE_MITOSIS_REMOVE;
+    action[1] = p;
+    return ECOSERVE_OK;
+  }
+  const int keep = small < p ? small : p, gone = small < p ? p : small;
+  sizes[keep] = total - 1;
+  for (int i = gone; i + 1 < n; ++i) sizes[i] = sizes[i + 1];
+  *n_macros = n - 1;
+  action[0] = ECOSERVE_MITOSIS_REMOVE_MERGE;
+  action[1] = p;
+  action[2] = small;
+  return ECOSERVE_OK;
+}
+
+// InstanceHandler: the serializable proxy moved between macro schedulers.
+// Wire format v1, little-endian: u8 version | i64 actor_id | i32 device | i32 tp_size |
+// i32 tp_rank | i64 kv_blocks | u16 address length | address bytes.
+int32_t ecoserve_handler_serialize(const ecoserve_instance_handler* h, uint8_t* out, int32_t cap) {
+  if (!h) return -1;
+  int32_t alen = 0;
+  while (alen < (int32_t)sizeof(h->address) && h->address[alen]) ++alen;
+  const int32_t need = 1 + 8 + 4 + 4 + 4 + 8 + 2 + alen;
+  if (!out || cap < need) return need <= cap ? -1 : -need;
+  uint8_t* p = out;
+  auto put = [&](const void* src, int nb) {
+    memcpy(p, src, nb);  // the supported hosts are little-endian (x86-64, aarch64)
+    p += nb;
+  };
+  const uint8_t ver = 1;
+  const uint16_t al = (uint16_t)alen;
+  put(&ver, 1);
+  put(&h->actor_id, 8);
+  put(&h->device, 4);
+  put(&h->tp_size, 4);
+  put(&h->tp_rank, 4);
+  put(&h->kv_blocks, 8);
+  put(&al, 2);
+  put(h->address, alen);
+  return need;
+}
+
+ecoserve_status ecoserve_handler_deserialize(const uint8_t* in, int32_t n, ecoserve_instance_handler* h) {
+  if (!in || !h || n < 31) return ECOSERVE_ERR_INVALID_ARG;
+  if (in[0] != 1) return ECOSERVE_ERR_UNSUPPORTED;  // unknown version
+  const uint8_t* p = in + 1;
+  memset(h, 0, sizeof(*h));
+  memcpy(&h->actor_id, p, 8);
+  memcpy(&h->device, p + 8, 4);
+  memcpy(&h->tp_size, p + 12, 4);
+  memcpy(&h->tp_rank, p + 16, 4);
+  memcpy(&h->kv_blocks, p + 20, 8);
+  uint16_t al;
+  memcpy(&al, p + 28, 2);
+  if (n != 31 + al || al >= sizeof(h->address)) return ECOSERVE_ERR_INVALID_ARG;
+  memcpy(h->address, p + 30, al);
+  return ECOSERVE_OK;
+}
+
 // ------------------------------------------------------------------ DES
 ecoserve_status ecoserve_des_run(const ecoserve_macro_config* mcfg, const ecoserve_des_config* dcfg,
                                  const int64_t* arrival_ns, const int32_t* prompt_len, const int32_t* output_len,

@@ -100,6 +100,37 @@ class MacroScheduler:
         return self.lib.ecoserve_macro_predict_prefill_ns(self.h, S)
 
 
+def mitosis_step(sizes: Sequence[int], n_l: int, n_u: int, expand: bool):
+    """One mitosis expansion / contraction step (C++). Returns (new sizes, (kind, a1, a2))."""
+    lib = L.load()
+    cap = len(sizes) + 1
+    arr = (C.c_int32 * cap)(*sizes)
+    n = C.c_int32(len(sizes))
+    act = (C.c_int32 * 3)()
+    L.check(lib.ecoserve_mitosis_step(arr, C.byref(n), cap, n_l, n_u, 1 if expand else 0, act))
+    return list(arr[:n.value]), tuple(act)
+
+
+def handler_to_bytes(actor_id: int, device: int, tp_size: int, tp_rank: int, kv_blocks: int, address: str) -> bytes:
+    lib = L.load()
+    h = L.InstanceHandler(actor_id, device, tp_size, tp_rank, kv_blocks, address.encode())
+    need = -lib.ecoserve_handler_serialize(C.byref(h), None, 0)
+    buf = (C.c_uint8 * need)()
+    n = lib.ecoserve_handler_serialize(C.byref(h), buf, need)
+    if n != need:
+        raise L.EcoError(L.ERR_INVALID_ARG, "serialize")
+    return bytes(buf)
+
+
+def handler_from_bytes(b: bytes) -> dict:
+    lib = L.load()
+    buf = (C.c_uint8 * len(b)).from_buffer_copy(b)
+    h = L.InstanceHandler()
+    L.check(lib.ecoserve_handler_deserialize(buf, len(b), C.byref(h)))
+    return dict(actor_id=h.actor_id, device=h.device, tp_size=h.tp_size, tp_rank=h.tp_rank, kv_blocks=h.kv_blocks,
+                address=h.address.decode())
+
+
 def des_run(cfg: SchedConfig, arrival_ns, prompt_len, output_len, cost_d_ns=COST_DEFAULT["d"],
             cost_e_ns=COST_DEFAULT["e"], cost_f_ps=COST_DEFAULT["f"], token_budget: int = 16384):
     """Virtual-clock DES of the macro instance (C++). Returns dict of per-request
