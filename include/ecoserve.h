@@ -158,6 +158,30 @@ ecoserve_status ecoserve_prefill_phase(ecoserve_instance* inst, const ecoserve_r
 ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* req_ids, int32_t n, int32_t steps,
                                       int32_t* tokens, int32_t* n_finished);
 
+/* KV migration between instances (mitosis contraction and
+ * rebalancing move a running request with its paged KV instead of recomputing it).
+ * A request's KV is blocks of the pool's block-major layout, so it moves as
+ * n_blocks contiguous copies of ecoserve_kv_pool_bytes(shape, 64, 1) bytes each. */
+typedef struct {
+  int64_t req_id;
+  int32_t prompt_len;
+  int32_t max_new_tokens;
+  int32_t n_generated;  /* >= 1 (prefilled) */
+  int32_t last_token;   /* the token the next decode step feeds */
+  int32_t n_blocks;     /* KV blocks the request holds */
+} ecoserve_req_state;
+/* Copies the request's blocks, in logical order, into `dst` (device pointer on
+ * any device, UVA; >= n_blocks * block bytes) and its prompt into `prompt`
+ * (host, >= prompt_len); fills *state. The request stays resident (release it
+ * after the destination imported it). Synchronous. */
+ecoserve_status ecoserve_kv_export(ecoserve_instance* inst, int64_t req_id, void* dst, int64_t dst_bytes,
+                                   int32_t* prompt, int32_t prompt_cap, ecoserve_req_state* state);
+/* Allocates state->n_blocks blocks, copies them from `src` (device, any device)
+ * and registers the request so decode phases continue it. All-or-nothing:
+ * KV_EXHAUSTED / STATE (resident req_id) leave the instance unchanged. Synchronous. */
+ecoserve_status ecoserve_kv_import(ecoserve_instance* inst, const ecoserve_req_state* state, const int32_t* prompt,
+                                   const void* src);
+
 /* Free the KV blocks of the given requests and forget them. */
 ecoserve_status ecoserve_release(ecoserve_instance* inst, const int64_t* req_ids, int32_t n);
 

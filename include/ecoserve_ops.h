@@ -59,6 +59,13 @@ ecoserve_status ecoserve_op_attention_prefill(const void* q, const void* pool, i
                                               int32_t n_seq, const int32_t* block_tables, int32_t bt_ld, void* out,
                                               void* stream);
 
+/* The same prefill attention on tcgen05 (head_dim 128 only): 128-query tiles, S and
+ * P V accumulated in TMEM, K / V loaded by TMA from the pool. */
+ecoserve_status ecoserve_op_attention_prefill_tc(const void* q, const void* pool, int64_t num_blocks,
+                                                 int32_t n_heads, int32_t n_kv, const int32_t* cu_seqlens_host,
+                                                 int32_t n_seq, const int32_t* block_tables, int32_t bt_ld, void* out,
+                                                 void* stream);
+
 /* Split-K decode attention over the same pool: q bf16 [B][M][D], ctx_lens int32
  * [B] (device), out bf16 [B][M*D]. n_splits x blocks_per_split must cover the
  * longest context; workspace f32 [B][M][n_splits][D + 2]. */

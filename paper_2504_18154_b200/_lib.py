@@ -72,6 +72,11 @@ class Timing(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class ReqState(C.Structure):
+    _fields_ = [("req_id", C.c_int64), ("prompt_len", C.c_int32), ("max_new_tokens", C.c_int32),
+                ("n_generated", C.c_int32), ("last_token", C.c_int32), ("n_blocks", C.c_int32)]
+
+
 class MacroConfig(C.Structure):
     _fields_ = [("n_instances", C.c_int32), ("slo_ttft_ns", C.c_int64), ("slo_tpot_ns", C.c_int64),
                 ("reserve_tokens", C.c_int32), ("block_tokens", C.c_int32), ("probe_printed", C.c_int32),
@@ -122,6 +127,8 @@ SIGNATURES = {
     "ecoserve_prefill_phase": (C.c_int, [P, C.POINTER(Request), I32, PI32]),
     "ecoserve_decode_phase": (C.c_int, [P, PI64, I32, I32, PI32, PI32]),
     "ecoserve_release": (C.c_int, [P, PI64, I32]),
+    "ecoserve_kv_export": (C.c_int, [P, I64, P, I64, PI32, I32, C.POINTER(ReqState)]),
+    "ecoserve_kv_import": (C.c_int, [P, C.POINTER(ReqState), PI32, P]),
     "ecoserve_get_status": (C.c_int, [P, C.POINTER(InstanceStatus), C.POINTER(ReqStatus), I32]),
     "ecoserve_debug_hidden": (C.c_int, [P, I64, I32, PF32]),
     "ecoserve_set_profiling": (C.c_int, [P, I32]),
@@ -149,6 +156,7 @@ SIGNATURES = {
     "ecoserve_op_lm_argmax": (C.c_int, [P, P, I32, I32, I32, P, P, P, P]),
     "ecoserve_op_rmsnorm": (C.c_int, [P, P, P, P, I32, I32, F32, P]),
     "ecoserve_op_attention_prefill": (C.c_int, [P, P, I64, I32, I32, I32, PI32, I32, P, I32, P, P]),
+    "ecoserve_op_attention_prefill_tc": (C.c_int, [P, P, I64, I32, I32, PI32, I32, P, I32, P, P]),
     "ecoserve_op_attention_decode": (C.c_int, [P, P, I32, I32, I32, P, I32, P, I32, I32, I32, P, P, P]),
 }
 

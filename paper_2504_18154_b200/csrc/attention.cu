@@ -408,12 +408,8 @@ __global__ void attn_combine_kernel(DecodeAttnArgs a) {
 template <int D>
 static cudaError_t prefill_d(const PrefillAttnArgs& a, cudaStream_t s) {
   const int smem = 5 * 64 * D * 2;
-  static bool cfg = false;
-  if (!cfg) {
-    cudaError_t e = cudaFuncSetAttribute(attn_prefill_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    cfg = true;
-  }
+  cudaError_t e = ensure_smem(attn_prefill_kernel<D>, smem);
+  if (e != cudaSuccess) return e;
   if (a.n_tiles == 0) return cudaSuccess;
   return launch_k(attn_prefill_kernel<D>, dim3(a.n_tiles, a.n_heads), dim3(128), smem, s, a);
 }
@@ -432,15 +428,11 @@ static cudaError_t decode_d(const DecodeAttnArgs& a, cudaStream_t s) {
   int smem = (2 * DEC_STAGES * 64 * D + 16 * D) * 2;
   const int red_bytes = 4 * 16 * (D + 2) * 4;
   if (smem < red_bytes) smem = red_bytes;
-  static bool cfg = false;
-  if (!cfg) {
-    cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    cfg = true;
-  }
+  cudaError_t e = ensure_smem(attn_decode_kernel<D>, smem);
+  if (e != cudaSuccess) return e;
   if (a.B == 0) return cudaSuccess;
   if (a.n_heads / a.n_kv > 16) return cudaErrorInvalidValue;
-  cudaError_t e = launch_k(attn_decode_kernel<D>, dim3(a.B, a.n_kv, a.n_splits), dim3(128), smem, s, a);
+  e = launch_k(attn_decode_kernel<D>, dim3(a.B, a.n_kv, a.n_splits), dim3(128), smem, s, a);
   if (e != cudaSuccess || a.n_splits == 1) return e;
   return launch_k(attn_combine_kernel<D>, dim3(a.B, a.n_heads), dim3(D), 0, s, a);
 }

@@ -143,6 +143,8 @@ struct ecoserve_instance {
   const bf16 *embed = nullptr, *lm_head = nullptr, *final_norm = nullptr;
   std::vector<LayerW> lw;
   CUtensorMap lm_a;
+  bool attn_tc = false;          // tcgen05 prefill attention (head_dim 128) in use
+  CUtensorMap attn_qmap, attn_kvmap;
   // workspace
   float* x = nullptr;            // [T_max][H] residual stream
   bf16* h = nullptr;             // [T_max][H] normed GEMM input
@@ -416,6 +418,15 @@ ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, cons
     inst->err = "cuTensorMapEncodeTiled failed (activations)";
     return ECOSERVE_ERR_CUDA;
   }
+  {  // tcgen05 prefill attention for head_dim 128 unless ECOSERVE_ATTN_TC=0
+    const char* ev = getenv("ECOSERVE_ATTN_TC");
+    inst->attn_tc = D == 128 && !(ev && ev[0] == '0');
+    const int64_t pool_rows = inst->num_blocks * (int64_t)L * 2 * Mkv * BLOCK;
+    if (inst->attn_tc && make_attn_tc_maps(&inst->attn_qmap, &inst->attn_kvmap, inst->q, T, M, inst->pool, pool_rows)) {
+      inst->err = "cuTensorMapEncodeTiled failed (attention)";
+      return ECOSERVE_ERR_CUDA;
+    }
+  }
   const int nmax = std::max(QKV, std::max(2 * F, H));
   inst->part_elems = 8LL * inst->B_max * nmax;
   CK(cudaMalloc(&inst->part, sizeof(float) * inst->part_elems));
@@ -608,7 +619,12 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
     a.n_heads = M;
     a.n_kv = inst->Mkv;
     a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
-    LAUNCH(P_ATTN_PREFILL, attn_flop, 1, attn_prefill_launch(a, D, st));
+    if (inst->attn_tc)
+      LAUNCH(P_ATTN_PREFILL, attn_flop, 1,
+             attn_prefill_tc_launch(&inst->attn_qmap, &inst->attn_kvmap, d_cu, d_bt, bt_ld, d_tiles, n_tiles, inst->ao,
+                                    M, inst->Mkv, l, inst->L, st));
+    else
+      LAUNCH(P_ATTN_PREFILL, attn_flop, 1, attn_prefill_launch(a, D, st));
     GemmEpi eo = resid_epi(inst);
     eo.mode = resid_mode_prefill(inst);
     LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * M * D, 1,
@@ -641,7 +657,8 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
   const float eps = inst->shape.rms_eps;
   LAUNCH(P_OTHER, 0, 1, embed_launch(d_ids, inst->embed, inst->x, B, H, st));
   if (inst->debug) CK(cudaMemcpyAsync(inst->dbg, inst->x, sizeof(float) * (int64_t)B * H, cudaMemcpyDeviceToDevice, st));
-  // split the context so that B x Mkv x splits fills the SMs about twice
+  // split the context only as much as needed for B x Mkv x splits to fill the SMs about
+  // twice (uniform 512-token chunks were measured slower: more CTAs, partials, combine)
   int n_splits = std::max(1, (2 * inst->num_sms + B * inst->Mkv - 1) / (B * inst->Mkv));
   n_splits = std::min(std::min(n_splits, max_blocks), 64);
   const int bps = (max_blocks + n_splits - 1) / n_splits;
@@ -741,6 +758,7 @@ ecoserve_status ecoserve_prefill_phase(ecoserve_instance* inst, const ecoserve_r
   if (inst->dead) return ECOSERVE_ERR_CUDA;
   if (n < 0 || (n > 0 && (!reqs || !first_tokens))) return ECOSERVE_ERR_INVALID_ARG;
   if (n == 0) return ECOSERVE_OK;
+  CK(cudaSetDevice(inst->device));  // the calling thread may have another current device
   // ---- validate everything first (all-or-nothing)
   int64_t need_blocks = 0;
   {
@@ -796,7 +814,7 @@ ecoserve_status ecoserve_prefill_phase(ecoserve_instance* inst, const ecoserve_r
     // q tiles, longest-first
     std::vector<std::pair<int, int>> tiles;
     for (int i = i0; i < i1; ++i)
-      for (int qs = 0; qs < rs[i]->S; qs += 64) tiles.push_back({i - i0, qs});
+      for (int qs = 0; qs < rs[i]->S; qs += inst->attn_tc ? 128 : 64) tiles.push_back({i - i0, qs});
     std::stable_sort(tiles.begin(), tiles.end(),
                      [](const std::pair<int, int>& a, const std::pair<int, int>& b) { return a.second > b.second; });
     // pack metadata: ids[T] pos[T] slot[T] cu[ns+1] rows[ns] bt[ns][bt_ld] tiles[2*nt]
@@ -867,6 +885,7 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
   if (inst->dead) return ECOSERVE_ERR_CUDA;
   if (n < 0 || steps < 0 || (n > 0 && (!req_ids || !tokens))) return ECOSERVE_ERR_INVALID_ARG;
   if (n > inst->B_max) return ECOSERVE_ERR_INVALID_ARG;
+  CK(cudaSetDevice(inst->device));
   std::vector<Req*> rs(n);
   for (int i = 0; i < n; ++i) {
     auto it = inst->reqs.find(req_ids[i]);
@@ -958,6 +977,62 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
     for (int i = 0; i < n; ++i) c += rs[i]->finished ? 1 : 0;
     *n_finished = c;
   }
+  return ECOSERVE_OK;
+}
+
+ecoserve_status ecoserve_kv_export(ecoserve_instance* inst, int64_t req_id, void* dst, int64_t dst_bytes,
+                                   int32_t* prompt, int32_t prompt_cap, ecoserve_req_state* state) {
+  if (!inst || !dst || !state) return ECOSERVE_ERR_INVALID_ARG;
+  if (inst->dead) return ECOSERVE_ERR_CUDA;
+  auto it = inst->reqs.find(req_id);
+  if (it == inst->reqs.end() || it->second.n_gen < 1) return ECOSERVE_ERR_STATE;
+  const Req& r = it->second;
+  const int64_t bb = inst->blk_stride * (int64_t)sizeof(bf16);
+  if (dst_bytes < bb * (int64_t)r.blocks.size() || (prompt && prompt_cap < r.S)) return ECOSERVE_ERR_INVALID_ARG;
+  CK(cudaSetDevice(inst->device));
+  for (size_t b = 0; b < r.blocks.size(); ++b)  // one contiguous span per block (all layers, K and V)
+    CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(dst) + b * bb, inst->pool + (int64_t)r.blocks[b] * inst->blk_stride,
+                       bb, cudaMemcpyDefault, inst->stream));
+  CK(cudaStreamSynchronize(inst->stream));
+  if (prompt) memcpy(prompt, r.prompt.data(), sizeof(int32_t) * r.S);
+  state->req_id = r.id;
+  state->prompt_len = r.S;
+  state->max_new_tokens = r.max_new;
+  state->n_generated = r.n_gen;
+  state->last_token = r.last_token;
+  state->n_blocks = (int32_t)r.blocks.size();
+  return ECOSERVE_OK;
+}
+
+ecoserve_status ecoserve_kv_import(ecoserve_instance* inst, const ecoserve_req_state* st, const int32_t* prompt,
+                                   const void* src) {
+  if (!inst || !st || !prompt || !src || st->prompt_len < 1 || st->n_generated < 1 || st->n_blocks < 0)
+    return ECOSERVE_ERR_INVALID_ARG;
+  if (inst->dead) return ECOSERVE_ERR_CUDA;
+  const int64_t kv_len = (int64_t)st->prompt_len + st->n_generated - 1;  // tokens whose K/V are stored
+  if (st->n_blocks != (int)((kv_len + BLOCK - 1) / BLOCK) || st->prompt_len + st->max_new_tokens > inst->P_max)
+    return ECOSERVE_ERR_INVALID_ARG;
+  if (inst->reqs.count(st->req_id)) return ECOSERVE_ERR_STATE;
+  if ((int64_t)inst->free_blocks.size() < st->n_blocks) return ECOSERVE_ERR_KV_EXHAUSTED;
+  CK(cudaSetDevice(inst->device));
+  Req r;
+  r.id = st->req_id;
+  r.S = st->prompt_len;
+  r.max_new = st->max_new_tokens;
+  r.n_gen = st->n_generated;
+  r.last_token = st->last_token;
+  r.finished = r.n_gen >= r.max_new;
+  r.prompt.assign(prompt, prompt + r.S);
+  const int64_t bb = inst->blk_stride * (int64_t)sizeof(bf16);
+  for (int b = 0; b < st->n_blocks; ++b) {
+    r.blocks.push_back(inst->free_blocks.back());
+    inst->free_blocks.pop_back();
+  }
+  for (int b = 0; b < st->n_blocks; ++b)
+    CK(cudaMemcpyAsync(inst->pool + (int64_t)r.blocks[b] * inst->blk_stride,
+                       reinterpret_cast<const uint8_t*>(src) + b * bb, bb, cudaMemcpyDefault, inst->stream));
+  CK(cudaStreamSynchronize(inst->stream));
+  inst->reqs[r.id] = std::move(r);
   return ECOSERVE_OK;
 }
 

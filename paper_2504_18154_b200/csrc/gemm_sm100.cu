@@ -693,12 +693,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 cudaError_t gemm2_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K,
                          const GemmEpi& epi, int num_sms, cudaStream_t stream) {
   if (epi.mode >= EPI_SWAP_F32) return cudaErrorInvalidValue;  // prefill (non-swapped) epilogues only
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Cfg::SMEM);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = ensure_smem(gemm_tc2_kernel, Gemm2Cfg::SMEM);
+  if (e != cudaSuccess) return e;
   const int work = ((m_rows + 255) / 256) * ((n_rows + 255) / 256);
   int clusters = num_sms / 2;
   if (work < clusters) clusters = work;
@@ -728,6 +724,24 @@ int make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols
   cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)r;
+}
+
+int make_tmap_bf16_nd(CUtensorMap* map, const void* ptr, int rank, const int64_t* dims, const int64_t* strides_bytes,
+                      const int* box) {
+  auto enc = get_encode();
+  if (!enc || rank < 1 || rank > 5) return -1;
+  cuuint64_t d[5], s[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = (cuuint64_t)dims[i];
+    b[i] = (cuuint32_t)box[i];
+    e[i] = 1;
+  }
+  for (int i = 0; i < rank - 1; ++i) s[i] = (cuuint64_t)strides_bytes[i];
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), d, s, b, e,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : (int)r;
@@ -782,12 +796,8 @@ template <int BN, int R>
 static cudaError_t launch_bn(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K,
                              int splits, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
   using C = GemmCfg<BN, R>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = ensure_smem(gemm_tc_kernel<BN, R>, C::SMEM);
+  if (e != cudaSuccess) return e;
   const int m_tiles = (m_rows + BM * C::RT - 1) / (BM * C::RT), n_tiles = (n_rows + BN - 1) / BN;
   const int work = m_tiles * n_tiles * splits;
   const int grid = work < num_sms ? work : num_sms;

@@ -68,6 +68,9 @@ int gemm_decode_splits(int m_rows, int K, int num_sms);
 
 // Creates a 2D bf16 tensor map (rows x cols, row-major, 128B swizzle, box 64 x box_rows).
 int make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int box_rows);
+// General bf16 tensor map, 128B swizzle: dims[0] innermost; strides_bytes[i] of dim i+1.
+int make_tmap_bf16_nd(CUtensorMap* map, const void* ptr, int rank, const int64_t* dims, const int64_t* strides_bytes,
+                      const int* box);
 
 // Launch; tile width bn in {64, 128, 256}; splits > 1 only with EPI_SWAP_F32.
 cudaError_t gemm_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K, int bn,
@@ -102,6 +105,15 @@ struct PrefillAttnArgs {
   float scale_log2;         // log2(e) / sqrt(D)
 };
 cudaError_t attn_prefill_launch(const PrefillAttnArgs& a, int head_dim, cudaStream_t s);
+
+// Prefill causal attention on tcgen05 (head_dim 128): 128-query tiles, K/V by TMA from the
+// block-major pool. qmap: 3D map over q [q_rows][n_heads][128]; kvmap: 2D map over the pool
+// as rows of 128 elements (rows = num_blocks * L * 2 * Mkv * 64).
+int make_attn_tc_maps(CUtensorMap* qmap, CUtensorMap* kvmap, const void* q, int64_t q_rows, int n_heads,
+                      const void* pool, int64_t pool_rows);
+cudaError_t attn_prefill_tc_launch(const CUtensorMap* qmap, const CUtensorMap* kvmap, const int* cu_seqlens,
+                                   const int* block_tables, int bt_ld, const int* tiles, int n_tiles, bf16* out,
+                                   int n_heads, int n_kv, int layer, int n_layers, cudaStream_t s);
 
 // Decode split-K paged attention + combine.
 struct DecodeAttnArgs {

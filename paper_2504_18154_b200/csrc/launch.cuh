@@ -8,6 +8,10 @@
 #include <cuda_runtime.h>
 #include <stdlib.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 namespace eco {
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -20,6 +24,24 @@ inline bool pdl_enabled() {
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
+}
+
+// Sets the kernel's max dynamic smem once per device (function attributes are per
+// device context; instances may live on several GPUs of one process).
+template <typename... KArgs>
+inline cudaError_t ensure_smem(void (*kernel)(KArgs...), int bytes) {
+  // keyed by (kernel, device): kernels of the same signature must not share the flag
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const std::pair<const void*, int> key(reinterpret_cast<const void*>(kernel), dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(key)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert(key);
+  return e;
 }
 
 template <typename... KArgs, typename... Args>

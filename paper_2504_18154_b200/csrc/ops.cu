@@ -179,6 +179,34 @@ ecoserve_status ecoserve_op_attention_prefill(const void* q, const void* pool, i
   return e == cudaSuccess ? ECOSERVE_OK : ECOSERVE_ERR_CUDA;
 }
 
+ecoserve_status ecoserve_op_attention_prefill_tc(const void* q, const void* pool, int64_t num_blocks,
+                                                 int32_t n_heads, int32_t n_kv, const int32_t* cu_seqlens_host,
+                                                 int32_t n_seq, const int32_t* block_tables, int32_t bt_ld, void* out,
+                                                 void* stream) {
+  if (!q || !pool || !cu_seqlens_host || !block_tables || !out || n_seq < 1 || n_heads % n_kv || num_blocks < 1)
+    return ECOSERVE_ERR_INVALID_ARG;
+  std::vector<int> tiles;
+  for (int s = 0; s < n_seq; ++s) {
+    const int len = cu_seqlens_host[s + 1] - cu_seqlens_host[s];
+    if (len < 1 || (len + 63) / 64 > bt_ld) return ECOSERVE_ERR_INVALID_ARG;
+    for (int qs = 0; qs < len; qs += 128) { tiles.push_back(s); tiles.push_back(qs); }
+  }
+  CUtensorMap qm, km;
+  if (make_attn_tc_maps(&qm, &km, q, cu_seqlens_host[n_seq], n_heads, pool, num_blocks * 2 * n_kv * 64))
+    return ECOSERVE_ERR_CUDA;
+  int* d = nullptr;
+  const size_t bytes = sizeof(int) * (tiles.size() + n_seq + 1);
+  OPCK(cudaMallocAsync((void**)&d, bytes, (cudaStream_t)stream));
+  OPCK(cudaMemcpyAsync(d, cu_seqlens_host, sizeof(int) * (n_seq + 1), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  OPCK(cudaMemcpyAsync(d + n_seq + 1, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice,
+                       (cudaStream_t)stream));
+  const cudaError_t e = attn_prefill_tc_launch(&qm, &km, d, block_tables, bt_ld, d + n_seq + 1,
+                                               (int)tiles.size() / 2, (bf16*)out, n_heads, n_kv, 0, 1,
+                                               (cudaStream_t)stream);
+  cudaFreeAsync(d, (cudaStream_t)stream);
+  return e == cudaSuccess ? ECOSERVE_OK : ECOSERVE_ERR_CUDA;
+}
+
 ecoserve_status ecoserve_op_attention_decode(const void* q, const void* pool, int32_t n_heads, int32_t n_kv,
                                              int32_t head_dim, const int32_t* ctx_lens, int32_t B,
                                              const int32_t* block_tables, int32_t bt_ld, int32_t n_splits,

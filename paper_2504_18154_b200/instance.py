@@ -161,6 +161,27 @@ class Instance:
                                                toks.ctypes.data_as(L.PI32), C.byref(nf)), self.h)
         return toks, nf.value
 
+    @property
+    def block_bytes(self) -> int:
+        return self.lib.ecoserve_kv_pool_bytes(C.byref(self.cshape), 64, 1)
+
+    def migrate_to(self, other: "Instance", req_id: int) -> dict:
+        """Move a running request with its paged KV to `other` (any GPU): export
+        into a staging buffer on the destination device (peer copy over NVLink),
+        import there, release here (mitosis contraction / rebalancing, N1)."""
+        st = L.ReqState()
+        _, reqs = self.status()
+        info = next(r for r in reqs if r["req_id"] == req_id)
+        stage = torch.empty(max(1, info["n_blocks"]) * self.block_bytes, dtype=torch.uint8, device=other.device)
+        prompt = np.zeros(info["prompt_len"], dtype=np.int32)
+        L.check(self.lib.ecoserve_kv_export(self.h, int(req_id), C.c_void_p(stage.data_ptr()), stage.numel(),
+                                            prompt.ctypes.data_as(L.PI32), len(prompt), C.byref(st)), self.h)
+        L.check(other.lib.ecoserve_kv_import(other.h, C.byref(st), prompt.ctypes.data_as(L.PI32),
+                                             C.c_void_p(stage.data_ptr())), other.h)
+        self.release([req_id])
+        return dict(req_id=st.req_id, n_blocks=st.n_blocks, bytes=st.n_blocks * self.block_bytes,
+                    n_generated=st.n_generated)
+
     def release(self, req_ids: Sequence[int]) -> None:
         ids = np.ascontiguousarray(req_ids, dtype=np.int64)
         L.check(self.lib.ecoserve_release(self.h, ids.ctypes.data_as(L.PI64), len(ids)), self.h)

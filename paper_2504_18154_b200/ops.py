@@ -90,6 +90,16 @@ def attention_prefill(q, pool, num_blocks, n_heads, n_kv, head_dim, cu_seqlens, 
     return out
 
 
+def attention_prefill_tc(q, pool, num_blocks, n_heads, n_kv, cu_seqlens, block_tables):
+    T = q.shape[0]
+    out = torch.empty(T, n_heads * 128, dtype=torch.bfloat16, device=q.device)
+    cu = np.ascontiguousarray(cu_seqlens, dtype=np.int32)
+    L.check(L.load().ecoserve_op_attention_prefill_tc(q.data_ptr(), pool.data_ptr(), num_blocks, n_heads, n_kv,
+                                                      cu.ctypes.data_as(L.PI32), len(cu) - 1, block_tables.data_ptr(),
+                                                      block_tables.shape[1], out.data_ptr(), _s()))
+    return out
+
+
 def attention_decode(q, pool, n_heads, n_kv, head_dim, ctx_lens, block_tables, n_splits, blocks_per_split):
     B = q.shape[0]
     out = torch.empty(B, n_heads * head_dim, dtype=torch.bfloat16, device=q.device)

@@ -1,0 +1,72 @@
+"""Edge cases of the phase calls against the fp64 oracle (GPU): empty calls, G = 1
+requests (finished by the prefill phase), prompts of exactly one / two KV blocks
+and one token, a long prompt spanning many 128-query tiles, decode batches above
+one 128-token GEMM tile (B = 300 -> three N tiles), B = 1, and decode calls on
+finished requests (-1 tokens)."""
+import numpy as np
+import pytest
+
+from oracle import transformer as T
+from synthetic.shapes import get_shape
+from synthetic.traces import random_prompts
+from synthetic.weights import make_weights
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def setup():
+    from paper_2504_18154_b200.instance import Instance, device_weights_from_host
+    shape = get_shape("tiny-d128")          # head_dim 128: the tcgen05 attention path
+    w = make_weights(shape, seed=0)
+    inst = Instance(shape, device_weights_from_host(w, "cuda:0"), 1024, 0, token_budget=4096, max_batch=512,
+                    max_positions=4096, debug_hidden=True)
+    yield shape, w, T.Model(shape, w.as_f64()), inst
+    inst.close()
+
+
+def tokens_match(model, prompt, got, margin=5e-2):
+    toks, outs = model.generate(list(prompt), len(got))
+    for k, g in enumerate(got):
+        if g != toks[k]:
+            assert T.top2_margin(outs[k].logits) <= margin, k
+            return k
+    return len(got)
+
+
+def test_empty_calls(setup):
+    _, _, _, inst = setup
+    assert len(inst.prefill([])) == 0
+    toks, nf = inst.decode([], 3)
+    assert toks.shape == (0, 3) and nf == 0
+
+
+def test_block_boundaries_and_g1(setup):
+    shape, _, model, inst = setup
+    lens = [1, 64, 128, 129, 1500]
+    prompts = random_prompts(21, lens, shape.vocab)
+    first = inst.prefill([(1000 + i, p, 1 if i == 0 else 5) for i, p in enumerate(prompts)])
+    st, rs = inst.status()
+    assert next(r for r in rs if r["req_id"] == 1000)["finished"]        # G = 1: done at prefill
+    for i, p in enumerate(prompts):
+        out = model.prefill(list(p))[1]
+        got = inst.hidden(1000 + i, shape.n_layers, len(p))
+        assert np.max(np.abs(got - out.hidden[-1])) / np.max(np.abs(out.hidden[-1])) <= 1e-2
+    toks, nf = inst.decode([1000 + i for i in range(len(lens))], 4)
+    assert (toks[0] == -1).all() and nf == len(lens)                    # finished request: -1
+    for i in range(1, len(lens)):
+        assert tokens_match(model, prompts[i], [first[i]] + list(toks[i])) >= 2
+    inst.release([1000 + i for i in range(len(lens))])
+
+
+@pytest.mark.parametrize("B", [1, 300])
+def test_decode_batch_sizes(setup, B):
+    shape, _, model, inst = setup
+    prompts = random_prompts(30 + B, [int(x) for x in np.random.default_rng(B).integers(2, 60, B)], shape.vocab)
+    first = inst.prefill([(5000 + i, p, 4) for i, p in enumerate(prompts)])
+    toks, nf = inst.decode([5000 + i for i in range(B)], 3)
+    assert nf == B
+    for i in range(0, B, max(1, B // 12)):
+        assert tokens_match(model, prompts[i], [first[i]] + list(toks[i])) >= 1
+    inst.release([5000 + i for i in range(B)])
+    assert inst.status()[0]["blocks_used"] == 0

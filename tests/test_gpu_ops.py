@@ -151,6 +151,30 @@ def test_attention_prefill(ops, D, M, Mkv):
         assert rel_err(got[cu[i]:cu[i + 1]], ref) < 1e-2, (i, S)
 
 
+@pytest.mark.parametrize("M,Mkv,lens", [(8, 2, [1, 63, 64, 65, 200, 130]), (32, 8, [128, 129, 255, 256, 520, 7]),
+                                         (4, 4, [1000, 3])])
+def test_attention_prefill_tcgen05(ops, M, Mkv, lens):
+    D = 128
+    rng = np.random.default_rng(M + len(lens))
+    nb = [(s + 63) // 64 for s in lens]
+    n_blocks = sum(nb) + 3
+    pool_h, pool_d = make_pool(rng, n_blocks, Mkv, D)
+    perm = rng.permutation(n_blocks)
+    bt = np.zeros((len(lens), max(nb)), dtype=np.int32)
+    k = 0
+    for i, b in enumerate(nb):
+        bt[i, :b] = perm[k:k + b]
+        k += b
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    q_h, q_d = bf16_rand(rng, (cu[-1], M, D))
+    got = ops.attention_prefill_tc(q_d, pool_d, n_blocks, M, Mkv, cu, torch.from_numpy(bt).cuda()).float().cpu().numpy()
+    for i, S in enumerate(lens):
+        ks = np.stack([pool_h[bt[i, t // 64], 0, :, t % 64, :] for t in range(S)])
+        vs = np.stack([pool_h[bt[i, t // 64], 1, :, t % 64, :] for t in range(S)])
+        ref = T.attention(q_h[cu[i]:cu[i + 1]], ks, vs, np.arange(S), np.arange(S)).reshape(S, M * D)
+        assert rel_err(got[cu[i]:cu[i + 1]], ref) < 1e-2, (i, S)
+
+
 @pytest.mark.parametrize("D,M,Mkv,splits,bps", [(128, 32, 8, 1, 64), (128, 32, 8, 4, 5), (32, 8, 2, 3, 7),
                                                  (128, 64, 8, 2, 9), (64, 4, 4, 1, 64)])
 def test_attention_decode(ops, D, M, Mkv, splits, bps):
