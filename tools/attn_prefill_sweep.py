@@ -9,7 +9,19 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2504_18154_b200 import ops  # noqa: E402
-from tools.gemm_prefill_sweep import timeit  # noqa: E402
+
+
+def timeit(fn, iters=10):
+    """Plain CUDA-event timing (the op wrappers copy host metadata, so no graph capture)."""
+    fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters * 1e3
 
 
 def main():
