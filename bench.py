@@ -224,8 +224,16 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         torch.cuda.synchronize()
         with ClockSampler(local_rank) as clk:
             t0 = time.perf_counter()
-            for _ in range(args.steps):
+            for k in range(args.steps):
+                # ECOSERVE_NCU_RANGE=1: the first timed step is the profiler range
+                # (`ncu --profile-from-start off` then records exactly one step)
+                rng_on = k == 0 and level == 1 and os.environ.get("ECOSERVE_NCU_RANGE") == "1"
+                if rng_on:
+                    torch.cuda.cudart().cudaProfilerStart()
                 step()
+                if rng_on:
+                    torch.cuda.synchronize()
+                    torch.cuda.cudart().cudaProfilerStop()
             torch.cuda.synchronize()
             wall = time.perf_counter() - t0
         if world > 1:

@@ -35,15 +35,36 @@ struct GemmCfg {
   static constexpr int A_BYTES = RT * BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = R == 3 ? 3 : (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  // epilogue staging: half an accumulator tile in f32 (BN/2 tokens x 128 features) for
+  // the bulk-store epilogues (BN <= 128, one A tile); otherwise just the argmax scratch
+  static constexpr bool BULK_EPI = BN <= 128 && RT == 1;
+  static constexpr int STAGING = BULK_EPI ? (BN / 2) * BM * 4 : 4 * BN * 8;
+  static constexpr int SMEM_MAX = 232448;  // 227 KB opt-in per CTA
+  static constexpr int FIT = (SMEM_MAX - 1024 - 256 - STAGING) / STAGE_BYTES;
+  static constexpr int STAGES = R == 3 ? 3 : FIT > 8 ? 8 : FIT;
   static constexpr int ACC_COLS = RT * BN;  // one accumulator stage
   static constexpr int TMEM_COLS = (2 * ACC_COLS) <= 32 ? 32 : (2 * ACC_COLS) <= 64 ? 64 : (2 * ACC_COLS) <= 128 ? 128
                                  : (2 * ACC_COLS) <= 256 ? 256 : 512;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + STAGING + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(4 * BN * 8 <= STAGING, "argmax scratch lives in the staging buffer");
   static_assert(2 * ACC_COLS <= 512, "two accumulator stages must fit the 512 TMEM columns");
 };
 
-__device__ __forceinline__ float silu_f(float z) { return z / (1.f + __expf(-z)); }
+__device__ __forceinline__ void trace_mark(const GemmEpi& e, int i) {
+  if (e.trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    e.trace[blockIdx.x * 16 + i] = t;
+  }
+}
+
+// fast-math division: the IEEE "/" slow path (zero / tiny numerators) stalls the epilogue
+__device__ __forceinline__ long long clk() { return clock64(); }
+__device__ __forceinline__ void trace_put(const GemmEpi& e, int i, long long v) {
+  if (e.trace) e.trace[blockIdx.x * 16 + i] = (unsigned long long)v;
+}
+
+__device__ __forceinline__ float silu_f(float z) { return __fdividef(z, 1.f + __expf(-z)); }
 
 // ---------------------------------------------------------------- epilogues
 // Non-swapped: this thread owns output row `m` (token), columns n0..n0+31 in v[].
@@ -232,14 +253,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   constexpr int R = C::RT;  // 128-row A tiles per work unit
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* staging = smem + C::STAGES * C::STAGE_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(staging + C::STAGING);
   uint64_t* empty_bar = full_bar + C::STAGES;
   uint64_t* tfull_bar = empty_bar + C::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_base_ptr = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  __shared__ float am_v[4][BN];
-  __shared__ int am_i[4][BN];
-  __shared__ int s_last;
+  int& s_last = *reinterpret_cast<int*>(tmem_base_ptr + 1);
+  auto am_v = reinterpret_cast<float(*)[BN]>(staging);               // [4][BN] argmax scratch
+  auto am_i = reinterpret_cast<int(*)[BN]>(staging + 4 * BN * 4);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int m_tiles = (m_rows + BM * R - 1) / (BM * R);  // work units of R x 128 rows
@@ -247,8 +269,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int kb_total = (K + BK - 1) / BK;
   const int kb_per = (kb_total + splits - 1) / splits;
   const int n_work = m_tiles * n_tiles * splits;
+  // bulk-store epilogue: f32 partials / SiLU output with 16-byte aligned token rows
+  const bool bulk_epi =
+      C::BULK_EPI && (reinterpret_cast<uintptr_t>(epi.out) & 15) == 0 &&
+      ((epi.mode == EPI_SWAP_F32 && m_rows % 4 == 0 && epi.ldo % 4 == 0) ||
+       (epi.mode == EPI_SWAP_SILU && splits == 1 && m_rows % 16 == 0 && epi.ldo % 8 == 0));
 
   if (threadIdx.x == 0) {
+    trace_mark(epi, 0);  // CTA start
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -271,6 +299,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // prologue done (smem, barriers, TMEM, descriptor prefetch): let the next kernel launch.
   // Threads wait for the previous kernel (PDL) right before their first dependent access.
   pdl_trigger();
+  if (threadIdx.x == 0) trace_mark(epi, 1);  // prologue done
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -322,6 +351,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tma_load_2d(sb, &mapB, &full_bar[stage], kb * BK, nt * BN);
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
+      trace_mark(epi, 6);  // last load issued
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -331,6 +361,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      bool first = true;
       for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
         const int ks = w % splits;
         const int kb0 = ks * kb_per, kb1 = min(kb_total, kb0 + kb_per);
@@ -340,6 +371,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
+          if (first) { trace_mark(epi, 2); first = false; }  // first stage landed
           const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t sb = sa + C::A_BYTES;
           const uint64_t db = umma_desc_sw128(sb);
@@ -358,6 +390,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tc_commit(&tfull_bar[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
+      trace_mark(epi, 3);  // last MMA issued
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -372,6 +405,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int mt = t / n_tiles, nt = t % n_tiles;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+      if (threadIdx.x == 64) trace_mark(epi, 5);  // accumulator ready
       const int row = q * 32 + lane;  // accumulator row (TMEM lane)
       const int m = mt * BM * R + row;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::ACC_COLS;
@@ -414,6 +448,77 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
+      } else if (C::BULK_EPI && bulk_epi) {
+        // accumulator -> smem, transposed to [token][feature] -> 16-byte coalesced row
+        // stores (instead of 128 scattered 4-byte stores per thread), half a tile at a time
+        const bool silu = epi.mode == EPI_SWAP_SILU;
+        constexpr int HALF = BN / 2;
+        const int m0 = mt * BM;
+        const int mcount = min(BM, m_rows - m0);
+        const int vec_per_row = silu ? mcount / 16 : mcount / 4;     // 16-byte vectors per token row
+        const int stg_row = silu ? BM / 2 * 2 : BM * 4;              // staging row bytes
+        char* gbase = silu ? reinterpret_cast<char*>(reinterpret_cast<bf16*>(epi.out) + m0 / 2)
+                           : reinterpret_cast<char*>(reinterpret_cast<float*>(epi.out) +
+                                                     (int64_t)ks * n_rows * epi.ldo + m0);
+        const int64_t gstride = silu ? epi.ldo * 2 : epi.ldo * 4;
+        const uint32_t stg_base = smem_u32(staging);
+        long long c_wr = 0, c_ld = 0, c_math = 0, c_out = 0, c0_ = 0;
+        for (int h = 0; h < 2; ++h) {
+          c0_ = clk();
+          asm volatile("bar.sync 1, 128;" ::: "memory");  // staging free (previous copy-out done)
+          c_wr += clk() - c0_;
+#pragma unroll 1
+          for (int cc = 0; cc < HALF; cc += 32) {
+            uint32_t v[32];
+            c0_ = clk();
+            tmem_ld32(tbase + h * HALF + cc, v);
+            tc_wait_ld();
+            const long long c1_ = clk();
+            c_ld += c1_ - c0_;
+            c0_ = c1_;
+            if (silu) {
+              // lanes 2j / 2j+1 hold gate_j / up_j; one exchange per token pair gives the
+              // even lane (gate, up) of token i and the odd lane those of token i + 1
+              const bool odd = lane & 1;
+              const uint32_t sbase = stg_base + (uint32_t)(row / 2) * 2u;
+#pragma unroll
+              for (int i = 0; i < 32; i += 2) {
+                const float send = odd ? __uint_as_float(v[i]) : __uint_as_float(v[i + 1]);
+                const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
+                const float g = odd ? recv : __uint_as_float(v[i]);
+                const float u = odd ? __uint_as_float(v[i + 1]) : recv;
+                const int tok = cc + i + (odd ? 1 : 0);
+                sts_u16(sbase + (uint32_t)(tok * stg_row), __bfloat16_as_ushort(__float2bfloat16_rn(silu_f(g) * u)));
+              }
+            } else {
+              const uint32_t sbase = stg_base + (uint32_t)row * 4u;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) sts_f32(sbase + (uint32_t)((cc + i) * stg_row), __uint_as_float(v[i]));
+            }
+            c_math += clk() - c0_;
+          }
+          c0_ = clk();
+          if (h == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");  // staging complete
+          const int n0 = nt * BN + h * HALF;
+          const int rows = min(HALF, n_rows - n0);
+          for (int idx = ep_tid; idx < rows * vec_per_row; idx += 128) {
+            const int r = idx / vec_per_row, c = idx % vec_per_row;
+            const uint4 val = lds128(stg_base + (uint32_t)(r * stg_row + c * 16));
+            *reinterpret_cast<uint4*>(gbase + (int64_t)(n0 + r) * gstride + c * 16) = val;
+          }
+          c_out += clk() - c0_;
+        }
+        if (threadIdx.x == 64) {
+          trace_put(epi, 8, c_wr);
+          trace_put(epi, 9, c_ld);
+          trace_put(epi, 10, c_math);
+          trace_put(epi, 11, c_out);
+        }
       } else if (epi.mode == EPI_SWAP_F32) {
         float* out = reinterpret_cast<float*>(epi.out) + (int64_t)ks * n_rows * epi.ldo;
 #pragma unroll 1
@@ -513,6 +618,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (lane == 0) mbar_arrive(&tempty_bar[acc]);
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (threadIdx.x == 64) trace_mark(epi, 4);  // (last) epilogue done
     }
   }
   tc_fence_before();

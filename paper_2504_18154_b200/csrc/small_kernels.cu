@@ -199,7 +199,7 @@ cudaError_t splitk_resid_rmsnorm_launch(const float* part, int splits, int rows,
                   eps);
 }
 
-__device__ __forceinline__ float silu_r(float z) { return z / (1.f + __expf(-z)); }
+__device__ __forceinline__ float silu_r(float z) { return __fdividef(z, 1.f + __expf(-z)); }
 
 // part [split][row][ld_part] f32; one thread per (row, column pair).
 __global__ void splitk_reduce_kernel(int mode, const float* __restrict__ part, int splits, int rows, int cols,
