@@ -40,6 +40,13 @@ ecoserve_status ecoserve_op_gemm_swap_bf16(const void* W, const void* X, int32_t
 ecoserve_status ecoserve_op_gemm_decode(const void* W, const void* X, int32_t m, int32_t n, int32_t k, int32_t r,
                                         int32_t splits, float* ws, float* out, int32_t bn, void* stream);
 
+/* Decode GEMM with the K split over the CTAs of a thread-block cluster and the split
+ * reduction in distributed shared memory (no partials in HBM): out f32 [n][m] =
+ * X W^T, partials summed in split order. splits 2..4 (clamped so every split owns a
+ * K block; ECOSERVE_ERR_INVALID_ARG outside), bn 64 or 128. */
+ecoserve_status ecoserve_op_gemm_cluster(const void* W, const void* X, int32_t m, int32_t n, int32_t k,
+                                         int32_t splits, float* out, int32_t bn, void* stream);
+
 /* Greedy LM head (rows a12/a16): tokens[i] = argmax_v (X [n][k] W[v][k]^T), lowest
  * v on ties, logits never materialised. workspace: f32 [n][ceil(V/128)] and
  * i32 [n][ceil(V/128)]. */

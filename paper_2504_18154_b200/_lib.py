@@ -152,6 +152,7 @@ SIGNATURES = {
     "ecoserve_op_gemm": (C.c_int, [P, P, I32, I32, I32, I32, P, I32, P]),
     "ecoserve_op_gemm_swap": (C.c_int, [P, P, I32, I32, I32, I32, P, P, I32, P]),
     "ecoserve_op_gemm_swap_bf16": (C.c_int, [P, P, I32, I32, I32, I32, P, P, P, I32, P]),
+    "ecoserve_op_gemm_cluster": (C.c_int, [P, P, I32, I32, I32, I32, P, I32, P]),
     "ecoserve_op_gemm_decode": (C.c_int, [P, P, I32, I32, I32, I32, I32, P, P, I32, P]),
     "ecoserve_op_lm_argmax": (C.c_int, [P, P, I32, I32, I32, P, P, P, P]),
     "ecoserve_op_rmsnorm": (C.c_int, [P, P, P, P, I32, I32, F32, P]),

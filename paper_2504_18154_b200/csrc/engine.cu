@@ -548,6 +548,20 @@ int decode_variant() {  // 1: 1-CTA/SM GEMM (default); 3: lean (co-resident with
   return v;
 }
 
+// Off by default: standalone the cluster kernel beats partials + reduction (O 12.8 vs
+// 11.5 + 7 us), but inside the decode step it measured 15-20 us slower per launch
+// (bench r01: decode 11.7k vs 13.8k tok/s) -- clusters need whole free GPC slices, so
+// they cannot start while the previous kernel's CTAs drain under PDL.
+// ECOSERVE_CLUSTER_SPLITK=1 enables it.
+bool use_cluster_splitk() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_CLUSTER_SPLITK");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 // norm_gamma / norm_out (optional): when the projection is a residual add split over K,
 // its reduction is fused with the following RMSNorm (one kernel: x += sum of partials,
 // out = rmsnorm(x) * gamma); *fused reports whether that happened.
@@ -563,6 +577,20 @@ cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const 
     e.mode = mode;
     *nk = 1;
     return gemm_launch_r(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, var, 1, e, inst->num_sms, inst->stream);
+  }
+  // split-K over a thread-block cluster, reduced in distributed shared memory with the
+  // epilogue in the same kernel (no partials in HBM; ECOSERVE_CLUSTER_SPLITK=0 disables)
+  if (use_cluster_splitk() && splits <= 4) {
+    // fewer splits when the clusters of `splits` CTAs would not all be resident at once
+    const int tiles = ((n_out + 127) / 128) * ((B + bn - 1) / bn);
+    int sc = splits;
+    while (sc >= 2 && gemm_cluster_max_active(bn, sc) < tiles) --sc;
+    sc = sc >= 2 ? gemm_effective_splits(K, sc) : 0;
+    if (sc >= 2) {
+      e.mode = mode;
+      *nk = 1;
+      return gemm_cluster_launch(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, sc, e, inst->stream);
+    }
   }
   // split-K: f32 partials, then one fixed-order reduction kernel applying the epilogue
   GemmEpi ge = e;

@@ -13,6 +13,9 @@
 #include <cudaTypedefs.h>
 #include <stdio.h>
 
+#include <map>
+#include <mutex>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "launch.cuh"
@@ -627,6 +630,276 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 1) {
     __syncwarp();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------- cluster split-K decode GEMM
+// Swap-AB decode projection with its K range split over the S CTAs of one thread-block
+// cluster (one 128-feature weight tile per cluster). The split partials are reduced
+// through distributed shared memory instead of HBM: CTA `rank` owns the token columns
+// [rank*CW, rank*CW + CW) of the tile; every CTA pushes the columns it does not own to
+// their owner (st.shared::cluster, [slot][token][feature] f32) and release-arrives on
+// the owner's mbarrier; the owner sums all S partials in rank order (the same order as
+// the f32-partials reduction kernel, so results are bit-identical to it) and applies
+// the epilogue (QKV RoPE + paged KV write, residual add, SiLU, bf16) to its columns.
+// No partial buffer, no reduction kernel.
+template <int BN, int S>
+struct ClusterCfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int CW = 16 * ((BN / 16 + S - 1) / S);  // token columns owned per rank
+  static constexpr int RECV = (S - 1) * CW * BM * 4;
+  static constexpr int FIT = (232448 - 1024 - 256 - RECV) / STAGE_BYTES;
+  static constexpr int STAGES = FIT > 8 ? 8 : FIT;
+  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + RECV + 1024 + 256;
+};
+
+template <int BN, int S>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_cluster_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                        int m_rows, int n_rows, int K, GemmEpi epi) {
+  using C = ClusterCfg<BN, S>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* recv = smem + C::STAGES * C::STAGE_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(recv + C::RECV);
+  uint64_t* empty_bar = full_bar + C::STAGES;
+  uint64_t* tfull_bar = empty_bar + C::STAGES;
+  uint64_t* recv_full = tfull_bar + 1;
+  uint32_t* tmem_base_ptr = reinterpret_cast<uint32_t*>(recv_full + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int rank = blockIdx.x % S;  // == %cluster_ctarank (1-D clusters of S CTAs along x)
+  const int tile = blockIdx.x / S;
+  const int m_tiles = (m_rows + BM - 1) / BM;
+  const int mt = tile % m_tiles, nt = tile / m_tiles;
+  const int kb_total = (K + BK - 1) / BK;
+  const int kb_per = (kb_total + S - 1) / S;
+  const int kb0 = rank * kb_per, kb1 = min(kb_total, kb0 + kb_per);
+
+  if (threadIdx.x == 0) {
+    trace_mark(epi, 0);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(tfull_bar, 1);
+    mbar_init(recv_full, (S - 1) * 128);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapB);
+  }
+  if (warp == 1) tmem_alloc(tmem_base_ptr, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // every CTA's barriers are initialised before any remote arrive
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_ptr;
+  pdl_trigger();
+  if (threadIdx.x == 0) trace_mark(epi, 1);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // weights (independent of the previous kernel) into the first stages before the PDL wait
+      const int n = kb1 - kb0;
+      const int npre = min(n, C::STAGES);
+      for (int i = 0; i < npre; ++i) {
+        mbar_arrive_expect_tx(&full_bar[i], C::STAGE_BYTES);
+        tma_load_2d(smem + i * C::STAGE_BYTES, &mapA, &full_bar[i], (kb0 + i) * BK, mt * BM);
+      }
+      pdl_wait();
+      for (int i = 0; i < npre; ++i)
+        tma_load_2d(smem + i * C::STAGE_BYTES + C::A_BYTES, &mapB, &full_bar[i], (kb0 + i) * BK, nt * BN);
+      int stage = npre % C::STAGES;
+      uint32_t phase = npre == C::STAGES ? 1 : 0;
+      for (int i = npre; i < n; ++i) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * C::STAGE_BYTES;
+        mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+        tma_load_2d(sa, &mapA, &full_bar[stage], (kb0 + i) * BK, mt * BM);
+        tma_load_2d(sa + C::A_BYTES, &mapB, &full_bar[stage], (kb0 + i) * BK, nt * BN);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+      trace_mark(epi, 6);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (kb == kb0) trace_mark(epi, 2);
+        const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
+        const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + C::A_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) tc_mma_f16(tmem_base, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+        tc_commit(&empty_bar[stage]);
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+      tc_commit(tfull_bar);
+      trace_mark(epi, 3);
+    }
+  } else {
+    pdl_wait();
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int m = mt * BM + row;
+    const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16);
+    const int n_base = nt * BN;
+    const int n_valid = min(BN, n_rows - n_base);
+    const uint32_t recv_u32 = smem_u32(recv);
+    mbar_wait(tfull_bar, 0);
+    tc_fence_after();
+    if (threadIdx.x == 64) trace_mark(epi, 5);
+    // 1) push the columns owned by the other ranks
+#pragma unroll 1
+    for (int o = 0; o < S; ++o) {
+      if (o == rank) continue;
+      const int lo = o * C::CW, hi = min(min(BN, lo + C::CW), n_valid);
+      const int slot = rank < o ? rank : rank - 1;
+      const uint32_t rb = mapa_u32(recv_u32 + (uint32_t)(slot * C::CW * BM * 4), (uint32_t)o);
+      // receive layout [slot][token / 4][feature][4]: one 16-byte store per 4 tokens, a warp
+      // writes 512 contiguous bytes (columns past `hi` are never read by the owner)
+#pragma unroll 1
+      for (int c = lo; c < hi; c += 16) {
+        uint32_t v[16];
+        tmem_ld16(tbase + c, v);
+        tc_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+          if (c + i < hi)
+            st_cluster_v4(rb + (uint32_t)((((c - lo + i) >> 2) * BM + row) * 16), __uint_as_float(v[i]),
+                          __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+      }
+      mbar_arrive_remote(mapa_u32(smem_u32(recv_full), (uint32_t)o));
+    }
+    // 2) own columns: sum the S partials in rank order, then the epilogue
+    const int lo = rank * C::CW, hi = min(min(BN, lo + C::CW), n_valid);
+    if (S > 1) mbar_wait_cluster(recv_full, 0);
+#pragma unroll 1
+    for (int c = lo; c < hi; c += 32) {
+      float f[32];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (c + 16 * h < hi) {  // warp-uniform
+          uint32_t v[16];
+          tmem_ld16(tbase + c + 16 * h, v);
+          tc_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            const int j = c + 16 * h + i - lo;  // token column within the owned range (multiple of 4)
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+              float4 part;
+              if (s == rank) {
+                part = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
+                                   __uint_as_float(v[i + 3]));
+              } else {
+                const int slot = s < rank ? s : s - 1;
+                part = lds_f32x4(recv_u32 + (uint32_t)(((slot * (C::CW / 4) + (j >> 2)) * BM + row) * 16));
+              }
+              acc.x += part.x;
+              acc.y += part.y;
+              acc.z += part.z;
+              acc.w += part.w;
+            }
+            f[16 * h + i] = acc.x;
+            f[16 * h + i + 1] = acc.y;
+            f[16 * h + i + 2] = acc.z;
+            f[16 * h + i + 3] = acc.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) f[16 * h + i] = 0.f;
+        }
+      }
+      epi_swap(epi, m, m_rows, n_base + c, n_base + hi, lane, f);
+    }
+    if (threadIdx.x == 64) trace_mark(epi, 4);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    __syncwarp();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+template <int BN, int S>
+static cudaError_t launch_cluster(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K,
+                                  const GemmEpi& epi, cudaStream_t stream) {
+  using C = ClusterCfg<BN, S>;
+  cudaError_t e = ensure_smem(gemm_cluster_kernel<BN, S>, C::SMEM);
+  if (e != cudaSuccess) return e;
+  const int tiles = ((m_rows + BM - 1) / BM) * ((n_rows + BN - 1) / BN);
+  if (tiles <= 0) return cudaSuccess;
+  return launch_kc(gemm_cluster_kernel<BN, S>, dim3(tiles * S), dim3(GEMM_THREADS), C::SMEM, stream, S, *mapA, *mapB,
+                   m_rows, n_rows, K, epi);
+}
+
+template <int BN, int S>
+static int max_active_clusters() {
+  using C = ClusterCfg<BN, S>;
+  if (ensure_smem(gemm_cluster_kernel<BN, S>, C::SMEM) != cudaSuccess) return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(S * 64);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_cluster_kernel<BN, S>, &cfg) != cudaSuccess) return 0;
+  return n;
+}
+
+int gemm_cluster_max_active(int bn, int splits) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, int> cache;  // (device, key)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int key = bn * 10 + splits;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find({dev, key});
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  switch (key) {
+    case 642: n = max_active_clusters<64, 2>(); break;
+    case 643: n = max_active_clusters<64, 3>(); break;
+    case 644: n = max_active_clusters<64, 4>(); break;
+    case 1282: n = max_active_clusters<128, 2>(); break;
+    case 1283: n = max_active_clusters<128, 3>(); break;
+    case 1284: n = max_active_clusters<128, 4>(); break;
+    default: n = 0;
+  }
+  cache[{dev, key}] = n;
+  return n;
+}
+
+cudaError_t gemm_cluster_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K,
+                                int bn, int splits, const GemmEpi& epi, cudaStream_t stream) {
+  if (epi.mode < EPI_SWAP_BF16 || gemm_effective_splits(K, splits) != splits) return cudaErrorInvalidValue;
+  const int key = bn * 10 + splits;
+  switch (key) {
+    case 642: return launch_cluster<64, 2>(mapA, mapB, m_rows, n_rows, K, epi, stream);
+    case 643: return launch_cluster<64, 3>(mapA, mapB, m_rows, n_rows, K, epi, stream);
+    case 644: return launch_cluster<64, 4>(mapA, mapB, m_rows, n_rows, K, epi, stream);
+    case 1282: return launch_cluster<128, 2>(mapA, mapB, m_rows, n_rows, K, epi, stream);
+    case 1283: return launch_cluster<128, 3>(mapA, mapB, m_rows, n_rows, K, epi, stream);
+    case 1284: return launch_cluster<128, 4>(mapA, mapB, m_rows, n_rows, K, epi, stream);
+    default: return cudaErrorInvalidValue;
   }
 }
 

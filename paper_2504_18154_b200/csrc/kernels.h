@@ -82,6 +82,13 @@ cudaError_t gemm_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_
 cudaError_t gemm_launch_r(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K, int bn,
                           int r, int splits, const GemmEpi& epi, int num_sms, cudaStream_t stream);
 int gemm_smem_bytes(int bn);
+// Swap-AB decode GEMM with K split over the CTAs of a thread-block cluster (splits 2..4,
+// bn 64 / 128) and the split reduction done in distributed shared memory; swapped
+// in-kernel epilogues (modes >= EPI_SWAP_BF16). splits must equal gemm_effective_splits.
+cudaError_t gemm_cluster_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K,
+                                int bn, int splits, const GemmEpi& epi, cudaStream_t stream);
+// How many clusters of `splits` CTAs of that kernel can be resident at once (0 if unsupported).
+int gemm_cluster_max_active(int bn, int splits);
 // CTA-pair (cta_group::2) 256 x 256-tile variant for the non-swapped (prefill) epilogues.
 // mapA box 128 rows (A), mapB box 128 rows (half of the 256 B rows of a tile).
 cudaError_t gemm2_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K,

@@ -87,6 +87,23 @@ ecoserve_status ecoserve_op_gemm_swap_bf16(const void* W, const void* X, int32_t
   return ECOSERVE_OK;
 }
 
+ecoserve_status ecoserve_op_gemm_cluster(const void* W, const void* X, int32_t m, int32_t n, int32_t k,
+                                         int32_t splits, float* out, int32_t bn, void* stream) {
+  if (!W || !X || !out || m < 1 || n < 1 || k < 1 || k % 8 || m % 2 || (bn != 64 && bn != 128))
+    return ECOSERVE_ERR_INVALID_ARG;
+  const int eff = gemm_effective_splits(k, splits);
+  if (eff < 2 || eff > 4) return ECOSERVE_ERR_INVALID_ARG;
+  CUtensorMap ma, mb;
+  if (make_tmap_bf16(&ma, W, m, k, 128) || make_tmap_bf16(&mb, X, n, k, bn)) return ECOSERVE_ERR_CUDA;
+  GemmEpi e;
+  memset(&e, 0, sizeof(e));
+  e.mode = EPI_SWAP_STORE;
+  e.resid = out;
+  e.ldr = m;
+  OPCK(gemm_cluster_launch(&ma, &mb, m, n, k, bn, eff, e, (cudaStream_t)stream));
+  return ECOSERVE_OK;
+}
+
 ecoserve_status ecoserve_op_gemm_decode(const void* W, const void* X, int32_t m, int32_t n, int32_t k, int32_t r,
                                         int32_t splits, float* ws, float* out, int32_t bn, void* stream) {
   if (!W || !X || !out || m < 1 || n < 1 || k < 1 || k % 8 || m % 2 || splits < 1 || r < 1 || r > 3 ||

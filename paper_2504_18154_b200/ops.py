@@ -58,6 +58,15 @@ def gemm_decode(W: torch.Tensor, X: torch.Tensor, r: int = 2, splits: int = 1, b
     return out
 
 
+def gemm_cluster(W: torch.Tensor, X: torch.Tensor, splits: int, bn: int = 128) -> torch.Tensor:
+    """out f32 [n][m] = X W^T, K split over a thread-block cluster, reduced in DSMEM."""
+    m, k = W.shape
+    n = X.shape[0]
+    out = torch.empty(n, m, dtype=torch.float32, device=W.device)
+    L.check(L.load().ecoserve_op_gemm_cluster(W.data_ptr(), X.data_ptr(), m, n, k, splits, out.data_ptr(), bn, _s()))
+    return out
+
+
 def lm_argmax(W: torch.Tensor, X: torch.Tensor) -> torch.Tensor:
     V, k = W.shape
     n = X.shape[0]

@@ -84,6 +84,20 @@ def test_gemm_decode_dual_tile(ops, m, n, k, r, splits, bn):
     assert rel_err(got, x @ w.T) < 1e-5
 
 
+@pytest.mark.parametrize("m,n,k,splits,bn", [(640, 37, 1024, 2, 64), (640, 37, 1024, 3, 128), (6144, 128, 4096, 3, 128),
+                                             (4096, 128, 4096, 4, 128), (4096, 200, 14336, 4, 128), (300, 5, 192, 3, 64),
+                                             (256, 64, 256, 4, 64)])
+def test_gemm_cluster_splitk(ops, m, n, k, splits, bn):
+    """split reduction through distributed shared memory == f32-partials path, bit for bit"""
+    rng = np.random.default_rng(m + n + k + splits)
+    w, W = bf16_rand(rng, (m, k), 1.0 / np.sqrt(k))
+    x, X = bf16_rand(rng, (n, k))
+    got = ops.gemm_cluster(W, X, splits, bn).cpu().numpy()
+    assert rel_err(got, x @ w.T) < 1e-5
+    ref = ops.gemm_swap(W, X, splits, bn).cpu().numpy()
+    assert np.array_equal(got, ref)
+
+
 @pytest.mark.parametrize("V,n,k",[(1000, 5, 256), (32000, 64, 1024), (4097, 130, 512)])
 def test_lm_argmax(ops, V, n, k):
     rng = np.random.default_rng(V + n)

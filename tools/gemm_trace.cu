@@ -32,6 +32,8 @@ int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int B = 128, COPIES = 8;
+  printf("{\"max_active_clusters\": {\"2\": %d, \"3\": %d, \"4\": %d}}\n", gemm_cluster_max_active(128, 2),
+         gemm_cluster_max_active(128, 3), gemm_cluster_max_active(128, 4));
   Shape shapes[] = {{"qkv", 6144, 4096, EPI_SWAP_F32}, {"o", 4096, 4096, EPI_SWAP_F32},
                     {"gu", 28672, 4096, EPI_SWAP_SILU}, {"down", 4096, 14336, EPI_SWAP_F32}};
   bf16* x;
@@ -55,7 +57,7 @@ int main() {
     }
     CUtensorMap xm;
     make_tmap_bf16(&xm, x, B, sh.k, 128);
-    for (int splits_req : {0, 2, 4}) {
+    for (int splits_req : {0, 2, 3, 4}) {
       int splits = splits_req == 0 ? gemm_decode_splits(sh.m, sh.k, sms) : splits_req;
       if (sh.mode == EPI_SWAP_SILU && splits > 1) continue;
       GemmEpi e;
@@ -68,6 +70,54 @@ int main() {
         e.trace = tr;
         return gemm_launch_r(&wm[i % COPIES], &xm, sh.m, B, sh.k, 128, 1, splits, e, sms, st);
       };
+      if (sh.mode == EPI_SWAP_F32 && splits >= 2 && splits <= 4) {
+        // the cluster split-K variant (DSMEM reduction + epilogue in one kernel), f32 store epilogue
+        GemmEpi ec;
+        memset(&ec, 0, sizeof(ec));
+        ec.mode = EPI_SWAP_STORE;
+        ec.resid = part;
+        ec.ldr = sh.m;
+        ec.indep = 1;
+        const int eff = gemm_effective_splits(sh.k, splits);
+        for (int i = 0; i < 8; ++i) gemm_cluster_launch(&wm[i % COPIES], &xm, sh.m, B, sh.k, 128, eff, ec, st);
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, st);
+        for (int i = 0; i < 40; ++i) gemm_cluster_launch(&wm[i % COPIES], &xm, sh.m, B, sh.k, 128, eff, ec, st);
+        cudaEventRecord(b, st);
+        cudaError_t err = cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        // traced launch: epilogue phases of the cluster kernel
+        cudaStreamSynchronize(st);
+        cudaMemset(trace, 0, 16 * 1024 * 8);
+        ec.trace = trace;
+        gemm_cluster_launch(&wm[3], &xm, sh.m, B, sh.k, 128, eff, ec, st);
+        ec.trace = nullptr;
+        cudaStreamSynchronize(st);
+        const int cgrid = ((sh.m + 127) / 128) * eff;
+        std::vector<unsigned long long> tc(cgrid * 16);
+        cudaMemcpy(tc.data(), trace, cgrid * 16 * 8, cudaMemcpyDeviceToHost);
+        unsigned long long T0 = ~0ull, T1 = 0;
+        double mma = 0, epi = 0, first = 0;
+        for (int c = 0; c < cgrid; ++c) {
+          T0 = std::min(T0, tc[c * 16]);
+          T1 = std::max(T1, tc[c * 16 + 4]);
+        }
+        double last_start = 0;
+        for (int c = 0; c < cgrid; ++c) {
+          const unsigned long long* r = &tc[c * 16];
+          first += (double)(r[2] - r[0]);
+          mma += (double)(r[3] - r[2]);
+          epi += (double)(r[4] - r[5]);
+          last_start = std::max(last_start, (double)(r[0] - T0));
+        }
+        printf("{\"op\": \"%s\", \"variant\": \"cluster\", \"splits\": %d, \"us_stream\": %.2f, \"gbs_stream\": %.0f, "
+               "\"span_us\": %.2f, \"last_cta_start_us\": %.2f, \"avg_first_us\": %.2f, \"avg_mma_us\": %.2f, \"avg_epi_us\": %.2f, \"err\": \"%s\"}\n",
+               sh.name, eff, ms * 1e3 / 40, (double)sh.m * sh.k * 2 / 1e9 / (ms / 40) * 1e3, (T1 - T0) / 1e3,
+               last_start / 1e3, first / cgrid / 1e3, mma / cgrid / 1e3, epi / cgrid / 1e3, cudaGetErrorString(err));
+      }
       for (int i = 0; i < 8; ++i) launch(i, nullptr);
       cudaEvent_t a, b;
       cudaEventCreate(&a);
