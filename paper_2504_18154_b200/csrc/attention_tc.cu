@@ -1,21 +1,26 @@
 // Prefill causal varlen attention on the 5th-generation tensor cores (SURVEY 8(a)
-// row a8; Eq. 2). One CTA = one 128-query tile of one
-// sequence x one q head, head_dim 128, K/V streamed 64 tokens (= one paged-pool
-// block) at a time by TMA straight out of the pool through the block table.
+// row a8; Eq. 2). One CTA = one 128-query tile of one sequence x
+// HP (= 2 when the GQA group is even) q heads of the same kv head, head_dim 128; K/V
+// stream 64 tokens (= one paged-pool block) at a time by TMA straight out of the pool
+// through the block table (4-stage ring), shared by the HP heads.
 //
-//   warp 0     TMA producer: Q tile once, then K / V blocks into a 3-stage ring
-//   warp 1     TMEM owner + single-thread MMA issuer:
-//                S_j = Q K_j^T      (M=128, N=64,  K=128; A, B K-major)   -> TMEM S[j%2]
-//                O_j = P_j V_j      (M=128, N=128, K=64;  B = V MN-major) -> TMEM O[j%2]
-//   warps 2-5  softmax: thread r owns query row r (TMEM lane r). Per block it loads
-//              its S row, applies the causal mask and the exp2 online softmax,
-//              writes P (bf16) as a K-major 128B-swizzled smem tile for the next
-//              MMA, and folds O_{j-1} into fp32 registers with the running
-//              rescale (the MMA writes each block's P V into a fresh TMEM
-//              buffer, so no TMEM read-modify-write is needed).
-// S and O are double buffered in TMEM (2 x 64 + 2 x 128 of 512 columns), so the
-// tensor core computes S_{j+1} and O_j while the softmax warps work on block j.
+//   warp 0          TMA producer: the HP Q tiles once, then K / V blocks
+//   warp 1          TMEM owner + single-thread MMA issuer, per block j and head e:
+//                     S_e[j%2] = Q_e K_j^T     (M=128, N=64, K=128; A, B K-major, smem)
+//                     O_e     += P_e[j%2] V_j  (M=128, N=128, K=64; A = P from TMEM,
+//                                               B = V MN-major from smem)
+//                   issue order per block: PV(j, e) then S(j+2, e) -- S is double
+//                   buffered, so the scores of the next block are always ready when
+//                   the softmax warps finish the current one.
+//   warps 2..       4 softmax warps per head; thread r owns query row r (TMEM lane). Per
+//                   block: load the S row, causal mask, exp2 online softmax with a lazily
+//                   updated running max (O in TMEM is rescaled only when the max grows by
+//                   more than 2^8 -- the stale max keeps P <= 256, exact after the final
+//                   1/l), P (bf16 pairs) written back over its own S columns (tcgen05.st)
+//                   as the A operand of the PV MMA.
+// TMEM per head e: S[0] / S[1] at columns e*256 + {0, 64}, O at e*256 + [128, 256).
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -27,13 +32,18 @@ namespace {
 constexpr int TQ = 128;   // queries per tile
 constexpr int TK = 64;    // keys per block (= KV block of the pool)
 constexpr int HD = 128;   // head dim
-constexpr int KV_STAGES = 3;
-constexpr int Q_BYTES = TQ * HD * 2;          // 32 KB: 2 panels [128][64]
+constexpr int KV_STAGES = 4;
+constexpr int Q_BYTES = TQ * HD * 2;          // 32 KB per head: 2 panels [128][64]
 constexpr int K_BYTES = TK * HD * 2;          // 16 KB: 2 panels [64][64]
 constexpr int V_BYTES = TK * HD * 2;          // 16 KB: 2 panels [64 keys][64 d]
-constexpr int P_BYTES = TQ * TK * 2;          // 16 KB: 1 panel [128][64]
-constexpr int SMEM = Q_BYTES + KV_STAGES * (K_BYTES + V_BYTES) + 2 * P_BYTES + 1024 + 512;
-constexpr int S_COL = 0, O_COL = 128;         // TMEM columns: S[2] at 0 / 64, O[2] at 128 / 256
+constexpr float RESCALE_LOG2 = 8.f;           // rescale O when the row max grows by > 2^8
+
+template <int HP>
+struct AttnCfg {
+  static constexpr int THREADS = 64 + 128 * HP;
+  static constexpr int SMEM = HP * Q_BYTES + KV_STAGES * (K_BYTES + V_BYTES) + 1024 + 512;
+  static constexpr int TMEM_COLS = HP == 2 ? 512 : 256;
+};
 
 // instruction descriptor, bf16 x bf16 -> f32, A K-major, B K-major (b_mn = 0) or MN-major (1)
 __host__ __device__ constexpr uint32_t idesc(int M, int N, int b_mn) {
@@ -60,6 +70,37 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ float fast_ex2(float x) {  // MUFU.EX2, flush-to-zero; 2^-inf = 0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// O[tmem] (+)= A[tmem] * B[smem desc]: A (M x 16 bf16 per step, K-major) read from TMEM,
+// 16 bf16 = 8 columns per K step
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 }  // namespace
 
 struct TcAttnParams {
@@ -70,31 +111,33 @@ struct TcAttnParams {
   bf16* out;               // [T][M*128]
   int n_heads, n_kv, layer, n_layers;
   float scale_log2;
+  int pv_wait;             // experiment switch: wait for PV(j) before S(j+2) reuses its buffer
 };
 
-__global__ void __launch_bounds__(192, 1)
+template <int HP>
+__global__ void __launch_bounds__(AttnCfg<HP>::THREADS, 1)
     attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kvmap,
                            TcAttnParams p) {
+  using C = AttnCfg<HP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm;
-  uint8_t* sKV = sQ + Q_BYTES;                               // stage s: K at s*(K+V), V after it
-  uint8_t* sP = sKV + KV_STAGES * (K_BYTES + V_BYTES);       // [2][P_BYTES]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * P_BYTES);
+  uint8_t* sQ = sm;                                          // [HP][Q_BYTES]
+  uint8_t* sKV = sQ + HP * Q_BYTES;                          // stage s: K at s*(K+V), V after it
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + KV_STAGES * (K_BYTES + V_BYTES));
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_full = q_full + 1;
   uint64_t* kv_empty = kv_full + KV_STAGES;
-  uint64_t* s_full = kv_empty + KV_STAGES;
-  uint64_t* s_empty = s_full + 2;
-  uint64_t* p_full = s_empty + 2;
-  uint64_t* p_empty = p_full + 2;
-  uint64_t* o_full = p_empty + 2;
-  uint64_t* o_empty = o_full + 2;
-  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(o_empty + 2);
+  uint64_t* s_full = kv_empty + KV_STAGES;   // [HP][2]
+  uint64_t* p_full = s_full + 2 * HP;        // [HP][2]
+  // o_done[e][b]: PV(j, e) complete for blocks j = b (mod 2). Two barriers alternating by
+  // block parity: a consumer lagging by several blocks can then never mistake a later
+  // phase for the one it waits on (PV(j + 2) needs P_{j+2}, which it has not produced)
+  uint64_t* o_done = p_full + 2 * HP;        // [HP][2]
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(o_done + 2 * HP);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int tile = blockIdx.x, h = blockIdx.y;
-  const int G = p.n_heads / p.n_kv, kvh = h / G;
+  const int tile = blockIdx.x, h0 = blockIdx.y * HP;
+  const int G = p.n_heads / p.n_kv, kvh = h0 / G;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -102,13 +145,12 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&s_full[s], 1);
-      mbar_init(&s_empty[s], 4);
-      mbar_init(&p_full[s], 4);
-      mbar_init(&p_empty[s], 1);
-      mbar_init(&o_full[s], 1);
-      mbar_init(&o_empty[s], 4);
+    for (int e = 0; e < HP; ++e) {
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&o_done[2 * e + b], 1);
+        mbar_init(&s_full[2 * e + b], 1);
+        mbar_init(&p_full[2 * e + b], 4);
+      }
     }
     fence_barrier_init();
   }
@@ -116,7 +158,7 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch(&qmap);
     tma_prefetch(&kvmap);
   }
-  if (warp == 1) tmem_alloc(tmem_ptr, 512);
+  if (warp == 1) tmem_alloc(tmem_ptr, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -132,8 +174,10 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, Q_BYTES);
-      for (int pn = 0; pn < 2; ++pn) tma_load_3d(sQ + pn * (TQ * 128), &qmap, q_full, pn * 64, h, tok0 + q_start);
+      mbar_arrive_expect_tx(q_full, HP * Q_BYTES);
+      for (int e = 0; e < HP; ++e)
+        for (int pn = 0; pn < 2; ++pn)
+          tma_load_3d(sQ + e * Q_BYTES + pn * (TQ * 128), &qmap, q_full, pn * 64, h0 + e, tok0 + q_start);
       for (int j = 0; j < n_kv; ++j) {
         const int s = j % KV_STAGES;
         if (j >= KV_STAGES) mbar_wait(&kv_empty[s], ((j / KV_STAGES) - 1) & 1);
@@ -154,130 +198,160 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       constexpr uint32_t id_s = idesc(TQ, TK, 0);
       constexpr uint32_t id_o = idesc(TQ, HD, 1);
-      const uint32_t aq = smem_u32(sQ);
-      auto issue_s = [&](int j) {
-        const int s = j % KV_STAGES;
-        mbar_wait(&kv_full[s], (j / KV_STAGES) & 1);
-        tc_fence_after();
-        const uint32_t ak = smem_u32(sKV + s * (K_BYTES + V_BYTES));
-        const uint32_t d = tmem + S_COL + (j & 1) * TK;
+      // S_e[j % 2] = Q_e K_j^T (the caller has waited for K_j)
+      auto mma_s = [&](int j, int e) {
+        const uint32_t ak = smem_u32(sKV + (j % KV_STAGES) * (K_BYTES + V_BYTES));
+        const uint32_t aq = smem_u32(sQ + e * Q_BYTES);
+        const uint32_t d = tmem + e * 256 + (j & 1) * 64;
 #pragma unroll
         for (int pn = 0; pn < 2; ++pn) {
           const uint64_t da = umma_desc_sw128(aq + pn * (TQ * 128)), db = umma_desc_sw128(ak + pn * (TK * 128));
 #pragma unroll
           for (int k = 0; k < 4; ++k) tc_mma_f16(d, da + 2 * k, db + 2 * k, id_s, (pn | k) ? 1u : 0u);
         }
-        tc_commit(&s_full[j & 1]);
+        tc_commit(&s_full[2 * e + (j & 1)]);
+      };
+      auto wait_k = [&](int j) {
+        mbar_wait(&kv_full[j % KV_STAGES], (j / KV_STAGES) & 1);
+        tc_fence_after();
       };
       mbar_wait(q_full, 0);
       tc_fence_after();
-      if (n_kv > 0) issue_s(0);
+      for (int j = 0; j < 2 && j < n_kv; ++j) {
+        wait_k(j);
+        for (int e = 0; e < HP; ++e) mma_s(j, e);
+      }
       for (int j = 0; j < n_kv; ++j) {
-        if (j + 1 < n_kv) {
-          if (j + 1 >= 2) mbar_wait(&s_empty[(j + 1) & 1], (((j + 1) >> 1) - 1) & 1);
-          tc_fence_after();
-          issue_s(j + 1);
-        }
-        // O_j = P_j V_j into a fresh TMEM buffer
-        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
-        if (j >= 2) mbar_wait(&o_empty[j & 1], ((j >> 1) - 1) & 1);
-        tc_fence_after();
         const int s = j % KV_STAGES;
-        const uint32_t ap = smem_u32(sP + (j & 1) * P_BYTES);
         const uint32_t av = smem_u32(sKV + s * (K_BYTES + V_BYTES) + K_BYTES);
-        const uint32_t d = tmem + O_COL + (j & 1) * HD;
-        const uint64_t da = umma_desc_sw128(ap);
+        const bool next = j + 2 < n_kv;
+        if (next) wait_k(j + 2);
 #pragma unroll
-        for (int k = 0; k < TK / 16; ++k)  // 16 keys per MMA: +32 B along P rows, +2 x 1024 B along V rows
-          tc_mma_f16(d, da + 2 * k, desc_mn_sw128(av + k * 2048, TK * 128), id_o, k ? 1u : 0u);
-        tc_commit(&o_full[j & 1]);
-        tc_commit(&kv_empty[s]);
-        tc_commit(&p_empty[j & 1]);
+        for (int e = 0; e < HP; ++e) {
+          mbar_wait(&p_full[2 * e + (j & 1)], (j >> 1) & 1);
+          tc_fence_after();
+          const uint32_t ap = tmem + e * 256 + (j & 1) * 64;  // P_j over S_j's first 32 columns
+          const uint32_t d = tmem + e * 256 + 128;
+#pragma unroll
+          for (int k = 0; k < TK / 16; ++k)  // 16 keys per MMA: +8 TMEM columns of P, +2 x 1024 B along V rows
+            tc_mma_ts(d, ap + 8 * k, desc_mn_sw128(av + k * 2048, TK * 128), id_o, (j > 0 || k > 0) ? 1u : 0u);
+          tc_commit(&o_done[2 * e + (j & 1)]);
+          if (e == HP - 1) tc_commit(&kv_empty[s]);
+          // S(j+2) overwrites buffer j % 2, which PV(j) reads P_j from: wait for PV(j)
+          if (next) {
+            if (p.pv_wait) {
+              mbar_wait(&o_done[2 * e + (j & 1)], (j >> 1) & 1);
+              tc_fence_after();
+            }
+            mma_s(j + 2, e);
+          }
+        }
       }
     }
   } else {
     // ------------------------------------------------------------ softmax warps
-    const int q = warp & 3;
+    const int e = (warp - 2) >> 2;
+    const int q = warp & 3;                   // TMEM lane quarter accessible to this warp
     const int r = q * 32 + lane;              // query row = TMEM lane
     const int qpos = q_start + r;
-    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    float o[HD];
-#pragma unroll
-    for (int i = 0; i < HD; ++i) o[i] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f, corr_prev = 1.f;
-    auto fold_o = [&](int jb, float corr) {   // o = o * corr + O_jb
-      mbar_wait(&o_full[jb & 1], (jb >> 1) & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int c0 = 0; c0 < HD; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(lane_base + O_COL + (jb & 1) * HD + c0, v);
-        tc_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) o[c0 + i] = o[c0 + i] * corr + __uint_as_float(v[i]);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_empty[jb & 1]);
-    };
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + e * 256;
+    float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < n_kv; ++j) {
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      const uint32_t sb = lane_base + (j & 1) * 64;
+      mbar_wait(&s_full[2 * e + (j & 1)], (j >> 1) & 1);
       tc_fence_after();
       float sv[TK];
-#pragma unroll
-      for (int c0 = 0; c0 < TK; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(lane_base + S_COL + (j & 1) * TK + c0, v);
+      {
+        uint32_t v0[32], v1[32];
+        tmem_ld32(sb, v0);
+        tmem_ld32(sb + 32, v1);
         tc_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c0 + i] = __uint_as_float(v[i]);
+        for (int i = 0; i < 32; ++i) {
+          sv[i] = __uint_as_float(v0[i]);
+          sv[32 + i] = __uint_as_float(v1[i]);
+        }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[j & 1]);
-      const bool diag = j * TK + TK - 1 > q_start;
-      float mx = m_run;
+      // causal mask on the diagonal blocks; the row max in raw score units (scale > 0),
+      // as an 8-way tree to keep the dependent chain short
+      if (j * TK + TK - 1 > q_start) {
 #pragma unroll
-      for (int c = 0; c < TK; ++c) {
-        float x = sv[c] * p.scale_log2;
-        if (diag && j * TK + c > qpos) x = -INFINITY;
-        sv[c] = x;
-        mx = fmaxf(mx, x);
+        for (int c = 0; c < TK; ++c)
+          if (j * TK + c > qpos) sv[c] = -INFINITY;
       }
-      const float corr = (m_run == -INFINITY) ? 0.f : exp2f(m_run - mx);
-      float rs = 0.f;
+      float mx8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx8[i] = sv[i];
+#pragma unroll
+      for (int c = 8; c < TK; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], sv[c]);
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * p.scale_log2;
+      const float m_new = fmaxf(m_run, mx);
+      if (j == 0) {
+        m_run = m_new;
+      } else {
+        const bool need = m_new > m_run + RESCALE_LOG2;
+        if (__any_sync(0xffffffffu, need)) {
+          // O (TMEM) *= exp2(m_run - m_new) for the rows whose max grew past the threshold;
+          // PV_{j-1} must have landed, PV_j is not issued before this warp's P_j arrives
+          const float corr = need ? exp2f(m_run - m_new) : 1.f;
+          if (need) m_run = m_new;
+          l_run *= corr;
+          mbar_wait(&o_done[2 * e + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c0 = 0; c0 < HD; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(lane_base + 128 + c0, v);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+            tmem_st32(lane_base + 128 + c0, v);
+          }
+        }
+      }
+      // P = 2^(s * scale - m_run); key 0 is never masked, so m_run is finite for every row
+      float rs8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rs8[i] = 0.f;
       uint32_t pk[TK / 2];
+      const float neg_m = -m_run;
 #pragma unroll
       for (int c = 0; c < TK; c += 2) {
-        const float a = (mx == -INFINITY) ? 0.f : exp2f(sv[c] - mx);
-        const float b = (mx == -INFINITY) ? 0.f : exp2f(sv[c + 1] - mx);
-        rs += a + b;
+        const float a = fast_ex2(fmaf(sv[c], p.scale_log2, neg_m));
+        const float b = fast_ex2(fmaf(sv[c + 1], p.scale_log2, neg_m));
+        rs8[(c >> 1) & 7] += a + b;
         pk[c / 2] = pack_bf16x2(a, b);
       }
-      l_run = l_run * corr + rs;
-      m_run = mx;
-      // P row -> K-major 128B-swizzled smem tile (row r: 128 B, 16-byte chunk c at c ^ (r % 8))
-      if (j >= 2) mbar_wait(&p_empty[j & 1], ((j >> 1) - 1) & 1);
-      uint8_t* prow = sP + (j & 1) * P_BYTES + (r >> 3) * 1024 + (r & 7) * 128;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) =
-            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-      fence_proxy_async();
+      l_run += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+      // P (bf16 pairs along the keys) over the first 32 columns of this S buffer
+      tmem_st32(sb, pk);
+      tc_wait_st();
+      tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[j & 1]);
-      if (j > 0) fold_o(j - 1, corr_prev);
-      corr_prev = corr;
+      if (lane == 0) mbar_arrive(&p_full[2 * e + (j & 1)]);
     }
-    if (n_kv > 0) fold_o(n_kv - 1, corr_prev);
-    if (qpos < len) {
-      const float inv = 1.f / l_run;
-      bf16* dst = p.out + (int64_t)(tok0 + qpos) * p.n_heads * HD + h * HD;
+    if (n_kv > 0) {
+      mbar_wait(&o_done[2 * e + ((n_kv - 1) & 1)], ((n_kv - 1) >> 1) & 1);
+      tc_fence_after();
+    }
+    // tcgen05.ld is warp-collective: every lane loads, rows past the sequence do not store
+    const float inv = 1.f / l_run;
+    bf16* dst = p.out + (int64_t)(tok0 + qpos) * p.n_heads * HD + (h0 + e) * HD;
 #pragma unroll
-      for (int i = 0; i < HD; i += 8)
-        *reinterpret_cast<uint4*>(dst + i) =
-            make_uint4(pack_bf16x2(o[i] * inv, o[i + 1] * inv), pack_bf16x2(o[i + 2] * inv, o[i + 3] * inv),
-                       pack_bf16x2(o[i + 4] * inv, o[i + 5] * inv), pack_bf16x2(o[i + 6] * inv, o[i + 7] * inv));
+    for (int c0 = 0; c0 < HD; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(lane_base + 128 + c0, v);
+      tc_wait_ld();
+      if (qpos < len) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+          *reinterpret_cast<uint4*>(dst + c0 + i) = make_uint4(
+              pack_bf16x2(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv),
+              pack_bf16x2(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv),
+              pack_bf16x2(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv),
+              pack_bf16x2(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv));
+      }
     }
   }
   tc_fence_before();
@@ -285,7 +359,7 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   if (warp == 1) {
     __syncwarp();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, C::TMEM_COLS);
   }
 }
 
@@ -306,7 +380,10 @@ int make_attn_tc_maps(CUtensorMap* qmap, CUtensorMap* kvmap, const void* q, int6
 cudaError_t attn_prefill_tc_launch(const CUtensorMap* qmap, const CUtensorMap* kvmap, const int* cu_seqlens,
                                    const int* block_tables, int bt_ld, const int* tiles, int n_tiles, bf16* out,
                                    int n_heads, int n_kv, int layer, int n_layers, cudaStream_t s) {
-  cudaError_t e = ensure_smem(attn_prefill_tc_kernel, SMEM);
+  if (n_kv < 1 || n_heads % n_kv) return cudaErrorInvalidValue;
+  const bool pair = (n_heads / n_kv) % 2 == 0;  // two q heads of one kv head per CTA
+  cudaError_t e = pair ? ensure_smem(attn_prefill_tc_kernel<2>, AttnCfg<2>::SMEM)
+                       : ensure_smem(attn_prefill_tc_kernel<1>, AttnCfg<1>::SMEM);
   if (e != cudaSuccess) return e;
   if (n_tiles == 0) return cudaSuccess;
   TcAttnParams p;
@@ -320,7 +397,15 @@ cudaError_t attn_prefill_tc_launch(const CUtensorMap* qmap, const CUtensorMap* k
   p.layer = layer;
   p.n_layers = n_layers;
   p.scale_log2 = (float)(1.4426950408889634 / sqrt((double)HD));
-  return launch_k(attn_prefill_tc_kernel, dim3(n_tiles, n_heads), dim3(192), SMEM, s, *qmap, *kvmap, p);
+  {
+    const char* ev = getenv("ECOSERVE_ATTN_PVWAIT");
+    p.pv_wait = (ev && ev[0] == '0') ? 0 : 1;
+  }
+  if (pair)
+    return launch_k(attn_prefill_tc_kernel<2>, dim3(n_tiles, n_heads / 2), dim3(AttnCfg<2>::THREADS),
+                    AttnCfg<2>::SMEM, s, *qmap, *kvmap, p);
+  return launch_k(attn_prefill_tc_kernel<1>, dim3(n_tiles, n_heads), dim3(AttnCfg<1>::THREADS), AttnCfg<1>::SMEM, s,
+                  *qmap, *kvmap, p);
 }
 
 }  // namespace eco

@@ -11,17 +11,21 @@ sys.path.insert(0, ".")
 from paper_2504_18154_b200 import ops  # noqa: E402
 
 
-def timeit(fn, iters=10):
-    """Plain CUDA-event timing (the op wrappers copy host metadata, so no graph capture)."""
+def timeit(fn, iters=10, rounds=3):
+    """Plain CUDA-event timing (the op wrappers copy host metadata, so no graph capture);
+    best of `rounds` rounds of `iters` calls."""
     fn()
     torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(iters):
-        fn()
-    e.record()
-    torch.cuda.synchronize()
-    return s.elapsed_time(e) / iters * 1e3
+    best = float("inf")
+    for _ in range(rounds):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(iters):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        best = min(best, s.elapsed_time(e) / iters * 1e3)
+    return best
 
 
 def main():
