@@ -41,6 +41,8 @@ def main():
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--blocks", type=int, default=8000)
     ap.add_argument("--rates", type=str, default="", help="comma list: fixed probes instead of bisection")
+    ap.add_argument("--policy", choices=("padg", "nodg"), default="padg",
+                    help="padg: macro routing + rolling activation; nodg: round-robin separate batching baseline")
     args = ap.parse_args()
 
     import torch
@@ -62,7 +64,7 @@ def main():
         w = random_device_weights(shape, seed=100 + g, device=dev)
         for _ in range(args.instances_per_gpu):
             insts.append(Instance(shape, w, args.blocks, g, token_budget=16384, max_batch=512,
-                                  max_positions=8192, free_raw_after_create=(args.instances_per_gpu == 1)))
+                                  max_positions=8192 + args.max_out, free_raw_after_create=(args.instances_per_gpu == 1)))
     lens, ns = profile_prefill(insts[0], vocab=shape.vocab)
     slo_ttft, slo_tpot = int(args.slo_ttft * 1e9), int(args.slo_tpot * 1e9)
     probes = []
@@ -75,7 +77,8 @@ def main():
             r.output_len = min(r.output_len, args.max_out)
             r.req_id += rid0[0]
         rid0[0] += args.n_req
-        srv = PaDGServer(insts, slo_ttft, slo_tpot, reserve_tokens=237, predictor_table=(lens, ns))
+        srv = PaDGServer(insts, slo_ttft, slo_tpot, reserve_tokens=237, predictor_table=(lens, ns),
+                         policy=args.policy)
         t0 = time.perf_counter()
         out = srv.run(trace, timeout_s=900)
         wall = time.perf_counter() - t0
@@ -103,7 +106,10 @@ def main():
     line = {"metric": "goodput req/s at TTFT/TPOT SLO", "value": gp, "unit": "req/s", "n_gpus": n_gpu,
             "instances": len(insts), "p": args.p, "slo": {"ttft_s": args.slo_ttft, "tpot_s": args.slo_tpot},
             "config": {"workload": f"{args.preset} Poisson, {args.n_req} req/probe, outputs <= {args.max_out}",
-                       "shape": args.shape, "macro": f"{len(insts)} instances, rolling activation (Alg. 1/2)"},
+                       "shape": args.shape,
+                       "macro": f"{len(insts)} instances, " + ("rolling activation (Alg. 1/2)" if args.policy == "padg"
+                                                               else "NoDG round-robin separate batching")},
+            "policy": args.policy,
             "predictor": {"lens": lens, "ns": ns}, "probes": probes}
     print(json.dumps(line), flush=True)
     for i in insts:

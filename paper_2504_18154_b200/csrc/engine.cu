@@ -18,6 +18,7 @@
 #include <memory>
 #include <string>
 #include <unordered_map>
+#include <chrono>
 #include <vector>
 
 #include <nccl.h>
@@ -553,6 +554,15 @@ int decode_variant() {  // 1: 1-CTA/SM GEMM (default); 3: lean (co-resident with
 // (bench r01: decode 11.7k vs 13.8k tok/s) -- clusters need whole free GPC slices, so
 // they cannot start while the previous kernel's CTAs drain under PDL.
 // ECOSERVE_CLUSTER_SPLITK=1 enables it.
+bool host_timing_enabled() {  // ECOSERVE_HOST_TIMING=1: per decode step host-enqueue vs wall time (stderr)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_HOST_TIMING");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 bool use_cluster_splitk() {
   static int v = -1;
   if (v < 0) {
@@ -979,6 +989,7 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
     for (int k = 0; k < B; ++k) kv_tokens += ctx[k];
     const double kv_bytes = kv_tokens * 2.0 * inst->Mkv * inst->D * 2.0;  // K and V, one layer
     const int pm = inst->prof.begin(P_DECODE, st);
+    const auto t_enq0 = std::chrono::steady_clock::now();
     bool final_normed = false;
     ecoserve_status es = run_layers_decode(inst, B, d, d + (pos - hm), d + (slot - hm), d + (ctx - hm), d + (bt - hm),
                                            bt_ld, max_blocks, kv_bytes, &final_normed);
@@ -987,7 +998,14 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
     if (es != ECOSERVE_OK) return es;
     inst->prof.end(pm, B, st);
     CK(cudaMemcpyAsync(inst->h_tokens, inst->d_tokens, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+    const auto t_enq1 = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(st));
+    if (host_timing_enabled()) {
+      const auto t_sync = std::chrono::steady_clock::now();
+      fprintf(stderr, "[ecoserve] decode step B=%d: host enqueue %.1f us, enqueue+gpu %.1f us\n", B,
+              std::chrono::duration<double, std::micro>(t_enq1 - t_enq0).count(),
+              std::chrono::duration<double, std::micro>(t_sync - t_enq0).count());
+    }
     inst->prof.resolve();
     inst->prof.tokens[1] += B;
     inst->prof.h2d += sizeof(int) * used;

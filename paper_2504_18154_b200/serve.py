@@ -16,6 +16,12 @@
 
 The ctypes calls into libecoserve.so release the GIL, so N instances on N GPUs
 run concurrently from one process.
+
+policy="nodg" is the paper's NoDG separate-batching baseline (vLLM-style,
+P:312-320, 675-676) on the same kernels and the same per-instance
+prefill-priority loop: every arrival is routed immediately, round-robin, with no
+constraint check and no deferral, so every instance interleaves prefills into
+its decode stream (no rolling activation).
 """
 from __future__ import annotations
 
@@ -185,7 +191,11 @@ class PaDGServer:
 
     def __init__(self, instances: Sequence, slo_ttft_ns: int, slo_tpot_ns: int, reserve_tokens: int,
                  predictor_table=None, token_budget: int = 16384, decode_steps_per_poll: int = 1,
-                 probe_printed: bool = False):
+                 probe_printed: bool = False, policy: str = "padg"):
+        if policy not in ("padg", "nodg"):
+            raise ValueError(f"unknown policy {policy!r}")
+        self.policy = policy
+        self._rr = 0
         self.clock = Clock()
         self.status_q: "queue.Queue" = queue.Queue()
         self.workers = [Worker(i, inst, self.clock, self.status_q, token_budget, decode_steps_per_poll)
@@ -230,6 +240,10 @@ class PaDGServer:
             now = self.clock.now()
             while pending and pending[0].arrival_ns <= now:
                 lr = pending.popleft()
+                if self.policy == "nodg":  # immediate round-robin dispatch (NoDG baseline)
+                    i, self._rr = self._rr, (self._rr + 1) % len(self.workers)
+                    self._send(lr, i)
+                    continue
                 i, _ = self.macro.route(lr.req_id, lr.arrival_ns, lr.S, now)
                 if i < 0:
                     self.route_log.append((now, lr.req_id, -1))

@@ -82,6 +82,26 @@ def test_live_serving_completes_and_rolls(S):
     assert sorted(x[1] for x in routed) == sorted(out)
 
 
+def test_nodg_policy_round_robin_no_deferral(S):
+    """NoDG separate batching (8(f) N3): immediate round-robin routing, every instance
+    takes prefills interleaved with its decode steps, nothing is ever deferred."""
+    trace = make_trace("alpaca", 40, seed=5, rate_per_s=400.0, vocab=1000)
+    for r in trace:
+        r.output_len = min(r.output_len, 6)
+    insts = [FakeInstance(scale=1.0) for _ in range(3)]
+    srv = S.PaDGServer(insts, slo_ttft_ns=8_000_000, slo_tpot_ns=SEC // 50, reserve_tokens=32,
+                       predictor_table=((16, 4096), (2_000_000, 60_000_000)), token_budget=4096, policy="nodg")
+    out = srv.run(trace, timeout_s=60)
+    assert all(r.t_done_ns >= 0 for r in out.values())
+    assert all(x[2] >= 0 for x in srv.route_log), "NoDG never defers"
+    order = [x[2] for x in sorted(srv.route_log, key=lambda x: (x[0], x[1]))]
+    by_arrival = sorted(out.values(), key=lambda r: (r.arrival_ns, r.req_id))
+    assert [r.inst for r in by_arrival] == [i % 3 for i in range(len(by_arrival))]
+    assert sorted(order) == sorted(r.inst for r in out.values())
+    with pytest.raises(ValueError):
+        S.PaDGServer(insts, 1, 1, 1, policy="fudg")
+
+
 def test_product_metrics_match_oracle_definition():
     import random
     from oracle import metrics as OM

@@ -91,13 +91,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 enc() {
 }
 
 template <int S, int MODE, int CS>
-float run(const CUtensorMap& w, const CUtensorMap& x, int mt, int kb, int* sink) {
+float run(const CUtensorMap& w, const CUtensorMap& x, int mt, int kb, int* sink, int grid = 148) {
   constexpr int STAGE = MODE == 0 ? 16384 : 32768;
   const int smem = S * STAGE + 2048;
   auto k = probe_kernel<S, MODE, CS>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(148);
+  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(32);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute attr[1];
@@ -146,12 +146,8 @@ int main() {
   mk(&xm4, x, B, 32);
   const int mt = N / 128, kb = K / 64;
   const double gb = (double)N * K * 2 / 1e9;
-  printf("{\"w_only_s6\": %.1f, \"w_only_s12\": %.1f, \"w_x_s4\": %.1f, \"w_x_s6\": %.1f, \"w_xmc2_s6\": %.1f, "
-         "\"w_xmc4_s4\": %.1f, \"w_xmc4_s6\": %.1f}\n",
-         gb / run<6, 0, 1>(wm, xm, mt, kb, sink) * 1e3, gb / run<12, 0, 1>(wm, xm, mt, kb, sink) * 1e3,
-         gb / run<4, 1, 1>(wm, xm, mt, kb, sink) * 1e3, gb / run<6, 1, 1>(wm, xm, mt, kb, sink) * 1e3,
-         gb / run<6, 2, 2>(wm, xm2, mt, kb, sink) * 1e3, gb / run<4, 2, 4>(wm, xm4, mt, kb, sink) * 1e3,
-         gb / run<6, 2, 4>(wm, xm4, mt, kb, sink) * 1e3);
+  for (int grid : {148, 112, 74})
+    printf("{\"grid\": %d, \"w_x_s6\": %.1f}\n", grid, gb / run<6, 1, 1>(wm, xm, mt, kb, sink, grid) * 1e3);
   cudaError_t err = cudaDeviceSynchronize();
   printf("status %s\n", cudaGetErrorString(err));
   return 0;
