@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <string.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <memory>
@@ -128,6 +129,15 @@ struct ecoserve_instance {
   int device = 0, num_sms = 148;
   int tp = 1, tp_rank = 0;
   ncclComm_t comm = nullptr;     // TP=2 pair (a17): all-reduce of the residual after O and down
+  // fused TP all-reduce over NVLink peer memory (N2): receive rows / flags written by the peer
+  bool tp_fused = false;
+  int tp_rows_max = 0, tp_epoch = 0;
+  float* tp_recv = nullptr;      // [2][tp_rows_max][H]
+  int* tp_flags = nullptr;       // [2][tp_rows_max]
+  float* tp_part = nullptr;      // prefill O / down partials [T_max][H]
+  float* peer_recv = nullptr;    // the peer's tp_recv / tp_flags (peer pointer or IPC mapping)
+  int* peer_flags = nullptr;
+  bool peer_ipc = false;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   bool dead = false;
@@ -239,6 +249,79 @@ static bool shape_ok(const ecoserve_model_shape* s) {
   return true;
 }
 
+namespace {
+bool tp_fused_enabled() {  // ECOSERVE_TP_FUSED=0: NCCL all-reduce + separate RMSNorm instead
+  const char* e = getenv("ECOSERVE_TP_FUSED");
+  return !(e && e[0] == '0');
+}
+
+// Exchange the receive buffers of the pair (N2): every rank allocates [2][rows][H]
+// receive rows + flags, the pair all-gathers {pid, device, pointers, IPC handles} over
+// the NCCL communicator, and maps the peer's buffers -- a direct peer pointer when both
+// ranks live in one process, an IPC mapping otherwise.
+struct TpPeerInfo {
+  int pid, device;
+  uint64_t recv, flags;
+  cudaIpcMemHandle_t h_recv, h_flags;
+};
+
+ecoserve_status tp_setup_peer(ecoserve_instance* inst) {
+  inst->tp_rows_max = std::max(inst->T_max, inst->B_max);
+  const int64_t rows = inst->tp_rows_max;
+  CK(cudaMalloc(&inst->tp_recv, sizeof(float) * 2 * rows * inst->H));
+  CK(cudaMalloc(&inst->tp_flags, sizeof(int) * 2 * rows));
+  CK(cudaMemset(inst->tp_flags, 0, sizeof(int) * 2 * rows));
+  CK(cudaMalloc(&inst->tp_part, sizeof(float) * (int64_t)inst->T_max * inst->H));
+  TpPeerInfo mine{};
+  mine.pid = (int)getpid();
+  mine.device = inst->device;
+  mine.recv = reinterpret_cast<uint64_t>(inst->tp_recv);
+  mine.flags = reinterpret_cast<uint64_t>(inst->tp_flags);
+  CK(cudaIpcGetMemHandle(&mine.h_recv, inst->tp_recv));
+  CK(cudaIpcGetMemHandle(&mine.h_flags, inst->tp_flags));
+  void* d_info = nullptr;
+  CK(cudaMalloc(&d_info, 2 * sizeof(TpPeerInfo)));
+  CK(cudaMemcpy(reinterpret_cast<char*>(d_info) + inst->tp_rank * sizeof(TpPeerInfo), &mine, sizeof(TpPeerInfo),
+                cudaMemcpyHostToDevice));
+  const ncclResult_t r =
+      ncclAllGather(reinterpret_cast<char*>(d_info) + inst->tp_rank * sizeof(TpPeerInfo), d_info, sizeof(TpPeerInfo),
+                    ncclChar, inst->comm, inst->stream);
+  if (r != ncclSuccess) {
+    cudaFree(d_info);
+    inst->err = std::string("ncclAllGather: ") + ncclGetErrorString(r);
+    return ECOSERVE_ERR_NCCL;
+  }
+  TpPeerInfo all[2];
+  CK(cudaStreamSynchronize(inst->stream));
+  CK(cudaMemcpy(all, d_info, sizeof(all), cudaMemcpyDeviceToHost));
+  cudaFree(d_info);
+  const TpPeerInfo& peer = all[1 - inst->tp_rank];
+  if (peer.pid == mine.pid) {
+    int ok = 0;
+    CK(cudaDeviceCanAccessPeer(&ok, inst->device, peer.device));
+    if (!ok) {
+      inst->err = "TP pair: no peer access between the two GPUs";
+      return ECOSERVE_ERR_CUDA;
+    }
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer.device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+    cudaGetLastError();
+    inst->peer_recv = reinterpret_cast<float*>(peer.recv);
+    inst->peer_flags = reinterpret_cast<int*>(peer.flags);
+  } else {
+    void* pr = nullptr;
+    void* pf = nullptr;
+    CK(cudaIpcOpenMemHandle(&pr, peer.h_recv, cudaIpcMemLazyEnablePeerAccess));
+    CK(cudaIpcOpenMemHandle(&pf, peer.h_flags, cudaIpcMemLazyEnablePeerAccess));
+    inst->peer_recv = reinterpret_cast<float*>(pr);
+    inst->peer_flags = reinterpret_cast<int*>(pf);
+    inst->peer_ipc = true;
+  }
+  inst->tp_fused = true;
+  return ECOSERVE_OK;
+}
+}  // namespace
+
 extern "C" {
 
 int64_t ecoserve_kv_pool_bytes(const ecoserve_model_shape* s, int32_t block_tokens, int64_t num_blocks) {
@@ -285,6 +368,12 @@ void ecoserve_instance_destroy(ecoserve_instance* inst) {
   if (inst->h_meta) cudaFreeHost(inst->h_meta);
   if (inst->h_tokens) cudaFreeHost(inst->h_tokens);
   for (cudaEvent_t e : inst->prof.pool) cudaEventDestroy(e);
+  if (inst->peer_ipc) {
+    if (inst->peer_recv) cudaIpcCloseMemHandle(inst->peer_recv);
+    if (inst->peer_flags) cudaIpcCloseMemHandle(inst->peer_flags);
+  }
+  for (void* p : {(void*)inst->tp_recv, (void*)inst->tp_flags, (void*)inst->tp_part})
+    if (p) cudaFree(p);
   if (inst->comm) ncclCommDestroy(inst->comm);
   if (inst->own_stream && inst->stream) cudaStreamDestroy(inst->stream);
   delete inst;
@@ -472,6 +561,10 @@ ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, cons
       inst->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
       return ECOSERVE_ERR_NCCL;
     }
+    if (tp_fused_enabled()) {
+      const ecoserve_status es = tp_setup_peer(inst);
+      if (es != ECOSERVE_OK) return es;
+    }
   }
   *out = holder.release();
   return ECOSERVE_OK;
@@ -622,6 +715,45 @@ cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const 
   return splitk_reduce_launch(red, inst->part, splits, B, n_out, n_out, e, inst->stream);
 }
 
+// Decode projection as raw f32 partials [splits][B][n_out] in inst->part (TP fused path).
+cudaError_t decode_partials(ecoserve_instance* inst, const CUtensorMap& wmap, const ActMaps& xm, int n_out, int K,
+                            int B, int* splits_out) {
+  const int bn = B <= 64 ? 64 : 128;
+  const int splits = gemm_effective_splits(K, gemm_decode_splits(n_out, K, inst->num_sms));
+  GemmEpi ge = epi_base(inst);
+  ge.mode = EPI_SWAP_F32;
+  ge.out = inst->part;
+  ge.ldo = n_out;
+  ge.indep = 1;
+  *splits_out = splits;
+  return gemm_launch_r(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, decode_variant(), splits, ge, inst->num_sms,
+                       inst->stream);
+}
+
+// TP=2 fused all-reduce + residual + RMSNorm over the peer's receive rows (N2)
+cudaError_t tp_allreduce(ecoserve_instance* inst, const float* part, int splits, int64_t plane, int64_t ldp, int rows,
+                         const bf16* gamma, bf16* h) {
+  TpAllreduceArgs a;
+  a.part = part;
+  a.splits = splits;
+  a.plane = plane;
+  a.ldp = ldp;
+  a.x = inst->x;
+  a.gamma = gamma;
+  a.h = h;
+  a.eps = inst->shape.rms_eps;
+  a.rows = rows;
+  a.rows_max = inst->tp_rows_max;
+  a.H = inst->H;
+  a.rank = inst->tp_rank;
+  a.epoch = ++inst->tp_epoch;
+  a.peer_recv = inst->peer_recv;
+  a.peer_flags = inst->peer_flags;
+  a.my_recv = inst->tp_recv;
+  a.my_flags = inst->tp_flags;
+  return tp_allreduce_norm_launch(a, inst->num_sms, inst->stream);
+}
+
 }  // namespace
 
 static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const int* d_ids, const int* d_pos,
@@ -632,9 +764,11 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
   const float eps = inst->shape.rms_eps;
   LAUNCH(P_OTHER, 0, 1, embed_launch(d_ids, inst->embed, inst->x, T, H, st));
   if (inst->debug) CK(cudaMemcpyAsync(inst->dbg, inst->x, sizeof(float) * (int64_t)T * H, cudaMemcpyDeviceToDevice, st));
+  bool h_ready = false;  // the previous layer's fused TP all-reduce already wrote this layer's norm
   for (int l = 0; l < L; ++l) {
     LayerW& w = inst->lw[l];
-    LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.attn_norm, inst->h, T, H, eps, st));
+    if (!h_ready) LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.attn_norm, inst->h, T, H, eps, st));
+    h_ready = false;
     GemmEpi e = epi_base(inst);
     e.mode = EPI_QKV;
     e.pos = d_pos;
@@ -663,23 +797,47 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
                                     M, inst->Mkv, l, inst->L, st));
     else
       LAUNCH(P_ATTN_PREFILL, attn_flop, 1, attn_prefill_launch(a, D, st));
-    GemmEpi eo = resid_epi(inst);
-    eo.mode = resid_mode_prefill(inst);
-    LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * M * D, 1,
-           prefill_gemm(inst, inst->m_ao.a, w.o_a, w.o_b, T, H, M * D, eo));
-    ALLREDUCE_X(T);
-    LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, T, H, eps, st));
+    if (inst->tp_fused) {  // partial -> fused all-reduce + residual + RMSNorm over NVLink (N2)
+      GemmEpi eo = epi_base(inst);
+      eo.mode = EPI_F32;
+      eo.out = inst->tp_part;
+      eo.ldo = H;
+      LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * M * D, 1,
+             prefill_gemm(inst, inst->m_ao.a, w.o_a, w.o_b, T, H, M * D, eo));
+      LAUNCH(P_OTHER, 0, 1, tp_allreduce(inst, inst->tp_part, 1, (int64_t)T * H, H, T, w.ffn_norm, inst->h));
+    } else {
+      GemmEpi eo = resid_epi(inst);
+      eo.mode = resid_mode_prefill(inst);
+      LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * M * D, 1,
+             prefill_gemm(inst, inst->m_ao.a, w.o_a, w.o_b, T, H, M * D, eo));
+      ALLREDUCE_X(T);
+      LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, T, H, eps, st));
+    }
     GemmEpi eg = epi_base(inst);
     eg.mode = EPI_SILU;
     eg.out = inst->act;
     eg.ldo = F;
     LAUNCH(P_GEMM_PREFILL, 2.0 * T * 2 * F * H, 1,
            prefill_gemm(inst, inst->m_h.a, w.gu_a, w.gu_b, T, 2 * F, H, eg));
-    GemmEpi ed = resid_epi(inst);
-    ed.mode = resid_mode_prefill(inst);
-    LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * F, 1,
-           prefill_gemm(inst, inst->m_act.a, w.d_a, w.d_b, T, H, F, ed));
-    ALLREDUCE_X(T);
+    if (inst->tp_fused) {  // the next layer's attention norm rides along (the final norm is the LM head's)
+      GemmEpi ed = epi_base(inst);
+      ed.mode = EPI_F32;
+      ed.out = inst->tp_part;
+      ed.ldo = H;
+      LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * F, 1,
+             prefill_gemm(inst, inst->m_act.a, w.d_a, w.d_b, T, H, F, ed));
+      const bool last = l + 1 == L;
+      LAUNCH(P_OTHER, 0, 1,
+             tp_allreduce(inst, inst->tp_part, 1, (int64_t)T * H, H, T, last ? nullptr : inst->lw[l + 1].attn_norm,
+                          inst->h));
+      h_ready = !last;
+    } else {
+      GemmEpi ed = resid_epi(inst);
+      ed.mode = resid_mode_prefill(inst);
+      LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * F, 1,
+             prefill_gemm(inst, inst->m_act.a, w.d_a, w.d_b, T, H, F, ed));
+      ALLREDUCE_X(T);
+    }
     if (inst->debug)
       CK(cudaMemcpyAsync(inst->dbg + (int64_t)(l + 1) * inst->T_max * H, inst->x, sizeof(float) * (int64_t)T * H,
                          cudaMemcpyDeviceToDevice, st));
@@ -736,12 +894,18 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     a.out = inst->ao;
     a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
     LAUNCH(P_ATTN_DECODE, kv_bytes, n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
-    GemmEpi eo = resid_epi(inst);
-    LAUNCH(P_GEMM_DECODE, 2.0 * H * M * D, nk,
-           decode_gemm(inst, w.o_a, inst->m_ao, H, M * D, B, resid_mode_decode(inst), eo, &nk,
-                       can_fuse ? w.ffn_norm : nullptr, inst->h, &fused));
-    ALLREDUCE_X(B);
-    if (!fused) LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, B, H, eps, st));
+    if (inst->tp_fused) {  // partials -> fused all-reduce + residual + RMSNorm over NVLink (N2)
+      int sp = 1;
+      LAUNCH(P_GEMM_DECODE, 2.0 * H * M * D, 1, decode_partials(inst, w.o_a, inst->m_ao, H, M * D, B, &sp));
+      LAUNCH(P_OTHER, 0, 1, tp_allreduce(inst, inst->part, sp, (int64_t)B * H, H, B, w.ffn_norm, inst->h));
+    } else {
+      GemmEpi eo = resid_epi(inst);
+      LAUNCH(P_GEMM_DECODE, 2.0 * H * M * D, nk,
+             decode_gemm(inst, w.o_a, inst->m_ao, H, M * D, B, resid_mode_decode(inst), eo, &nk,
+                         can_fuse ? w.ffn_norm : nullptr, inst->h, &fused));
+      ALLREDUCE_X(B);
+      if (!fused) LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, B, H, eps, st));
+    }
     GemmEpi eg = epi_base(inst);
     eg.out = inst->act;
     eg.ldo = F;
@@ -750,12 +914,21 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     // the down projection's reduction also applies the next RMSNorm: the next layer's
     // attention norm, or after the last layer the final norm (into the LM-head input)
     const bool last = l + 1 == L;
-    GemmEpi ed = resid_epi(inst);
-    LAUNCH(P_GEMM_DECODE, 2.0 * H * F, nk,
-           decode_gemm(inst, w.d_a, inst->m_act, H, F, B, resid_mode_decode(inst), ed, &nk,
-                       can_fuse ? (last ? inst->final_norm : inst->lw[l + 1].attn_norm) : nullptr,
-                       last ? inst->hl : inst->h, &fused));
-    ALLREDUCE_X(B);
+    if (inst->tp_fused) {
+      int sp = 1;
+      LAUNCH(P_GEMM_DECODE, 2.0 * H * F, 1, decode_partials(inst, w.d_a, inst->m_act, H, F, B, &sp));
+      LAUNCH(P_OTHER, 0, 1,
+             tp_allreduce(inst, inst->part, sp, (int64_t)B * H, H, B,
+                          last ? inst->final_norm : inst->lw[l + 1].attn_norm, last ? inst->hl : inst->h));
+      fused = true;
+    } else {
+      GemmEpi ed = resid_epi(inst);
+      LAUNCH(P_GEMM_DECODE, 2.0 * H * F, nk,
+             decode_gemm(inst, w.d_a, inst->m_act, H, F, B, resid_mode_decode(inst), ed, &nk,
+                         can_fuse ? (last ? inst->final_norm : inst->lw[l + 1].attn_norm) : nullptr,
+                         last ? inst->hl : inst->h, &fused));
+      ALLREDUCE_X(B);
+    }
     h_ready = fused && !last;
     if (last) *final_normed = fused;
     if (inst->debug)

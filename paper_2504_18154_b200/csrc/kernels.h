@@ -142,6 +142,23 @@ struct DecodeAttnArgs {
 };
 cudaError_t attn_decode_launch(const DecodeAttnArgs& a, int head_dim, cudaStream_t s);
 
+// ------------------------------------------------------------------ TP=2 fused all-reduce (N2)
+struct TpAllreduceArgs {
+  const float* part;       // this rank's partials [splits][plane] (row stride ldp)
+  int splits;
+  int64_t plane, ldp;
+  float* x;                // residual [rows][H] f32, updated in place
+  const bf16* gamma;       // next RMSNorm weight, or null (x only)
+  bf16* h;                 // rmsnorm(x) * gamma [rows][H]
+  float eps;
+  int rows, rows_max, H, rank, epoch;
+  float* peer_recv;        // the peer's receive rows [2][rows_max][H] (P2P)
+  int* peer_flags;         // the peer's flags [2][rows_max] (P2P)
+  const float* my_recv;    // this rank's receive rows, written by the peer
+  const int* my_flags;
+};
+cudaError_t tp_allreduce_norm_launch(const TpAllreduceArgs& a, int num_sms, cudaStream_t s);
+
 // ------------------------------------------------------------------ small kernels
 cudaError_t embed_launch(const int* ids, const bf16* E, float* x, int n, int H, cudaStream_t s);
 cudaError_t rmsnorm_launch(const float* x, int64_t ldx, const int* rows, const bf16* gamma, bf16* out, int n, int H,
