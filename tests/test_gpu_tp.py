@@ -3,6 +3,8 @@ heads / FFN columns sharded, residual all-reduced with NCCL after the O and
 down projections. Checks (reading A19/A20, C4): both ranks return identical
 tokens and bitwise-identical residual streams; hidden states match the fp64
 oracle within 1e-2 per layer; tokens match where the oracle's margin > 5e-2.
+Both all-reduce paths are checked: fused with the residual add and RMSNorm over
+NVLink peer memory (default, 8(f) N2) and NCCL + separate RMSNorm.
 Needs 2 GPUs (gpurun --gpus 2); skipped with a reason on a 1-GPU box."""
 import numpy as np
 import pytest
@@ -38,7 +40,11 @@ def _worker(rank, nccl_id, q):
         q.put((rank, None, None, None, repr(e)))
 
 
-def test_tp2_pair_matches_oracle():
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_tp2_pair_matches_oracle(fused, monkeypatch):
+    """fused=1: all-reduce + residual + RMSNorm over NVLink peer memory (N2);
+    fused=0: NCCL all-reduce + separate RMSNorm."""
+    monkeypatch.setenv("ECOSERVE_TP_FUSED", fused)  # inherited by the spawned ranks
     if torch.cuda.device_count() < 2:
         pytest.skip("TP=2 needs 2 GPUs (gpurun --gpus 2)")
     from oracle import transformer as T
