@@ -1199,6 +1199,21 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
   return ECOSERVE_OK;
 }
 
+// Direct NVLink copies for a buffer on another GPU: enable peer access from this
+// instance's device (without it, cross-device cudaMemcpyAsync is staged through the host).
+static void enable_peer_for(int dev, const void* ptr) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  if (at.type != cudaMemoryTypeDevice || at.device == dev) return;
+  int ok = 0;
+  if (cudaDeviceCanAccessPeer(&ok, dev, at.device) == cudaSuccess && ok) {
+    if (cudaDeviceEnablePeerAccess(at.device, 0) != cudaSuccess) cudaGetLastError();  // already enabled is fine
+  }
+}
+
 ecoserve_status ecoserve_kv_export(ecoserve_instance* inst, int64_t req_id, void* dst, int64_t dst_bytes,
                                    int32_t* prompt, int32_t prompt_cap, ecoserve_req_state* state) {
   if (!inst || !dst || !state) return ECOSERVE_ERR_INVALID_ARG;
@@ -1209,6 +1224,7 @@ ecoserve_status ecoserve_kv_export(ecoserve_instance* inst, int64_t req_id, void
   const int64_t bb = inst->blk_stride * (int64_t)sizeof(bf16);
   if (dst_bytes < bb * (int64_t)r.blocks.size() || (prompt && prompt_cap < r.S)) return ECOSERVE_ERR_INVALID_ARG;
   CK(cudaSetDevice(inst->device));
+  enable_peer_for(inst->device, dst);
   for (size_t b = 0; b < r.blocks.size(); ++b)  // one contiguous span per block (all layers, K and V)
     CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(dst) + b * bb, inst->pool + (int64_t)r.blocks[b] * inst->blk_stride,
                        bb, cudaMemcpyDefault, inst->stream));
@@ -1234,6 +1250,7 @@ ecoserve_status ecoserve_kv_import(ecoserve_instance* inst, const ecoserve_req_s
   if (inst->reqs.count(st->req_id)) return ECOSERVE_ERR_STATE;
   if ((int64_t)inst->free_blocks.size() < st->n_blocks) return ECOSERVE_ERR_KV_EXHAUSTED;
   CK(cudaSetDevice(inst->device));
+  enable_peer_for(inst->device, src);
   Req r;
   r.id = st->req_id;
   r.S = st->prompt_len;
