@@ -223,7 +223,10 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a) {
   pdl_trigger();
   pdl_wait();
 
-  const int b = blockIdx.x, kvh = blockIdx.y, split = blockIdx.z;
+  // CTAs in longest-context-first order, all kv heads of a sequence adjacent (LPT:
+  // the long sequences start in the first wave, short ones fill the tail)
+  const int rank = blockIdx.x / a.n_kv, kvh = blockIdx.x % a.n_kv, split = blockIdx.z;
+  const int b = a.order ? a.order[rank] : rank;
   const int G = a.n_heads / a.n_kv;
   const int ctx = a.ctx_lens[b];
   const int n_blocks = (ctx + 63) / 64;
@@ -432,7 +435,7 @@ static cudaError_t decode_d(const DecodeAttnArgs& a, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   if (a.B == 0) return cudaSuccess;
   if (a.n_heads / a.n_kv > 16) return cudaErrorInvalidValue;
-  e = launch_k(attn_decode_kernel<D>, dim3(a.B, a.n_kv, a.n_splits), dim3(128), smem, s, a);
+  e = launch_k(attn_decode_kernel<D>, dim3(a.B * a.n_kv, 1, a.n_splits), dim3(128), smem, s, a);
   if (e != cudaSuccess || a.n_splits == 1) return e;
   return launch_k(attn_combine_kernel<D>, dim3(a.B, a.n_heads), dim3(D), 0, s, a);
 }

@@ -847,7 +847,8 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
 
 static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const int* d_ids, const int* d_pos,
                                          const int* d_slot, const int* d_ctx, const int* d_bt, int bt_ld,
-                                         int max_blocks, double kv_bytes, bool* final_normed) {
+                                         int max_blocks, double kv_bytes, bool* final_normed,
+                                         const int* d_order = nullptr) {
   cudaStream_t st = inst->stream;
   const int L = inst->L, H = inst->H, M = inst->M, D = inst->D, F = inst->F;
   const float eps = inst->shape.rms_eps;
@@ -893,6 +894,7 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     a.part_ml = inst->attn_ws + (int64_t)B * M * n_splits * D;
     a.out = inst->ao;
     a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
+    a.order = d_order;
     LAUNCH(P_ATTN_DECODE, kv_bytes, n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
     if (inst->tp_fused) {  // partials -> fused all-reduce + residual + RMSNorm over NVLink (N2)
       int sp = 1;
@@ -1141,7 +1143,8 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
     int* ctx = slot + B;
     int* rows = ctx + B;
     int* bt = rows + B;
-    const int64_t used = (bt - hm) + (int64_t)B * bt_ld;
+    int* ord = bt + (int64_t)B * bt_ld;  // decode attention: longest context first
+    const int64_t used = (ord - hm) + B;
     if (used > inst->meta_cap) return ECOSERVE_ERR_INVALID_ARG;
     if (inst->debug) inst->dbg_rows.clear();
     for (int k = 0; k < B; ++k) {
@@ -1155,6 +1158,8 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
       for (int b = 0; b < bt_ld; ++b) bt[k * bt_ld + b] = b < (int)r->blocks.size() ? r->blocks[b] : 0;
       if (inst->debug) inst->dbg_rows[r->id] = {k, 1};
     }
+    for (int k = 0; k < B; ++k) ord[k] = k;
+    std::stable_sort(ord, ord + B, [ctx](int x, int y) { return ctx[x] > ctx[y]; });
     cudaStream_t st = inst->stream;
     CK(cudaMemcpyAsync(inst->d_meta, hm, sizeof(int) * used, cudaMemcpyHostToDevice, st));
     int* d = inst->d_meta;
@@ -1165,7 +1170,7 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
     const auto t_enq0 = std::chrono::steady_clock::now();
     bool final_normed = false;
     ecoserve_status es = run_layers_decode(inst, B, d, d + (pos - hm), d + (slot - hm), d + (ctx - hm), d + (bt - hm),
-                                           bt_ld, max_blocks, kv_bytes, &final_normed);
+                                           bt_ld, max_blocks, kv_bytes, &final_normed, d + (ord - hm));
     if (es != ECOSERVE_OK) return es;
     es = lm_head_argmax(inst, d + (rows - hm), B, P_GEMM_DECODE, final_normed);
     if (es != ECOSERVE_OK) return es;

@@ -139,6 +139,7 @@ struct DecodeAttnArgs {
   float* part_ml;           // [B][M][n_splits][2] (max (log2 domain), sum)
   bf16* out;                // [B][M*D]
   float scale_log2;
+  const int* order;         // optional [B]: sequences longest-context first (null = 0..B-1)
 };
 cudaError_t attn_decode_launch(const DecodeAttnArgs& a, int head_dim, cudaStream_t s);
 

@@ -248,6 +248,7 @@ ecoserve_status ecoserve_op_attention_decode(const void* q, const void* pool, in
   a.part_ml = workspace ? workspace + (int64_t)B * n_heads * n_splits * head_dim : nullptr;
   a.out = (bf16*)out;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)head_dim));
+  a.order = nullptr;
   OPCK(attn_decode_launch(a, head_dim, (cudaStream_t)stream));
   return ECOSERVE_OK;
 }
