@@ -141,7 +141,7 @@ cudaError_t argmax_reduce_launch(const float* val, const int* idx, int n, int pa
 // Decode O / down projection tail fused with the next RMSNorm: per row,
 //   x += sum_s part[s][row][:]  (fixed split order)  ;  out = bf16(rmsnorm(x) * gamma)
 // One CTA per row; each thread keeps its <= 4 float4 of the row in registers.
-__global__ void splitk_resid_rmsnorm_kernel(const float* __restrict__ part, int splits, int rows,
+__global__ void __launch_bounds__(1024) splitk_resid_rmsnorm_kernel(const float* __restrict__ part, int splits, int rows,
                                             float* __restrict__ x, const bf16* __restrict__ gamma,
                                             bf16* __restrict__ out, int H, float eps) {
   pdl_trigger();
@@ -193,7 +193,8 @@ __global__ void splitk_resid_rmsnorm_kernel(const float* __restrict__ part, int 
 cudaError_t splitk_resid_rmsnorm_launch(const float* part, int splits, int rows, float* x, const bf16* gamma,
                                         bf16* out, int H, float eps, cudaStream_t s) {
   if (rows == 0) return cudaSuccess;
-  const int threads = H > 4096 ? 512 : (H >= 1024 ? 256 : 64);
+  // one float4 per thread up to H = 4096 (more loads in flight: only `rows` CTAs run)
+  const int threads = H >= 4096 ? 1024 : (H >= 1024 ? 256 : 64);
   if (H % 4 || H > threads * 16) return cudaErrorInvalidValue;
   return launch_k(splitk_resid_rmsnorm_kernel, dim3(rows), dim3(threads), 0, s, part, splits, rows, x, gamma, out, H,
                   eps);
@@ -216,7 +217,7 @@ __device__ __forceinline__ int ld_acquire_sys(const int* p) {
   return v;
 }
 
-__global__ void tp_allreduce_norm_kernel(TpAllreduceArgs a) {
+__global__ void __launch_bounds__(1024) tp_allreduce_norm_kernel(TpAllreduceArgs a) {
   pdl_trigger();
   pdl_wait();
   const int H = a.H;
@@ -299,10 +300,11 @@ __global__ void tp_allreduce_norm_kernel(TpAllreduceArgs a) {
 
 cudaError_t tp_allreduce_norm_launch(const TpAllreduceArgs& a, int num_sms, cudaStream_t s) {
   if (a.rows == 0) return cudaSuccess;
-  const int threads = a.H > 4096 ? 512 : (a.H >= 1024 ? 256 : 64);
+  const int threads = a.H >= 4096 ? 1024 : (a.H >= 1024 ? 256 : 64);
   if (a.H % 4 || a.H > threads * 16 || a.rows > a.rows_max) return cudaErrorInvalidValue;
   // every CTA co-resident (rows are grid-strided): the two ranks wait on each other row by row
-  const int grid = a.rows < 2 * num_sms ? a.rows : 2 * num_sms;
+  const int per_sm = threads >= 1024 ? 1 : 2;
+  const int grid = a.rows < per_sm * num_sms ? a.rows : per_sm * num_sms;
   return launch_k(tp_allreduce_norm_kernel, dim3(grid), dim3(threads), 0, s, a);
 }
 
