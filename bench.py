@@ -276,6 +276,11 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         if os.path.exists(tfile):
             traffic = json.load(open(tfile)).get(dom)
         roof = dict(breakdown[dom])
+        traffic_note = None
+        if isinstance(traffic, dict):
+            traffic, traffic_note = traffic.get("dram_bytes"), traffic.get("note")
+        if traffic_note:
+            roof["traffic_note"] = traffic_note
         roof.update({"kernel": dom, "traffic": traffic, "peak_source": src +
                      (" sustained bf16 (kernel timed inside a long step)" if roof["bound"] == "tensor" else " HBM copy"),
                      "timing": "per-launch CUDA events on the instance stream over a second timed pass of the "
