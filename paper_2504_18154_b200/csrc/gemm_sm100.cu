@@ -12,6 +12,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <map>
 #include <mutex>
@@ -926,9 +927,11 @@ struct Gemm2Cfg {
 // (B) advancing across a band, token panels fastest inside it. The ~74 tiles in flight
 // then touch ~GM A panels and ~74/GM B panels, and each weight panel is read from HBM
 // once per band instead of once per token panel (the gate/up prefill projection read
-// 9 GB per launch with n-fastest order, 9x its operands).
-__device__ __forceinline__ void tile_mn(int w, int m_tiles, int n_tiles, int& mt, int& nt) {
-  constexpr int GM = 8;
+// 9 GB per launch with n-fastest order, 9x its operands; 1.5 GB with GM = 8). Less
+// HBM traffic is less power: under sw_power_cap the SM clock, and with it this
+// tensor-bound GEMM, rises (bench A/B on one box: GM 4 / 8 / 16 -> 42.9k / 43.7k /
+// 44.0k tok/s; default 16, ECOSERVE_GEMM_BAND overrides).
+__device__ __forceinline__ void tile_mn(int w, int m_tiles, int n_tiles, int GM, int& mt, int& nt) {
   const int band = w / (GM * n_tiles);
   const int m0 = band * GM;
   const int gm = min(GM, m_tiles - m0);
@@ -958,6 +961,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   const int n_tiles = (n_rows + BN - 1) / BN;
   const int kb_total = (K + BK - 1) / BK;
   const int n_work = m_tiles * n_tiles;
+  const int band = epi.band > 0 ? epi.band : 16;  // token panels per band (tile_mn)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -990,7 +994,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         if (kb >= 0 && kb + 1 < kb_total) { ++kb; return true; }
         if (kb >= 0) w += ncl;
         if (w >= n_work) return false;
-        tile_mn(w, m_tiles, n_tiles, mt, nt);
+        tile_mn(w, m_tiles, n_tiles, band, mt, nt);
         kb = 0;
         return true;
       };
@@ -1056,7 +1060,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     uint32_t acc_phase = 0;
     for (int w = cid; w < n_work; w += ncl) {
       int mt, nt;
-      tile_mn(w, m_tiles, n_tiles, mt, nt);
+      tile_mn(w, m_tiles, n_tiles, band, mt, nt);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int m = mt * 2 * BM + rank * BM + q * 32 + lane;
@@ -1085,7 +1089,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 }
 
 cudaError_t gemm2_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K,
-                         const GemmEpi& epi, int num_sms, cudaStream_t stream) {
+                         const GemmEpi& epi_in, int num_sms, cudaStream_t stream) {
+  static int band_env = -1;  // ECOSERVE_GEMM_BAND: token panels per band of the tile order (default 16)
+  if (band_env < 0) {
+    const char* ev = getenv("ECOSERVE_GEMM_BAND");
+    band_env = ev ? atoi(ev) : 0;
+  }
+  GemmEpi epi = epi_in;
+  if (epi.band <= 0) epi.band = band_env;
   if (epi.mode >= EPI_SWAP_F32) return cudaErrorInvalidValue;  // prefill (non-swapped) epilogues only
   cudaError_t e = ensure_smem(gemm_tc2_kernel, Gemm2Cfg::SMEM);
   if (e != cudaSuccess) return e;

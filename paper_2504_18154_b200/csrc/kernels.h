@@ -58,8 +58,10 @@ struct GemmEpi {
   // which operand does not depend on the previous kernel on the stream (0 none,
   // 1 A, 2 B): it is prefetched into the first smem stages before the PDL wait
   int indep;
-  // optional per-CTA phase timestamps (%globaltimer, ns), [grid][8]; null in the engine
+  // optional per-CTA phase timestamps (%globaltimer, ns), [grid][16]; null in the engine
   unsigned long long* trace;
+  // pair GEMM tile order: token panels per band (0 = default 16)
+  int band;
 };
 
 // Split count for a decode GEMM: minimises waves x K-blocks per CTA (+ a per-split reduction cost).
