@@ -382,9 +382,8 @@ cudaError_t splitk_reduce_launch(int mode, const float* part, int splits, int ro
   if (n == 0) return cudaSuccess;
   if (cols % 2) return cudaErrorInvalidValue;
   const int threads = 256;
-  splitk_reduce_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(mode, part, splits, rows, cols,
-                                                                                    ld_part, epi);
-  return cudaGetLastError();
+  return launch_k(splitk_reduce_kernel, dim3((unsigned)((n + threads - 1) / threads)), dim3(threads), 0, s, mode, part,
+                  splits, rows, cols, ld_part, epi);
 }
 
 }  // namespace eco
