@@ -42,7 +42,10 @@ struct GemmCfg {
   // epilogue staging: half an accumulator tile in f32 (BN/2 tokens x 128 features) for
   // the bulk-store epilogues (BN <= 128, one A tile); otherwise just the argmax scratch
   static constexpr bool BULK_EPI = BN <= 128 && RT == 1;
-  static constexpr int STAGING = BULK_EPI ? (BN / 2) * BM * 4 : 4 * BN * 8;
+  // (argmax epilogue: 4 x BN (max, idx) + one padded [32][BM + 1] f32 chunk)
+  static constexpr int ARGMAX_STG = 4 * BN * 8 + 32 * (BM + 1) * 4;
+  static constexpr int STAGING = BULK_EPI ? ((BN / 2) * BM * 4 > ARGMAX_STG ? (BN / 2) * BM * 4 : ARGMAX_STG)
+                                          : 4 * BN * 8;
   static constexpr int SMEM_MAX = 232448;  // 227 KB opt-in per CTA
   static constexpr int FIT = (SMEM_MAX - 1024 - 256 - STAGING) / STAGE_BYTES;
   static constexpr int STAGES = R == 3 ? 3 : FIT > 8 ? 8 : FIT;
@@ -413,7 +416,52 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int row = q * 32 + lane;  // accumulator row (TMEM lane)
       const int m = mt * BM * R + row;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::ACC_COLS;
-      if (epi.mode == EPI_SWAP_ARGMAX) {
+      if (epi.mode == EPI_SWAP_ARGMAX && C::BULK_EPI) {
+        // per 32-token chunk: the 128 x 32 accumulator slice goes to smem transposed
+        // ([token][row], padded row stride), then thread t scans rows 32*(t/32).. of token
+        // t%32 -- 32 compares per thread instead of a 5-round shuffle argmax per token
+        const int n_valid = min(BN, n_rows - nt * BN);
+        float* stg = reinterpret_cast<float*>(staging + 4 * BN * 8);  // after am_v / am_i
+        constexpr int LDS = BM + 1;
+        const int tok = ep_tid & 31, qq = ep_tid >> 5;
+        for (int c0 = 0; c0 < n_valid; c0 += 32) {  // warp-uniform
+          uint32_t v[32];
+          tmem_ld32(tbase + c0, v);
+          tc_wait_ld();
+          asm volatile("bar.sync 1, 128;" ::: "memory");  // previous chunk's scans are done
+#pragma unroll
+          for (int i = 0; i < 32; ++i) stg[i * LDS + row] = (m < m_rows) ? __uint_as_float(v[i]) : -INFINITY;
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          // rows in increasing order: ties keep the lowest index (reading A6); NaN wins
+          const float* col = stg + tok * LDS + qq * 32;
+          float bv = col[0];
+          int bi = mt * BM + qq * 32;
+#pragma unroll 8
+          for (int r = 1; r < 32; ++r) {
+            const float x = col[r];
+            if (x > bv || (isnan(x) && !isnan(bv))) { bv = x; bi = mt * BM + qq * 32 + r; }
+          }
+          am_v[qq][c0 + tok] = bv;
+          am_i[qq][c0 + tok] = bi;
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int c = ep_tid; c < n_valid; c += 128) {
+          const int n = nt * BN + c;
+          float bv = am_v[0][c];
+          int bi = am_i[0][c];
+          for (int k = 1; k < 4; ++k) {
+            const float ov = am_v[k][c];
+            const int oi = am_i[k][c];
+            if ((ov > bv) || (ov == bv && oi < bi) || (isnan(ov) && !isnan(bv))) { bv = ov; bi = oi; }
+          }
+          epi.am_val[(int64_t)n * epi.am_ld + mt] = bv;
+          epi.am_idx[(int64_t)n * epi.am_ld + mt] = bi;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      } else if (epi.mode == EPI_SWAP_ARGMAX) {
         for (int c0 = 0; c0 < BN; c0 += 32) {
           uint32_t v[32];
           tmem_ld32(tbase + c0, v);
