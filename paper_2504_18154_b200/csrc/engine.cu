@@ -154,6 +154,7 @@ struct ecoserve_instance {
   const bf16 *embed = nullptr, *lm_head = nullptr, *final_norm = nullptr;
   std::vector<LayerW> lw;
   CUtensorMap lm_a;
+  CUtensorMap* d_wmaps = nullptr;  // device copies: [L][4] (qkv_a, o_a, gu_a, d_a) then lm_a (L2 prefetch)
   bool attn_tc = false;          // tcgen05 prefill attention (head_dim 128) in use
   CUtensorMap attn_qmap, attn_kvmap;
   // workspace
@@ -372,7 +373,7 @@ void ecoserve_instance_destroy(ecoserve_instance* inst) {
     if (inst->peer_recv) cudaIpcCloseMemHandle(inst->peer_recv);
     if (inst->peer_flags) cudaIpcCloseMemHandle(inst->peer_flags);
   }
-  for (void* p : {(void*)inst->tp_recv, (void*)inst->tp_flags, (void*)inst->tp_part})
+  for (void* p : {(void*)inst->tp_recv, (void*)inst->tp_flags, (void*)inst->tp_part, (void*)inst->d_wmaps})
     if (p) cudaFree(p);
   if (inst->comm) ncclCommDestroy(inst->comm);
   if (inst->own_stream && inst->stream) cudaStreamDestroy(inst->stream);
@@ -490,6 +491,19 @@ ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, cons
   if (make_tmap_bf16(&inst->lm_a, inst->lm_head, V, H, 128)) {
     inst->err = "cuTensorMapEncodeTiled failed (lm_head)";
     return ECOSERVE_ERR_CUDA;
+  }
+  {  // decode weight maps in global memory for the next-GEMM L2 prefetch
+    std::vector<CUtensorMap> maps;
+    for (int l = 0; l < L; ++l) {
+      const LayerW& w = inst->lw[l];
+      maps.push_back(w.qkv_a);
+      maps.push_back(w.o_a);
+      maps.push_back(w.gu_a);
+      maps.push_back(w.d_a);
+    }
+    maps.push_back(inst->lm_a);
+    CK(cudaMalloc(&inst->d_wmaps, sizeof(CUtensorMap) * maps.size()));
+    CK(cudaMemcpy(inst->d_wmaps, maps.data(), sizeof(CUtensorMap) * maps.size(), cudaMemcpyHostToDevice));
   }
 
   // ---- workspace
@@ -663,6 +677,31 @@ bool use_cluster_splitk() {
     v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
+}
+
+// Next-GEMM L2 prefetch (ECOSERVE_L2_PREFETCH=1): measured neutral in the bench step
+// (decode 14.74k vs 14.81k tok/s on one box) -- the next kernel's pre-PDL-wait weight
+// loads already cover the boundary -- so off by default.
+bool use_l2_prefetch() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_L2_PREFETCH");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// The next decode GEMM (weights `map_idx` in d_wmaps, n_out x K) as the L2-prefetch
+// target of the current one.
+void set_prefetch(ecoserve_instance* inst, GemmEpi& e, int map_idx, int n_out, int K, int B) {
+  if (!use_l2_prefetch()) return;
+  const int bn = B <= 64 ? 64 : 128;
+  e.pf_map = inst->d_wmaps + map_idx;
+  e.pf_m_rows = n_out;
+  e.pf_K = K;
+  e.pf_splits = gemm_effective_splits(K, gemm_decode_splits(n_out, K, inst->num_sms));
+  e.pf_n_tiles = (B + bn - 1) / bn;
+  e.pf_kb = 6;
 }
 
 // norm_gamma / norm_out (optional): when the projection is a residual add split over K,
@@ -902,6 +941,7 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
       LAUNCH(P_OTHER, 0, 1, tp_allreduce(inst, inst->part, sp, (int64_t)B * H, H, B, w.ffn_norm, inst->h));
     } else {
       GemmEpi eo = resid_epi(inst);
+      set_prefetch(inst, eo, 4 * l + 2, 2 * F, H, B);  // gate/up next
       LAUNCH(P_GEMM_DECODE, 2.0 * H * M * D, nk,
              decode_gemm(inst, w.o_a, inst->m_ao, H, M * D, B, resid_mode_decode(inst), eo, &nk,
                          can_fuse ? w.ffn_norm : nullptr, inst->h, &fused));
@@ -911,6 +951,7 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     GemmEpi eg = epi_base(inst);
     eg.out = inst->act;
     eg.ldo = F;
+    set_prefetch(inst, eg, 4 * l + 3, H, F, B);  // down next
     LAUNCH(P_GEMM_DECODE, 2.0 * 2 * F * H, nk,
            decode_gemm(inst, w.gu_a, inst->m_h, 2 * F, H, B, EPI_SWAP_SILU, eg, &nk));
     // the down projection's reduction also applies the next RMSNorm: the next layer's
@@ -925,6 +966,7 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
       fused = true;
     } else {
       GemmEpi ed = resid_epi(inst);
+      if (!last) set_prefetch(inst, ed, 4 * (l + 1), inst->QKV, H, B);  // next layer's QKV
       LAUNCH(P_GEMM_DECODE, 2.0 * H * F, nk,
              decode_gemm(inst, w.d_a, inst->m_act, H, F, B, resid_mode_decode(inst), ed, &nk,
                          can_fuse ? (last ? inst->final_norm : inst->lw[l + 1].attn_norm) : nullptr,

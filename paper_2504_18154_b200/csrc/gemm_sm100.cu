@@ -359,6 +359,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
       trace_mark(epi, 6);  // last load issued
+      // fill the HBM gap at the kernel boundary: the next GEMM's first weight stages -> L2
+      if (epi.pf_map) {
+        const int w2 = blockIdx.x;
+        const int m_tiles2 = (epi.pf_m_rows + BM - 1) / BM;
+        if (w2 < m_tiles2 * epi.pf_n_tiles * epi.pf_splits) {
+          const int kb_total2 = (epi.pf_K + BK - 1) / BK;
+          const int kb_per2 = (kb_total2 + epi.pf_splits - 1) / epi.pf_splits;
+          const int ks2 = w2 % epi.pf_splits, mt2 = (w2 / epi.pf_splits) / epi.pf_n_tiles;
+          const int kb0 = ks2 * kb_per2, kb1 = min(kb_total2, kb0 + min(kb_per2, epi.pf_kb));
+          for (int k2 = kb0; k2 < kb1; ++k2)
+            asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                             reinterpret_cast<uint64_t>(epi.pf_map)),
+                         "r"(k2 * BK), "r"(mt2 * BM * R)
+                         : "memory");
+        }
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer

@@ -62,6 +62,12 @@ struct GemmEpi {
   unsigned long long* trace;
   // pair GEMM tile order: token panels per band (0 = default 16)
   int band;
+  // L2 prefetch of the NEXT decode GEMM's first stages (null = none): once this CTA's
+  // producer has issued its last load it prefetches, into L2, the first pf_kb weight
+  // K blocks of the work unit the same blockIdx runs in the next GEMM (tensor map in
+  // global memory; geometry m_rows / K / splits / token tiles of that GEMM)
+  const CUtensorMap* pf_map;
+  int pf_m_rows, pf_K, pf_splits, pf_n_tiles, pf_kb;
 };
 
 // Split count for a decode GEMM: minimises waves x K-blocks per CTA (+ a per-split reduction cost).
