@@ -60,18 +60,20 @@ ecoserve_status ecoserve_op_rmsnorm(const float* x, const int32_t* rows, const v
 /* Causal varlen prefill attention over a paged pool laid out as in ecoserve.h
  * for a single layer (n_layers = 1): q bf16 [T][M][D] (RoPE applied), out bf16
  * [T][M*D]. block_tables int32 [n_seq][bt_ld] (physical block of each 64-token
- * logical block). */
+ * logical block). ctx_off_host (host int32 [n_seq], or NULL = zeros): chunked
+ * prefill -- sequence s's q rows are the chunk at positions ctx_off[s] + i, attending
+ * to pool keys 0 .. ctx_off[s] + i (the earlier chunks' K / V already in the pool). */
 ecoserve_status ecoserve_op_attention_prefill(const void* q, const void* pool, int64_t num_blocks, int32_t n_heads,
                                               int32_t n_kv, int32_t head_dim, const int32_t* cu_seqlens_host,
                                               int32_t n_seq, const int32_t* block_tables, int32_t bt_ld, void* out,
-                                              void* stream);
+                                              void* stream, const int32_t* ctx_off_host);
 
 /* The same prefill attention on tcgen05 (head_dim 128 only): 128-query tiles, S and
  * P V accumulated in TMEM, K / V loaded by TMA from the pool. */
 ecoserve_status ecoserve_op_attention_prefill_tc(const void* q, const void* pool, int64_t num_blocks,
                                                  int32_t n_heads, int32_t n_kv, const int32_t* cu_seqlens_host,
                                                  int32_t n_seq, const int32_t* block_tables, int32_t bt_ld, void* out,
-                                                 void* stream);
+                                                 void* stream, const int32_t* ctx_off_host);
 
 /* Split-K decode attention over the same pool: q bf16 [B][M][D], ctx_lens int32
  * [B] (device), out bf16 [B][M*D]. n_splits x blocks_per_split must cover the

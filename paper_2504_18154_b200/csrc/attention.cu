@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(PrefillAttnArgs a) {
   const int seq = a.tiles[2 * tile], q_start = a.tiles[2 * tile + 1];
   const int tok0 = a.cu_seqlens[seq];
   const int len = a.cu_seqlens[seq + 1] - tok0;
+  const int off = a.ctx_off ? a.ctx_off[seq] : 0;  // chunked prefill: cached tokens before the chunk
   const int kvh = h / (a.n_heads / a.n_kv);
   const int* bt = a.block_tables + (int64_t)seq * a.bt_ld;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(PrefillAttnArgs a) {
       cp_async16(base + swz<D>(r, c) * 16, a.q + ((int64_t)(tok0 + qrow) * a.n_heads + h) * D + c * 8);
     }
   }
-  const int n_kv_tiles = (min(q_start + 64, len) + 63) / 64;
+  const int n_kv_tiles = (off + min(q_start + 64, len) + 63) / 64;
   auto kv_ptr = [&](const bf16* cache, int j) {
     return cache + (int64_t)bt[j] * a.blk_stride + (int64_t)kvh * 64 * D;
   };
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(PrefillAttnArgs a) {
   for (int i = 0; i < ND; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
   const int g = lane >> 2, t4 = lane & 3;
-  const int qpos0 = q_start + warp * 16 + g;  // rows g and g+8 of this warp
+  const int qpos0 = off + q_start + warp * 16 + g;  // positions of rows g and g+8 of this warp
 
   for (int j = 0; j < n_kv_tiles; ++j) {
     const int buf = j & 1;
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(PrefillAttnArgs a) {
       }
     }
     // scale, causal mask on the diagonal tile, online softmax (log2 domain)
-    const bool diag = (j * 64 + 63 > q_start);
+    const bool diag = (j * 64 + 63 > off + q_start);
     float mnew[2] = {mrow[0], mrow[1]};
 #pragma unroll
     for (int n = 0; n < 8; ++n) {

@@ -112,6 +112,7 @@ struct TcAttnParams {
   int n_heads, n_kv, layer, n_layers;
   float scale_log2;
   int pv_wait;             // experiment switch: wait for PV(j) before S(j+2) reuses its buffer
+  const int* ctx_off;      // optional [n_seq]: cached tokens before this chunk (chunked prefill)
 };
 
 template <int HP>
@@ -169,7 +170,8 @@ __global__ void __launch_bounds__(AttnCfg<HP>::THREADS, 1)
   const int seq = p.tiles[2 * tile], q_start = p.tiles[2 * tile + 1];
   const int tok0 = p.cu_seqlens[seq];
   const int len = p.cu_seqlens[seq + 1] - tok0;
-  const int n_kv = (min(q_start + TQ, len) + TK - 1) / TK;  // causal: keys < q_start + 128
+  const int off = p.ctx_off ? p.ctx_off[seq] : 0;  // chunked prefill: cached tokens before the chunk
+  const int n_kv = (off + min(q_start + TQ, len) + TK - 1) / TK;  // causal: keys < off + q_start + 128
   const int* bt = p.block_tables + (int64_t)seq * p.bt_ld;
 
   if (warp == 0) {
@@ -253,7 +255,7 @@ __global__ void __launch_bounds__(AttnCfg<HP>::THREADS, 1)
     const int e = (warp - 2) >> 2;
     const int q = warp & 3;                   // TMEM lane quarter accessible to this warp
     const int r = q * 32 + lane;              // query row = TMEM lane
-    const int qpos = q_start + r;
+    const int qpos = off + q_start + r;       // position of this query row
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + e * 256;
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < n_kv; ++j) {
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(AttnCfg<HP>::THREADS, 1)
       }
       // causal mask on the diagonal blocks; the row max in raw score units (scale > 0),
       // as an 8-way tree to keep the dependent chain short
-      if (j * TK + TK - 1 > q_start) {
+      if (j * TK + TK - 1 > off + q_start) {
 #pragma unroll
         for (int c = 0; c < TK; ++c)
           if (j * TK + c > qpos) sv[c] = -INFINITY;
@@ -337,13 +339,14 @@ __global__ void __launch_bounds__(AttnCfg<HP>::THREADS, 1)
     }
     // tcgen05.ld is warp-collective: every lane loads, rows past the sequence do not store
     const float inv = 1.f / l_run;
-    bf16* dst = p.out + (int64_t)(tok0 + qpos) * p.n_heads * HD + (h0 + e) * HD;
+    const int lrow = q_start + r;             // row of the chunk
+    bf16* dst = p.out + (int64_t)(tok0 + lrow) * p.n_heads * HD + (h0 + e) * HD;
 #pragma unroll
     for (int c0 = 0; c0 < HD; c0 += 32) {
       uint32_t v[32];
       tmem_ld32(lane_base + 128 + c0, v);
       tc_wait_ld();
-      if (qpos < len) {
+      if (lrow < len) {
 #pragma unroll
         for (int i = 0; i < 32; i += 8)
           *reinterpret_cast<uint4*>(dst + c0 + i) = make_uint4(
@@ -379,7 +382,8 @@ int make_attn_tc_maps(CUtensorMap* qmap, CUtensorMap* kvmap, const void* q, int6
 
 cudaError_t attn_prefill_tc_launch(const CUtensorMap* qmap, const CUtensorMap* kvmap, const int* cu_seqlens,
                                    const int* block_tables, int bt_ld, const int* tiles, int n_tiles, bf16* out,
-                                   int n_heads, int n_kv, int layer, int n_layers, cudaStream_t s) {
+                                   int n_heads, int n_kv, int layer, int n_layers, cudaStream_t s,
+                                   const int* ctx_off) {
   if (n_kv < 1 || n_heads % n_kv) return cudaErrorInvalidValue;
   const bool pair = (n_heads / n_kv) % 2 == 0;  // two q heads of one kv head per CTA
   cudaError_t e = pair ? ensure_smem(attn_prefill_tc_kernel<2>, AttnCfg<2>::SMEM)
@@ -397,6 +401,7 @@ cudaError_t attn_prefill_tc_launch(const CUtensorMap* qmap, const CUtensorMap* k
   p.layer = layer;
   p.n_layers = n_layers;
   p.scale_log2 = (float)(1.4426950408889634 / sqrt((double)HD));
+  p.ctx_off = ctx_off;
   {
     const char* ev = getenv("ECOSERVE_ATTN_PVWAIT");
     p.pv_wait = (ev && ev[0] == '0') ? 0 : 1;

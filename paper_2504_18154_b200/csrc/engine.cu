@@ -825,6 +825,7 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
     a.block_tables = d_bt;
     a.bt_ld = bt_ld;
     a.tiles = d_tiles;
+    a.ctx_off = nullptr;
     a.n_tiles = n_tiles;
     a.out = inst->ao;
     a.n_heads = M;

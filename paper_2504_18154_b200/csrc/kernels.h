@@ -120,6 +120,7 @@ struct PrefillAttnArgs {
   bf16* out;                // [T][M*D]
   int n_heads, n_kv;
   float scale_log2;         // log2(e) / sqrt(D)
+  const int* ctx_off;       // optional [n_seq]: cached tokens before this chunk (chunked prefill)
 };
 cudaError_t attn_prefill_launch(const PrefillAttnArgs& a, int head_dim, cudaStream_t s);
 
@@ -128,9 +129,12 @@ cudaError_t attn_prefill_launch(const PrefillAttnArgs& a, int head_dim, cudaStre
 // as rows of 128 elements (rows = num_blocks * L * 2 * Mkv * 64).
 int make_attn_tc_maps(CUtensorMap* qmap, CUtensorMap* kvmap, const void* q, int64_t q_rows, int n_heads,
                       const void* pool, int64_t pool_rows);
+// ctx_off (optional [n_seq]): tokens of each sequence already in the pool before this
+// chunk; its q rows sit at positions ctx_off + i and attend to pool keys 0..position.
 cudaError_t attn_prefill_tc_launch(const CUtensorMap* qmap, const CUtensorMap* kvmap, const int* cu_seqlens,
                                    const int* block_tables, int bt_ld, const int* tiles, int n_tiles, bf16* out,
-                                   int n_heads, int n_kv, int layer, int n_layers, cudaStream_t s);
+                                   int n_heads, int n_kv, int layer, int n_layers, cudaStream_t s,
+                                   const int* ctx_off = nullptr);
 
 // Decode split-K paged attention + combine.
 struct DecodeAttnArgs {

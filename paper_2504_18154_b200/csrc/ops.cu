@@ -159,24 +159,36 @@ ecoserve_status ecoserve_op_rmsnorm(const float* x, const int32_t* rows, const v
   return ECOSERVE_OK;
 }
 
+// chunk offsets (optional) -> device, appended after the tiles: returns the device pointer or null
+static int* append_offsets(int* d, size_t at, const int32_t* ctx_off_host, int n_seq, cudaStream_t st,
+                           cudaError_t* err) {
+  if (!ctx_off_host) return nullptr;
+  *err = cudaMemcpyAsync(d + at, ctx_off_host, sizeof(int) * n_seq, cudaMemcpyHostToDevice, st);
+  return d + at;
+}
+
 ecoserve_status ecoserve_op_attention_prefill(const void* q, const void* pool, int64_t num_blocks, int32_t n_heads,
                                               int32_t n_kv, int32_t head_dim, const int32_t* cu_seqlens_host,
                                               int32_t n_seq, const int32_t* block_tables, int32_t bt_ld, void* out,
-                                              void* stream) {
+                                              void* stream, const int32_t* ctx_off_host) {
   if (!q || !pool || !cu_seqlens_host || !block_tables || !out || n_seq < 1 || n_heads % n_kv || num_blocks < 1)
     return ECOSERVE_ERR_INVALID_ARG;
   std::vector<int> tiles;
   for (int s = 0; s < n_seq; ++s) {
     const int len = cu_seqlens_host[s + 1] - cu_seqlens_host[s];
-    if (len < 1 || (len + 63) / 64 > bt_ld) return ECOSERVE_ERR_INVALID_ARG;
+    const int off = ctx_off_host ? ctx_off_host[s] : 0;
+    if (len < 1 || off < 0 || (off + len + 63) / 64 > bt_ld) return ECOSERVE_ERR_INVALID_ARG;
     for (int qs = 0; qs < len; qs += 64) { tiles.push_back(s); tiles.push_back(qs); }
   }
   int* d = nullptr;
-  const size_t bytes = sizeof(int) * (tiles.size() + n_seq + 1);
+  const size_t bytes = sizeof(int) * (tiles.size() + 2 * n_seq + 1);
   OPCK(cudaMallocAsync((void**)&d, bytes, (cudaStream_t)stream));
   OPCK(cudaMemcpyAsync(d, cu_seqlens_host, sizeof(int) * (n_seq + 1), cudaMemcpyHostToDevice, (cudaStream_t)stream));
   OPCK(cudaMemcpyAsync(d + n_seq + 1, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice,
                        (cudaStream_t)stream));
+  cudaError_t oe = cudaSuccess;
+  int* d_off = append_offsets(d, n_seq + 1 + tiles.size(), ctx_off_host, n_seq, (cudaStream_t)stream, &oe);
+  OPCK(oe);
   PrefillAttnArgs a;
   a.q = (const bf16*)q;
   a.k_cache = (const bf16*)pool;
@@ -191,6 +203,7 @@ ecoserve_status ecoserve_op_attention_prefill(const void* q, const void* pool, i
   a.n_heads = n_heads;
   a.n_kv = n_kv;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)head_dim));
+  a.ctx_off = d_off;
   const cudaError_t e = attn_prefill_launch(a, head_dim, (cudaStream_t)stream);
   cudaFreeAsync(d, (cudaStream_t)stream);
   return e == cudaSuccess ? ECOSERVE_OK : ECOSERVE_ERR_CUDA;
@@ -199,27 +212,31 @@ ecoserve_status ecoserve_op_attention_prefill(const void* q, const void* pool, i
 ecoserve_status ecoserve_op_attention_prefill_tc(const void* q, const void* pool, int64_t num_blocks,
                                                  int32_t n_heads, int32_t n_kv, const int32_t* cu_seqlens_host,
                                                  int32_t n_seq, const int32_t* block_tables, int32_t bt_ld, void* out,
-                                                 void* stream) {
+                                                 void* stream, const int32_t* ctx_off_host) {
   if (!q || !pool || !cu_seqlens_host || !block_tables || !out || n_seq < 1 || n_heads % n_kv || num_blocks < 1)
     return ECOSERVE_ERR_INVALID_ARG;
   std::vector<int> tiles;
   for (int s = 0; s < n_seq; ++s) {
     const int len = cu_seqlens_host[s + 1] - cu_seqlens_host[s];
-    if (len < 1 || (len + 63) / 64 > bt_ld) return ECOSERVE_ERR_INVALID_ARG;
+    const int off = ctx_off_host ? ctx_off_host[s] : 0;
+    if (len < 1 || off < 0 || (off + len + 63) / 64 > bt_ld) return ECOSERVE_ERR_INVALID_ARG;
     for (int qs = 0; qs < len; qs += 128) { tiles.push_back(s); tiles.push_back(qs); }
   }
   CUtensorMap qm, km;
   if (make_attn_tc_maps(&qm, &km, q, cu_seqlens_host[n_seq], n_heads, pool, num_blocks * 2 * n_kv * 64))
     return ECOSERVE_ERR_CUDA;
   int* d = nullptr;
-  const size_t bytes = sizeof(int) * (tiles.size() + n_seq + 1);
+  const size_t bytes = sizeof(int) * (tiles.size() + 2 * n_seq + 1);
   OPCK(cudaMallocAsync((void**)&d, bytes, (cudaStream_t)stream));
   OPCK(cudaMemcpyAsync(d, cu_seqlens_host, sizeof(int) * (n_seq + 1), cudaMemcpyHostToDevice, (cudaStream_t)stream));
   OPCK(cudaMemcpyAsync(d + n_seq + 1, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice,
                        (cudaStream_t)stream));
+  cudaError_t oe = cudaSuccess;
+  int* d_off = append_offsets(d, n_seq + 1 + tiles.size(), ctx_off_host, n_seq, (cudaStream_t)stream, &oe);
+  OPCK(oe);
   const cudaError_t e = attn_prefill_tc_launch(&qm, &km, d, block_tables, bt_ld, d + n_seq + 1,
                                                (int)tiles.size() / 2, (bf16*)out, n_heads, n_kv, 0, 1,
-                                               (cudaStream_t)stream);
+                                               (cudaStream_t)stream, d_off);
   cudaFreeAsync(d, (cudaStream_t)stream);
   return e == cudaSuccess ? ECOSERVE_OK : ECOSERVE_ERR_CUDA;
 }

@@ -88,24 +88,34 @@ def rmsnorm(x: torch.Tensor, gamma: torch.Tensor, eps: float, rows=None) -> torc
     return out
 
 
-def attention_prefill(q, pool, num_blocks, n_heads, n_kv, head_dim, cu_seqlens, block_tables):
+def _offsets(ctx_off):
+    if ctx_off is None:
+        return None, None
+    off = np.ascontiguousarray(ctx_off, dtype=np.int32)
+    return off, off.ctypes.data_as(L.PI32)
+
+
+def attention_prefill(q, pool, num_blocks, n_heads, n_kv, head_dim, cu_seqlens, block_tables, ctx_off=None):
+    """ctx_off: per-sequence cached tokens before the chunk (chunked prefill), or None."""
     T = q.shape[0]
     out = torch.empty(T, n_heads * head_dim, dtype=torch.bfloat16, device=q.device)
     cu = np.ascontiguousarray(cu_seqlens, dtype=np.int32)
     n_seq = len(cu) - 1
+    off, poff = _offsets(ctx_off)
     L.check(L.load().ecoserve_op_attention_prefill(q.data_ptr(), pool.data_ptr(), num_blocks, n_heads, n_kv, head_dim,
                                                    cu.ctypes.data_as(L.PI32), n_seq, block_tables.data_ptr(),
-                                                   block_tables.shape[1], out.data_ptr(), _s()))
+                                                   block_tables.shape[1], out.data_ptr(), _s(), poff))
     return out
 
 
-def attention_prefill_tc(q, pool, num_blocks, n_heads, n_kv, cu_seqlens, block_tables):
+def attention_prefill_tc(q, pool, num_blocks, n_heads, n_kv, cu_seqlens, block_tables, ctx_off=None):
     T = q.shape[0]
     out = torch.empty(T, n_heads * 128, dtype=torch.bfloat16, device=q.device)
     cu = np.ascontiguousarray(cu_seqlens, dtype=np.int32)
+    off, poff = _offsets(ctx_off)
     L.check(L.load().ecoserve_op_attention_prefill_tc(q.data_ptr(), pool.data_ptr(), num_blocks, n_heads, n_kv,
                                                       cu.ctypes.data_as(L.PI32), len(cu) - 1, block_tables.data_ptr(),
-                                                      block_tables.shape[1], out.data_ptr(), _s()))
+                                                      block_tables.shape[1], out.data_ptr(), _s(), poff))
     return out
 
 

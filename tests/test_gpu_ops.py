@@ -189,6 +189,38 @@ def test_attention_prefill_tcgen05(ops, M, Mkv, lens):
         assert rel_err(got[cu[i]:cu[i + 1]], ref) < 1e-2, (i, S)
 
 
+@pytest.mark.parametrize("tc", [False, True])
+@pytest.mark.parametrize("M,Mkv", [(8, 2), (4, 4)])
+def test_attention_prefill_chunked(ops, tc, M, Mkv):
+    """Chunked prefill (N3 hybrid batching): the chunk's q rows sit at positions
+    ctx_off + i and attend to every pool key up to their position."""
+    D = 128
+    rng = np.random.default_rng(M + (7 if tc else 3))
+    full = [300, 129, 700, 64]               # total tokens in the pool per sequence
+    off = [0, 64, 333, 63]                   # tokens before the chunk
+    lens = [f - o for f, o in zip(full, off)]  # chunk lengths
+    nb = [(s + 63) // 64 for s in full]
+    n_blocks = sum(nb) + 3
+    pool_h, pool_d = make_pool(rng, n_blocks, Mkv, D)
+    perm = rng.permutation(n_blocks)
+    bt = np.zeros((len(full), max(nb)), dtype=np.int32)
+    k = 0
+    for i, b in enumerate(nb):
+        bt[i, :b] = perm[k:k + b]
+        k += b
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    q_h, q_d = bf16_rand(rng, (cu[-1], M, D))
+    fn = ops.attention_prefill_tc if tc else (lambda *a, **kw: ops.attention_prefill(a[0], a[1], a[2], a[3], a[4], D,
+                                                                                        *a[5:], **kw))
+    got = fn(q_d, pool_d, n_blocks, M, Mkv, cu, torch.from_numpy(bt).cuda(), ctx_off=off).float().cpu().numpy()
+    for i, S in enumerate(full):
+        ks = np.stack([pool_h[bt[i, t // 64], 0, :, t % 64, :] for t in range(S)])
+        vs = np.stack([pool_h[bt[i, t // 64], 1, :, t % 64, :] for t in range(S)])
+        qpos = off[i] + np.arange(lens[i])
+        ref = T.attention(q_h[cu[i]:cu[i + 1]], ks, vs, qpos, np.arange(S)).reshape(lens[i], M * D)
+        assert rel_err(got[cu[i]:cu[i + 1]], ref) < 1e-2, (i, S)
+
+
 @pytest.mark.parametrize("D,M,Mkv,splits,bps", [(128, 32, 8, 1, 64), (128, 32, 8, 4, 5), (32, 8, 2, 3, 7),
                                                  (128, 64, 8, 2, 9), (64, 4, 4, 1, 64)])
 def test_attention_decode(ops, D, M, Mkv, splits, bps):

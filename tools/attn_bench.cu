@@ -78,6 +78,7 @@ int main(int argc, char** argv) {
     a.block_tables = d_bt;
     a.bt_ld = bt_ld;
     a.tiles = d_tiles;
+    a.ctx_off = nullptr;
     a.n_tiles = n_tiles;
     a.out = out;
     a.n_heads = M;
