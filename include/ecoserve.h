@@ -158,6 +158,29 @@ ecoserve_status ecoserve_prefill_phase(ecoserve_instance* inst, const ecoserve_r
 ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* req_ids, int32_t n, int32_t steps,
                                       int32_t* tokens, int32_t* n_finished);
 
+/* Hybrid batching (chunked prefill: the Sarathi-style NoDG baseline
+ * on these kernels). One forward pass over prompt chunks and decode tokens together:
+ * each chunk continues its request's prompt where the previous chunk ended (a new
+ * req_id starts at token 0 and registers the request; prompt / prompt_len /
+ * max_new_tokens are read only then); each decode_ids[k] (a prefilled, unfinished
+ * request) advances by one token. Chunk rows attend to the request's cached K / V
+ * plus the chunk (causal); decode rows use the split-K decode attention.
+ * chunk_tokens[i]: the request's first token if chunk i completes its prompt, else -1;
+ * decode_tokens[k]: the next token. All-or-nothing on validation errors
+ * (INVALID_ARG, STATE for chunks of prefilled or decodes of unprefilled requests,
+ * KV_EXHAUSTED). n_chunks + n_decode <= max_batch, total tokens <= token_budget. */
+typedef struct {
+  int64_t req_id;
+  const int32_t* prompt;   /* host, the full prompt (first chunk only) */
+  int32_t prompt_len;
+  int32_t max_new_tokens;
+  int32_t chunk_len;       /* tokens of this chunk */
+} ecoserve_chunk;
+
+ecoserve_status ecoserve_hybrid_step(ecoserve_instance* inst, const ecoserve_chunk* chunks, int32_t n_chunks,
+                                     const int64_t* decode_ids, int32_t n_decode, int32_t* chunk_tokens,
+                                     int32_t* decode_tokens);
+
 /* KV migration between instances (mitosis contraction and
  * rebalancing move a running request with its paged KV instead of recomputing it).
  * A request's KV is blocks of the pool's block-major layout, so it moves as

@@ -47,6 +47,11 @@ class Request(C.Structure):
                 ("max_new_tokens", C.c_int32)]
 
 
+class Chunk(C.Structure):
+    _fields_ = [("req_id", C.c_int64), ("prompt", C.POINTER(C.c_int32)), ("prompt_len", C.c_int32),
+                ("max_new_tokens", C.c_int32), ("chunk_len", C.c_int32)]
+
+
 class InstanceStatus(C.Structure):
     _fields_ = [("alive", C.c_int32), ("n_requests", C.c_int32), ("blocks_total", C.c_int64),
                 ("blocks_used", C.c_int64)]
@@ -126,6 +131,7 @@ SIGNATURES = {
                                            I32, P, P, C.POINTER(EngineConfig), C.POINTER(P)]),
     "ecoserve_prefill_phase": (C.c_int, [P, C.POINTER(Request), I32, PI32]),
     "ecoserve_decode_phase": (C.c_int, [P, PI64, I32, I32, PI32, PI32]),
+    "ecoserve_hybrid_step": (C.c_int, [P, C.POINTER(Chunk), I32, PI64, I32, PI32, PI32]),
     "ecoserve_release": (C.c_int, [P, PI64, I32]),
     "ecoserve_kv_export": (C.c_int, [P, I64, P, I64, PI32, I32, C.POINTER(ReqState)]),
     "ecoserve_kv_import": (C.c_int, [P, C.POINTER(ReqState), PI32, P]),

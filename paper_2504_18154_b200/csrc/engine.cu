@@ -42,6 +42,7 @@ struct Req {
   int n_gen = 0;
   int last_token = -1;
   bool finished = false;
+  int prefilled = 0;  // prompt tokens whose K / V are in the pool (chunked prefill)
   std::vector<int> blocks;
 };
 
@@ -795,9 +796,25 @@ cudaError_t tp_allreduce(ecoserve_instance* inst, const float* part, int splits,
 
 }  // namespace
 
+// Hybrid (chunked-prefill + decode) batch of ecoserve_hybrid_step: rows [0, Tc) are
+// prompt chunks (prefill attention with per-chunk context offsets), rows [Tc, Tc + n_dec)
+// one decode token each (split-K decode attention over the pool).
+struct HybridTail {
+  int Tc = 0;
+  const int* d_ctx_off = nullptr;  // [n_chunks]
+  int n_dec = 0;
+  const int* d_ctx = nullptr;      // [n_dec] context incl. the current token
+  const int* d_bt = nullptr;       // [n_dec][bt_ld]
+  int bt_ld = 1;
+  const int* d_order = nullptr;    // [n_dec] longest context first
+  int n_splits = 1, bps = 1;
+  double kv_bytes = 0;
+};
+
 static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const int* d_ids, const int* d_pos,
                                           const int* d_slot, const int* d_cu, const int* d_bt, int bt_ld,
-                                          const int* d_tiles, int n_tiles, double attn_flop) {
+                                          const int* d_tiles, int n_tiles, double attn_flop,
+                                          const HybridTail* hy = nullptr) {
   cudaStream_t st = inst->stream;
   const int L = inst->L, H = inst->H, M = inst->M, D = inst->D, F = inst->F;
   const float eps = inst->shape.rms_eps;
@@ -825,18 +842,41 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
     a.block_tables = d_bt;
     a.bt_ld = bt_ld;
     a.tiles = d_tiles;
-    a.ctx_off = nullptr;
+    a.ctx_off = hy ? hy->d_ctx_off : nullptr;
     a.n_tiles = n_tiles;
     a.out = inst->ao;
     a.n_heads = M;
     a.n_kv = inst->Mkv;
     a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
-    if (inst->attn_tc)
-      LAUNCH(P_ATTN_PREFILL, attn_flop, 1,
-             attn_prefill_tc_launch(&inst->attn_qmap, &inst->attn_kvmap, d_cu, d_bt, bt_ld, d_tiles, n_tiles, inst->ao,
-                                    M, inst->Mkv, l, inst->L, st));
-    else
-      LAUNCH(P_ATTN_PREFILL, attn_flop, 1, attn_prefill_launch(a, D, st));
+    if (n_tiles > 0) {
+      if (inst->attn_tc)
+        LAUNCH(P_ATTN_PREFILL, attn_flop, 1,
+               attn_prefill_tc_launch(&inst->attn_qmap, &inst->attn_kvmap, d_cu, d_bt, bt_ld, d_tiles, n_tiles,
+                                      inst->ao, M, inst->Mkv, l, inst->L, st, a.ctx_off));
+      else
+        LAUNCH(P_ATTN_PREFILL, attn_flop, 1, attn_prefill_launch(a, D, st));
+    }
+    if (hy && hy->n_dec > 0) {  // decode rows of a hybrid batch
+      DecodeAttnArgs da;
+      da.q = inst->q + (int64_t)hy->Tc * M * D;
+      da.k_cache = k_layer(inst, l);
+      da.v_cache = v_layer(inst, l);
+      da.blk_stride = inst->blk_stride;
+      da.ctx_lens = hy->d_ctx;
+      da.block_tables = hy->d_bt;
+      da.bt_ld = hy->bt_ld;
+      da.B = hy->n_dec;
+      da.n_heads = M;
+      da.n_kv = inst->Mkv;
+      da.n_splits = hy->n_splits;
+      da.blocks_per_split = hy->bps;
+      da.part_o = inst->attn_ws;
+      da.part_ml = inst->attn_ws + (int64_t)hy->n_dec * M * hy->n_splits * D;
+      da.out = inst->ao + (int64_t)hy->Tc * M * D;
+      da.scale_log2 = a.scale_log2;
+      da.order = hy->d_order;
+      LAUNCH(P_ATTN_DECODE, hy->kv_bytes, hy->n_splits > 1 ? 2 : 1, attn_decode_launch(da, D, st));
+    }
     if (inst->tp_fused) {  // partial -> fused all-reduce + residual + RMSNorm over NVLink (N2)
       GemmEpi eo = epi_base(inst);
       eo.mode = EPI_F32;
@@ -1051,6 +1091,7 @@ ecoserve_status ecoserve_prefill_phase(ecoserve_instance* inst, const ecoserve_r
     r.S = reqs[i].prompt_len;
     r.max_new = reqs[i].max_new_tokens;
     r.prompt.assign(reqs[i].prompt, reqs[i].prompt + r.S);
+    r.prefilled = r.S;
     const int nb = (r.S + BLOCK - 1) / BLOCK;
     for (int b = 0; b < nb; ++b) {
       r.blocks.push_back(inst->free_blocks.back());
@@ -1131,6 +1172,231 @@ ecoserve_status ecoserve_prefill_phase(ecoserve_instance* inst, const ecoserve_r
       first_tokens[i] = r->last_token;
     }
     i0 = i1;
+  }
+  return ECOSERVE_OK;
+}
+
+// ---------------------------------------------------------------- hybrid batches (N3)
+ecoserve_status ecoserve_hybrid_step(ecoserve_instance* inst, const ecoserve_chunk* chunks, int32_t n_chunks,
+                                     const int64_t* decode_ids, int32_t n_decode, int32_t* chunk_tokens,
+                                     int32_t* decode_tokens) {
+  if (!inst) return ECOSERVE_ERR_INVALID_ARG;
+  if (inst->dead) return ECOSERVE_ERR_CUDA;
+  if (n_chunks < 0 || n_decode < 0 || (n_chunks > 0 && (!chunks || !chunk_tokens)) ||
+      (n_decode > 0 && (!decode_ids || !decode_tokens)) || n_chunks + n_decode > inst->B_max)
+    return ECOSERVE_ERR_INVALID_ARG;
+  if (n_chunks + n_decode == 0) return ECOSERVE_OK;
+  CK(cudaSetDevice(inst->device));
+  // ---- validate (all-or-nothing)
+  int Tc = 0;
+  int64_t need = 0;
+  std::unordered_map<int64_t, int> seen;
+  for (int i = 0; i < n_chunks; ++i) {
+    const ecoserve_chunk& c = chunks[i];
+    if (c.chunk_len < 1 || seen.count(c.req_id)) return ECOSERVE_ERR_INVALID_ARG;
+    seen[c.req_id] = i;
+    auto it = inst->reqs.find(c.req_id);
+    int pre = 0, S = 0, have = 0;
+    if (it == inst->reqs.end()) {  // first chunk of a new request
+      if (!c.prompt || c.prompt_len < 1 || c.max_new_tokens < 1 || c.prompt_len + c.max_new_tokens > inst->P_max) {
+        inst->err = "invalid request " + std::to_string(c.req_id);
+        return ECOSERVE_ERR_INVALID_ARG;
+      }
+      for (int t = 0; t < c.prompt_len; ++t)
+        if (c.prompt[t] < 0 || c.prompt[t] >= inst->V) {
+          inst->err = "token id out of range in request " + std::to_string(c.req_id);
+          return ECOSERVE_ERR_INVALID_ARG;
+        }
+      S = c.prompt_len;
+    } else {
+      if (it->second.n_gen > 0) {
+        inst->err = "chunk for an already prefilled request " + std::to_string(c.req_id);
+        return ECOSERVE_ERR_STATE;
+      }
+      pre = it->second.prefilled;
+      S = it->second.S;
+      have = (int)it->second.blocks.size();
+    }
+    if (pre + c.chunk_len > S) return ECOSERVE_ERR_INVALID_ARG;
+    need += std::max(0, (pre + c.chunk_len + BLOCK - 1) / BLOCK - have);
+    Tc += c.chunk_len;
+  }
+  std::vector<Req*> ds(n_decode);
+  for (int k = 0; k < n_decode; ++k) {
+    auto it = inst->reqs.find(decode_ids[k]);
+    if (it == inst->reqs.end() || it->second.n_gen < 1 || it->second.finished || seen.count(decode_ids[k])) {
+      inst->err = "hybrid decode of an unknown, unprefilled, finished or chunked req_id " +
+                  std::to_string(decode_ids[k]);
+      return ECOSERVE_ERR_STATE;
+    }
+    seen[decode_ids[k]] = -1 - k;
+    ds[k] = &it->second;
+    const int p = ds[k]->S + ds[k]->n_gen - 1;
+    if (p / BLOCK >= (int)ds[k]->blocks.size()) ++need;
+  }
+  const int T = Tc + n_decode;
+  if (T > inst->T_max) return ECOSERVE_ERR_INVALID_ARG;
+  if (need > (int64_t)inst->free_blocks.size()) {
+    inst->err = "KV pool exhausted";
+    return ECOSERVE_ERR_KV_EXHAUSTED;
+  }
+  // ---- register new requests, allocate blocks
+  std::vector<Req*> cs(n_chunks);
+  std::vector<int> pre(n_chunks);
+  for (int i = 0; i < n_chunks; ++i) {
+    const ecoserve_chunk& c = chunks[i];
+    auto it = inst->reqs.find(c.req_id);
+    if (it == inst->reqs.end()) {
+      Req r;
+      r.id = c.req_id;
+      r.S = c.prompt_len;
+      r.max_new = c.max_new_tokens;
+      r.prompt.assign(c.prompt, c.prompt + r.S);
+      it = inst->reqs.emplace(r.id, std::move(r)).first;
+    }
+    cs[i] = &it->second;
+    pre[i] = cs[i]->prefilled;
+    while ((int)cs[i]->blocks.size() * BLOCK < pre[i] + c.chunk_len) {
+      cs[i]->blocks.push_back(inst->free_blocks.back());
+      inst->free_blocks.pop_back();
+    }
+  }
+  for (int k = 0; k < n_decode; ++k) {
+    const int p = ds[k]->S + ds[k]->n_gen - 1;
+    if (p / BLOCK >= (int)ds[k]->blocks.size()) {
+      ds[k]->blocks.push_back(inst->free_blocks.back());
+      inst->free_blocks.pop_back();
+    }
+  }
+  // ---- metadata: ids pos slot [T] | cu [nc+1] | off [nc] | bt_c [nc][ld] | tiles | ctx [nd] | bt_d [nd][ld] | ord [nd] | lm rows
+  int bt_ld = 1, max_blocks = 1;
+  for (Req* r : cs) bt_ld = std::max(bt_ld, (int)r->blocks.size());
+  for (Req* r : ds) {
+    bt_ld = std::max(bt_ld, (int)r->blocks.size());
+    max_blocks = std::max(max_blocks, (int)r->blocks.size());
+  }
+  const int qt = inst->attn_tc ? 128 : 64;
+  std::vector<std::pair<int, int>> tiles;
+  for (int i = 0; i < n_chunks; ++i)
+    for (int qs = 0; qs < chunks[i].chunk_len; qs += qt) tiles.push_back({i, qs});
+  std::stable_sort(tiles.begin(), tiles.end(), [&](const std::pair<int, int>& a, const std::pair<int, int>& b) {
+    return pre[a.first] + a.second > pre[b.first] + b.second;  // most keys first
+  });
+  int* hm = inst->h_meta;
+  int* ids = hm;
+  int* pos = ids + T;
+  int* slot = pos + T;
+  int* cu = slot + T;
+  int* off = cu + n_chunks + 1;
+  int* bt_c = off + n_chunks;
+  int* tl = bt_c + (int64_t)n_chunks * bt_ld;
+  int* ctx = tl + 2 * tiles.size();
+  int* bt_d = ctx + n_decode;
+  int* ord = bt_d + (int64_t)n_decode * bt_ld;
+  int* lm = ord + n_decode;
+  const int64_t used = (lm - hm) + n_chunks + n_decode;
+  if (used > inst->meta_cap) {
+    inst->err = "metadata buffer too small";
+    return ECOSERVE_ERR_INVALID_ARG;
+  }
+  int t = 0, nl = 0;
+  double attn_flop = 0;
+  std::vector<int> completes(n_chunks, 0);
+  for (int i = 0; i < n_chunks; ++i) {
+    Req* r = cs[i];
+    const int len = chunks[i].chunk_len;
+    cu[i] = t;
+    off[i] = pre[i];
+    for (int j = 0; j < len; ++j, ++t) {
+      const int p = pre[i] + j;
+      ids[t] = r->prompt[p];
+      pos[t] = p;
+      slot[t] = r->blocks[p / BLOCK] * BLOCK + p % BLOCK;
+    }
+    for (int b = 0; b < bt_ld; ++b) bt_c[(int64_t)i * bt_ld + b] = b < (int)r->blocks.size() ? r->blocks[b] : 0;
+    attn_flop += 4.0 * inst->M * inst->D * ((double)len * pre[i] + 0.5 * len * (len + 1.0));
+    if (pre[i] + len == r->S) {
+      completes[i] = 1;
+      lm[nl++] = t - 1;
+    }
+  }
+  cu[n_chunks] = t;
+  for (size_t k = 0; k < tiles.size(); ++k) {
+    tl[2 * k] = tiles[k].first;
+    tl[2 * k + 1] = tiles[k].second;
+  }
+  double kv_tokens = 0;
+  for (int k = 0; k < n_decode; ++k, ++t) {
+    Req* r = ds[k];
+    const int p = r->S + r->n_gen - 1;
+    ids[t] = r->last_token;
+    pos[t] = p;
+    slot[t] = r->blocks[p / BLOCK] * BLOCK + p % BLOCK;
+    ctx[k] = p + 1;
+    kv_tokens += p + 1;
+    for (int b = 0; b < bt_ld; ++b) bt_d[(int64_t)k * bt_ld + b] = b < (int)r->blocks.size() ? r->blocks[b] : 0;
+    lm[nl++] = t;
+  }
+  for (int k = 0; k < n_decode; ++k) ord[k] = k;
+  std::stable_sort(ord, ord + n_decode, [ctx](int x, int y) { return ctx[x] > ctx[y]; });
+  HybridTail hy;
+  int* d = inst->d_meta;
+  hy.Tc = Tc;
+  hy.d_ctx_off = d + (off - hm);
+  hy.n_dec = n_decode;
+  hy.d_ctx = d + (ctx - hm);
+  hy.d_bt = d + (bt_d - hm);
+  hy.bt_ld = bt_ld;
+  hy.d_order = d + (ord - hm);
+  if (n_decode > 0) {
+    int n_splits = std::max(1, (2 * inst->num_sms + n_decode * inst->Mkv - 1) / (n_decode * inst->Mkv));
+    n_splits = std::min(std::min(n_splits, max_blocks), 64);
+    hy.bps = (max_blocks + n_splits - 1) / n_splits;
+    hy.n_splits = (max_blocks + hy.bps - 1) / hy.bps;
+    if ((int64_t)n_decode * inst->M * hy.n_splits * (inst->D + 2) > inst->attn_ws_elems) return ECOSERVE_ERR_INVALID_ARG;
+  }
+  hy.kv_bytes = kv_tokens * 2.0 * inst->Mkv * inst->D * 2.0;
+  cudaStream_t st = inst->stream;
+  CK(cudaMemcpyAsync(inst->d_meta, hm, sizeof(int) * used, cudaMemcpyHostToDevice, st));
+  const int pm = inst->prof.begin(Tc > 0 ? P_PREFILL : P_DECODE, st);
+  inst->dbg_rows.clear();
+  for (int i = 0; i < n_chunks; ++i)
+    if (inst->debug) inst->dbg_rows[cs[i]->id] = {cu[i], chunks[i].chunk_len};
+  for (int k = 0; k < n_decode; ++k)
+    if (inst->debug) inst->dbg_rows[ds[k]->id] = {Tc + k, 1};
+  ecoserve_status es = run_layers_prefill(inst, T, d, d + (pos - hm), d + (slot - hm), d + (cu - hm), d + (bt_c - hm),
+                                          bt_ld, d + (tl - hm), (int)tiles.size(), attn_flop, &hy);
+  if (es != ECOSERVE_OK) return es;
+  if (nl > 0) {
+    es = lm_head_argmax(inst, d + (lm - hm), nl, P_OTHER);
+    if (es != ECOSERVE_OK) return es;
+  }
+  inst->prof.end(pm, T, st);
+  if (nl > 0) CK(cudaMemcpyAsync(inst->h_tokens, inst->d_tokens, sizeof(int) * nl, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  inst->prof.resolve();
+  inst->prof.tokens[0] += Tc;
+  inst->prof.tokens[1] += n_decode;
+  inst->prof.h2d += sizeof(int) * used;
+  inst->prof.d2h += sizeof(int) * nl;
+  int li = 0;
+  for (int i = 0; i < n_chunks; ++i) {
+    Req* r = cs[i];
+    r->prefilled = pre[i] + chunks[i].chunk_len;
+    chunk_tokens[i] = -1;
+    if (completes[i]) {
+      r->last_token = inst->h_tokens[li++];
+      r->n_gen = 1;
+      r->finished = r->n_gen >= r->max_new;
+      chunk_tokens[i] = r->last_token;
+    }
+  }
+  for (int k = 0; k < n_decode; ++k) {
+    Req* r = ds[k];
+    r->last_token = inst->h_tokens[li++];
+    r->n_gen += 1;
+    r->finished = r->n_gen >= r->max_new;
+    decode_tokens[k] = r->last_token;
   }
   return ECOSERVE_OK;
 }
@@ -1305,6 +1571,7 @@ ecoserve_status ecoserve_kv_import(ecoserve_instance* inst, const ecoserve_req_s
   r.max_new = st->max_new_tokens;
   r.n_gen = st->n_generated;
   r.last_token = st->last_token;
+  r.prefilled = r.S;
   r.finished = r.n_gen >= r.max_new;
   r.prompt.assign(prompt, prompt + r.S);
   const int64_t bb = inst->blk_stride * (int64_t)sizeof(bf16);

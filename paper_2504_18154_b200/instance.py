@@ -161,6 +161,25 @@ class Instance:
                                                toks.ctypes.data_as(L.PI32), C.byref(nf)), self.h)
         return toks, nf.value
 
+    def hybrid_step(self, chunks: Sequence[Tuple[int, np.ndarray, int, int]], decode_ids: Sequence[int]):
+        """One hybrid (chunked-prefill + decode) forward pass (N3, Sarathi-style).
+        chunks: (req_id, full prompt int32[S], max_new_tokens, chunk_len) -- each
+        continues its request's prompt; decode_ids advance one token each.
+        Returns (chunk_tokens [-1 unless the chunk completed the prompt], decode_tokens)."""
+        nc, nd = len(chunks), len(decode_ids)
+        arr = (L.Chunk * max(nc, 1))()
+        keep = []
+        for i, (rid, prompt, g, clen) in enumerate(chunks):
+            p = np.ascontiguousarray(prompt, dtype=np.int32)
+            keep.append(p)
+            arr[i] = L.Chunk(int(rid), p.ctypes.data_as(L.PI32), len(p), int(g), int(clen))
+        ids = np.ascontiguousarray(decode_ids, dtype=np.int64)
+        ct = np.zeros(max(nc, 1), dtype=np.int32)
+        dt = np.zeros(max(nd, 1), dtype=np.int32)
+        L.check(self.lib.ecoserve_hybrid_step(self.h, arr, nc, ids.ctypes.data_as(L.PI64), nd,
+                                              ct.ctypes.data_as(L.PI32), dt.ctypes.data_as(L.PI32)), self.h)
+        return ct[:nc], dt[:nd]
+
     @property
     def block_bytes(self) -> int:
         return self.lib.ecoserve_kv_pool_bytes(C.byref(self.cshape), 64, 1)
