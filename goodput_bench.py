@@ -41,8 +41,10 @@ def main():
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--blocks", type=int, default=8000)
     ap.add_argument("--rates", type=str, default="", help="comma list: fixed probes instead of bisection")
-    ap.add_argument("--policy", choices=("padg", "nodg"), default="padg",
-                    help="padg: macro routing + rolling activation; nodg: round-robin separate batching baseline")
+    ap.add_argument("--policy", choices=("padg", "nodg", "sarathi"), default="padg",
+                    help="padg: macro routing + rolling activation; nodg: round-robin separate batching; "
+                         "sarathi: round-robin hybrid (chunked-prefill) batching")
+    ap.add_argument("--chunk-budget", type=int, default=1024, help="sarathi: tokens per hybrid iteration")
     args = ap.parse_args()
 
     import torch
@@ -78,7 +80,7 @@ def main():
             r.req_id += rid0[0]
         rid0[0] += args.n_req
         srv = PaDGServer(insts, slo_ttft, slo_tpot, reserve_tokens=237, predictor_table=(lens, ns),
-                         policy=args.policy)
+                         policy=args.policy, chunk_budget=args.chunk_budget)
         t0 = time.perf_counter()
         out = srv.run(trace, timeout_s=900)
         wall = time.perf_counter() - t0
@@ -107,8 +109,10 @@ def main():
             "instances": len(insts), "p": args.p, "slo": {"ttft_s": args.slo_ttft, "tpot_s": args.slo_tpot},
             "config": {"workload": f"{args.preset} Poisson, {args.n_req} req/probe, outputs <= {args.max_out}",
                        "shape": args.shape,
-                       "macro": f"{len(insts)} instances, " + ("rolling activation (Alg. 1/2)" if args.policy == "padg"
-                                                               else "NoDG round-robin separate batching")},
+                       "macro": f"{len(insts)} instances, " + {
+                           "padg": "rolling activation (Alg. 1/2)", "nodg": "NoDG round-robin separate batching",
+                           "sarathi": f"NoDG round-robin hybrid batching, {args.chunk_budget}-token iterations"}[
+                           args.policy]},
             "policy": args.policy,
             "predictor": {"lens": lens, "ns": ns}, "probes": probes}
     print(json.dumps(line), flush=True)

@@ -22,6 +22,12 @@ P:312-320, 675-676) on the same kernels and the same per-instanc
 prefill-priority loop: every arrival is routed immediately, round-robin, with no
 constraint check and no deferral, so every instance interleaves prefills into
 its decode stream (no rolling activation).
+
+policy="sarathi" is the NoDG hybrid-batching baseline (Sarathi-Serve):
+round-robin routing, and every worker iteration is ONE forward pass
+(Instance.hybrid_step) that decodes every running request by one token and fills
+the rest of a per-iteration token budget (`chunk_budget`) with prompt chunks,
+FIFO; a request starts decoding in the iteration after its last chunk.
 """
 from __future__ import annotations
 
@@ -67,8 +73,9 @@ class Clock:
 
 class Worker(threading.Thread):
     def __init__(self, idx: int, inst, clock: Clock, status_q: "queue.Queue", token_budget: int,
-                 decode_steps_per_poll: int = 1, max_batch: int = 256):
+                 decode_steps_per_poll: int = 1, max_batch: int = 256, hybrid_budget: int = 0):
         super().__init__(daemon=True)
+        self.hybrid_budget = hybrid_budget   # > 0: Sarathi-style hybrid iterations
         self.idx, self.inst, self.clock = idx, inst, clock
         self.inbox: "queue.Queue" = queue.Queue()
         self.status_q = status_q
@@ -101,9 +108,63 @@ class Worker(threading.Thread):
 
     def run(self):
         try:
-            self._loop()
+            if self.hybrid_budget > 0:
+                self._loop_hybrid()
+            else:
+                self._loop()
         except BaseException as e:  # surfaced by the server
             self.error = e
+
+    def _loop_hybrid(self):
+        """Sarathi-style stall-free batching: every iteration decodes all running
+        requests by one token and spends the rest of the token budget on prompt chunks."""
+        prefilled: Dict[int, int] = {}
+        self.phase = DECODE
+        while not self.stop_flag.is_set():
+            self._drain_inbox(block=False)
+            if not self.pending and not self.running:
+                self._drain_inbox(block=True)
+                continue
+            dec = list(self.running)
+            budget = self.hybrid_budget - len(dec)
+            chunks, taken = [], []
+            for r in self.pending:
+                if budget <= 0 or len(chunks) + len(dec) >= self.max_batch:
+                    break
+                done = prefilled.get(r.req_id, 0)
+                take = min(budget, r.S - done)
+                chunks.append((r.req_id, r.prompt, r.G, take))
+                taken.append((r, take))
+                budget -= take
+            t0 = self.clock.now()
+            ct, dt = self.inst.hybrid_step(chunks, [r.req_id for r in dec])
+            t = self.clock.now()
+            self.timeline.append((t0, t, "hybrid", len(dec), sum(x[1] for x in taken)))
+            fin, keep = [], []
+            for r, tok in zip(dec, dt):
+                r.tokens.append(int(tok))
+                r.n_gen += 1
+                if r.n_gen >= r.G:
+                    r.t_done_ns = t
+                    fin.append(r)
+                else:
+                    keep.append(r)
+            for (r, take), tok in zip(taken, ct):
+                prefilled[r.req_id] = prefilled.get(r.req_id, 0) + take
+                if tok >= 0:  # the prompt is complete: first token
+                    self.pending.remove(r)
+                    prefilled.pop(r.req_id, None)
+                    r.t_first_ns = r.t_decode_begin_ns = t
+                    r.n_gen = 1
+                    r.tokens.append(int(tok))
+                    if r.G <= 1:
+                        r.t_done_ns = t
+                        fin.append(r)
+                    else:
+                        keep.append(r)
+            self.running = keep
+            self._finish(fin)
+            self.push_status(fin)
 
     def _loop(self):
         while not self.stop_flag.is_set():
@@ -191,15 +252,16 @@ class PaDGServer:
 
     def __init__(self, instances: Sequence, slo_ttft_ns: int, slo_tpot_ns: int, reserve_tokens: int,
                  predictor_table=None, token_budget: int = 16384, decode_steps_per_poll: int = 1,
-                 probe_printed: bool = False, policy: str = "padg"):
-        if policy not in ("padg", "nodg"):
+                 probe_printed: bool = False, policy: str = "padg", chunk_budget: int = 1024):
+        if policy not in ("padg", "nodg", "sarathi"):
             raise ValueError(f"unknown policy {policy!r}")
         self.policy = policy
         self._rr = 0
         self.clock = Clock()
         self.status_q: "queue.Queue" = queue.Queue()
-        self.workers = [Worker(i, inst, self.clock, self.status_q, token_budget, decode_steps_per_poll)
-                        for i, inst in enumerate(instances)]
+        hb = chunk_budget if policy == "sarathi" else 0
+        self.workers = [Worker(i, inst, self.clock, self.status_q, token_budget, decode_steps_per_poll,
+                               hybrid_budget=hb) for i, inst in enumerate(instances)]
         blocks = [inst.num_blocks for inst in instances]
         self.macro = MacroScheduler(SchedConfig(len(instances), slo_ttft_ns, slo_tpot_ns, reserve_tokens, blocks,
                                                 probe_printed=probe_printed, table=predictor_table))
@@ -240,7 +302,7 @@ class PaDGServer:
             now = self.clock.now()
             while pending and pending[0].arrival_ns <= now:
                 lr = pending.popleft()
-                if self.policy == "nodg":  # immediate round-robin dispatch (NoDG baseline)
+                if self.policy != "padg":  # immediate round-robin dispatch (NoDG baselines)
                     i, self._rr = self._rr, (self._rr + 1) % len(self.workers)
                     self._send(lr, i)
                     continue

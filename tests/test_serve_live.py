@@ -45,9 +45,34 @@ class FakeInstance:
                     toks[i, s] = (rid + n) % 997
         return toks, 0
 
+    def hybrid_step(self, chunks, decode_ids):
+        toks = sum(c[3] for c in chunks) + len(decode_ids)
+        time.sleep((2e-3 + 14.3e-6 * toks) * self.scale)
+        self.calls.append(("hybrid", len(chunks), len(decode_ids), toks))
+        if not hasattr(self, "pre"):
+            self.pre = {}
+        ct = []
+        for rid, p, g, take in chunks:
+            st = self.pre.setdefault(rid, [0, len(p)])
+            assert rid not in self.gen and 0 < take <= st[1] - st[0]
+            st[0] += take
+            if st[0] == st[1]:
+                self.gen[rid] = [1, g]
+                ct.append(int(rid % 997))
+            else:
+                ct.append(-1)
+        dt = []
+        for rid in decode_ids:
+            n, g = self.gen[rid]
+            assert n < g
+            self.gen[rid][0] += 1
+            dt.append((rid + n) % 997)
+        return np.array(ct, dtype=np.int32), np.array(dt, dtype=np.int32)
+
     def release(self, ids):
         for rid in ids:
             del self.gen[rid]
+            getattr(self, "pre", {}).pop(rid, None)
 
 
 @pytest.fixture(scope="module")
@@ -100,6 +125,26 @@ def test_nodg_policy_round_robin_no_deferral(S):
     assert sorted(order) == sorted(r.inst for r in out.values())
     with pytest.raises(ValueError):
         S.PaDGServer(insts, 1, 1, 1, policy="fudg")
+
+
+def test_sarathi_policy_hybrid_iterations(S):
+    """NoDG hybrid batching (8(f) N3): every worker iteration is one hybrid step within
+    the token budget; prompts longer than the budget are split into chunks."""
+    trace = make_trace("alpaca", 30, seed=8, rate_per_s=300.0, vocab=1000)
+    for r in trace:
+        r.output_len = min(r.output_len, 5)
+    insts = [FakeInstance(scale=1.0) for _ in range(2)]
+    srv = S.PaDGServer(insts, slo_ttft_ns=8_000_000, slo_tpot_ns=SEC // 50, reserve_tokens=32,
+                       predictor_table=((16, 4096), (2_000_000, 60_000_000)), token_budget=4096, policy="sarathi",
+                       chunk_budget=48)
+    out = srv.run(trace, timeout_s=60)
+    assert all(r.t_done_ns >= 0 for r in out.values())
+    for r in out.values():
+        assert len(r.tokens) == r.G and r.t_first_ns == r.t_decode_begin_ns <= r.t_done_ns
+    for inst in insts:
+        assert inst.calls and all(c[0] == "hybrid" for c in inst.calls)
+        assert all(c[3] <= 48 or c[1] == 0 for c in inst.calls)   # budget (decode-only calls may exceed)
+    assert any(r.S > 48 for r in out.values())                    # some prompts needed several chunks
 
 
 def test_product_metrics_match_oracle_definition():
