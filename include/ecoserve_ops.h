@@ -77,11 +77,13 @@ ecoserve_status ecoserve_op_attention_prefill_tc(const void* q, const void* pool
 
 /* Split-K decode attention over the same pool: q bf16 [B][M][D], ctx_lens int32
  * [B] (device), out bf16 [B][M*D]. n_splits x blocks_per_split must cover the
- * longest context; workspace f32 [B][M][n_splits][D + 2]. */
+ * longest context; workspace f32 [B][M][n_splits][D + 2]. use_tma (head_dim 128):
+ * stage K / V by TMA (the engine's path) instead of cp.async. */
 ecoserve_status ecoserve_op_attention_decode(const void* q, const void* pool, int32_t n_heads, int32_t n_kv,
                                              int32_t head_dim, const int32_t* ctx_lens, int32_t B,
                                              const int32_t* block_tables, int32_t bt_ld, int32_t n_splits,
-                                             int32_t blocks_per_split, float* workspace, void* out, void* stream);
+                                             int32_t blocks_per_split, float* workspace, void* out, void* stream,
+                                             int32_t use_tma);
 
 #ifdef __cplusplus
 }

@@ -164,7 +164,7 @@ SIGNATURES = {
     "ecoserve_op_rmsnorm": (C.c_int, [P, P, P, P, I32, I32, F32, P]),
     "ecoserve_op_attention_prefill": (C.c_int, [P, P, I64, I32, I32, I32, PI32, I32, P, I32, P, P, PI32]),
     "ecoserve_op_attention_prefill_tc": (C.c_int, [P, P, I64, I32, I32, PI32, I32, P, I32, P, P, PI32]),
-    "ecoserve_op_attention_decode": (C.c_int, [P, P, I32, I32, I32, P, I32, P, I32, I32, I32, P, P, P]),
+    "ecoserve_op_attention_decode": (C.c_int, [P, P, I32, I32, I32, P, I32, P, I32, I32, I32, P, P, P, I32]),
 }
 
 _lib = None

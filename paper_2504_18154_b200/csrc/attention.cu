@@ -15,6 +15,7 @@
 // The pool must be zero-initialised at allocation (slots beyond a sequence's
 // length are read and masked; masked V rows must be finite).
 #include <math.h>
+#include <string.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -213,14 +214,30 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(PrefillAttnArgs a) {
 // ------------------------------------------------------------------ decode
 static constexpr int DEC_STAGES = 3;
 
-template <int D>
-__global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a) {
+// byte offset of 16-byte chunk c (0..15) of row r in a [64][128] bf16 tile staged by
+// TMA with 128B swizzle as two [64][64] panels (chunk c%8 of a panel row at c ^ (r%8))
+__device__ __forceinline__ uint32_t tma_swz(int r, int c) {
+  return (uint32_t)((c >> 3) * 8192 + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+}
+
+// TMA: K/V tiles arrive by cp.async.bulk.tensor (one elected thread, mbarrier per
+// stage) into 128B-swizzled panels; otherwise cp.async into the XOR-swizzled layout.
+template <int D, bool TMA>
+__global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a, const __grid_constant__ CUtensorMap kvmap) {
   constexpr int NK = D / 16, ND = D / 8;
-  extern __shared__ __align__(128) uint8_t sm[];
+  extern __shared__ __align__(128) uint8_t sm_raw[];
+  uint8_t* sm = TMA ? reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023))
+                    : sm_raw;
   bf16* sK = reinterpret_cast<bf16*>(sm);                  // [STAGES][64][D]
   bf16* sV = sK + DEC_STAGES * 64 * D;
   bf16* sQ = sV + DEC_STAGES * 64 * D;                     // [16][D]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sQ + 16 * D);  // [STAGES] (TMA)
   float* red = reinterpret_cast<float*>(sm);               // reused after the main loop
+  if (TMA && threadIdx.x == 0) {
+    for (int s = 0; s < DEC_STAGES; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+    tma_prefetch(&kvmap);
+  }
   pdl_trigger();
   pdl_wait();
 
@@ -245,15 +262,34 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a) {
     *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sQ) + swz<D>(r, c) * 16) = v;
   }
   auto issue = [&](int blk, int st) {
-    const int64_t off = (int64_t)bt[blk] * a.blk_stride + (int64_t)kvh * 64 * D;
-    load_tile64<D, 128>(sK + st * 64 * D, a.k_cache + off, tid);
-    load_tile64<D, 128>(sV + st * 64 * D, a.v_cache + off, tid);
+    if constexpr (TMA) {
+      if (tid == 0) {
+        // pool rows: ((block * L + layer) * 2 + kv) * Mkv * 64 + kvh * 64 + token
+        const int64_t base = ((int64_t)bt[blk] * a.n_layers + a.layer) * 2;
+        const int krow = (int)((base * a.n_kv + kvh) * 64);
+        const int vrow = (int)(((base + 1) * a.n_kv + kvh) * 64);
+        mbar_arrive_expect_tx(&full[st], 2 * 64 * D * 2);
+        for (int pn = 0; pn < 2; ++pn) {
+          tma_load_2d(reinterpret_cast<uint8_t*>(sK + st * 64 * D) + pn * 8192, &kvmap, &full[st], pn * 64, krow);
+          tma_load_2d(reinterpret_cast<uint8_t*>(sV + st * 64 * D) + pn * 8192, &kvmap, &full[st], pn * 64, vrow);
+        }
+      }
+    } else {
+      const int64_t off = (int64_t)bt[blk] * a.blk_stride + (int64_t)kvh * 64 * D;
+      load_tile64<D, 128>(sK + st * 64 * D, a.k_cache + off, tid);
+      load_tile64<D, 128>(sV + st * 64 * D, a.v_cache + off, tid);
+    }
+  };
+  // K/V tile chunk offsets (bytes) in either staging layout
+  auto kv_off = [&](int r, int c) -> uint32_t {
+    if constexpr (TMA) return tma_swz(r, c);
+    else return (uint32_t)swz<D>(r, c) * 16;
   };
   // prologue
 #pragma unroll
   for (int s = 0; s < DEC_STAGES - 1; ++s) {
     if (blk0 + s < blk1) issue(blk0 + s, s);
-    cp_async_commit();
+    if (!TMA) cp_async_commit();
   }
   __syncthreads();
   uint32_t qf[NK][4];
@@ -273,18 +309,22 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a) {
     {
       const int nb = blk + DEC_STAGES - 1;
       if (nb < blk1) issue(nb, (it + DEC_STAGES - 1) % DEC_STAGES);
-      cp_async_commit();
+      if (!TMA) cp_async_commit();
     }
-    cp_async_wait<DEC_STAGES - 1>();
-    __syncthreads();
     const int st = it % DEC_STAGES;
+    if constexpr (TMA) {
+      mbar_wait(&full[st], (it / DEC_STAGES) & 1);
+    } else {
+      cp_async_wait<DEC_STAGES - 1>();
+      __syncthreads();
+    }
     const uint32_t kb = smem_u32(sK + st * 64 * D), vb = smem_u32(sV + st * 64 * D);
     float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
     for (int kk = 0; kk < NK; ++kk) {
       uint32_t b0, b1, b2, b3;
       const int r = warp * 16 + (lane & 7) + ((lane >> 4) << 3);
-      ldmatrix_x4(kb + swz<D>(r, kk * 2 + ((lane >> 3) & 1)) * 16, b0, b1, b2, b3);
+      ldmatrix_x4(kb + kv_off(r, kk * 2 + ((lane >> 3) & 1)), b0, b1, b2, b3);
       mma_bf16_16816(s[0], qf[kk], b0, b1);
       mma_bf16_16816(s[1], qf[kk], b2, b3);
     }
@@ -332,13 +372,13 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a) {
     for (int dn = 0; dn < ND; dn += 2) {
       uint32_t b0, b1, b2, b3;
       const int r = warp * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
-      ldmatrix_x4_trans(vb + swz<D>(r, dn + (lane >> 4)) * 16, b0, b1, b2, b3);
+      ldmatrix_x4_trans(vb + kv_off(r, dn + (lane >> 4)), b0, b1, b2, b3);
       mma_bf16_16816(o[dn], af, b0, b1);
       mma_bf16_16816(o[dn + 1], af, b2, b3);
     }
     __syncthreads();
   }
-  cp_async_wait<0>();
+  if (!TMA) cp_async_wait<0>();
   __syncthreads();
   // quad sums of l
 #pragma unroll
@@ -429,14 +469,22 @@ cudaError_t attn_prefill_launch(const PrefillAttnArgs& a, int head_dim, cudaStre
 
 template <int D>
 static cudaError_t decode_d(const DecodeAttnArgs& a, cudaStream_t s) {
+  const bool tma = D == 128 && a.kvmap != nullptr;
   int smem = (2 * DEC_STAGES * 64 * D + 16 * D) * 2;
   const int red_bytes = 4 * 16 * (D + 2) * 4;
   if (smem < red_bytes) smem = red_bytes;
-  cudaError_t e = ensure_smem(attn_decode_kernel<D>, smem);
+  if (tma) smem += 1024 + 64;  // 1 KB alignment slack + stage barriers
+  cudaError_t e = tma ? ensure_smem(attn_decode_kernel<D, true>, smem) : ensure_smem(attn_decode_kernel<D, false>, smem);
   if (e != cudaSuccess) return e;
   if (a.B == 0) return cudaSuccess;
   if (a.n_heads / a.n_kv > 16) return cudaErrorInvalidValue;
-  e = launch_k(attn_decode_kernel<D>, dim3(a.B * a.n_kv, 1, a.n_splits), dim3(128), smem, s, a);
+  CUtensorMap dummy;
+  memset(&dummy, 0, sizeof(dummy));
+  const CUtensorMap& map = tma ? *a.kvmap : dummy;
+  if (tma)
+    e = launch_k(attn_decode_kernel<D, true>, dim3(a.B * a.n_kv, 1, a.n_splits), dim3(128), smem, s, a, map);
+  else
+    e = launch_k(attn_decode_kernel<D, false>, dim3(a.B * a.n_kv, 1, a.n_splits), dim3(128), smem, s, a, map);
   if (e != cudaSuccess || a.n_splits == 1) return e;
   return launch_k(attn_combine_kernel<D>, dim3(a.B, a.n_heads), dim3(D), 0, s, a);
 }

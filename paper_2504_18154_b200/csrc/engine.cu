@@ -875,6 +875,9 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
       da.out = inst->ao + (int64_t)hy->Tc * M * D;
       da.scale_log2 = a.scale_log2;
       da.order = hy->d_order;
+      da.kvmap = inst->attn_tc ? &inst->attn_kvmap : nullptr;
+      da.layer = l;
+      da.n_layers = inst->L;
       LAUNCH(P_ATTN_DECODE, hy->kv_bytes, hy->n_splits > 1 ? 2 : 1, attn_decode_launch(da, D, st));
     }
     if (inst->tp_fused) {  // partial -> fused all-reduce + residual + RMSNorm over NVLink (N2)
@@ -975,6 +978,9 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     a.out = inst->ao;
     a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
     a.order = d_order;
+    a.kvmap = inst->attn_tc ? &inst->attn_kvmap : nullptr;  // TMA staging of K / V (head_dim 128)
+    a.layer = l;
+    a.n_layers = L;
     LAUNCH(P_ATTN_DECODE, kv_bytes, n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
     if (inst->tp_fused) {  // partials -> fused all-reduce + residual + RMSNorm over NVLink (N2)
       int sp = 1;

@@ -152,6 +152,11 @@ struct DecodeAttnArgs {
   bf16* out;                // [B][M*D]
   float scale_log2;
   const int* order;         // optional [B]: sequences longest-context first (null = 0..B-1)
+  // optional (head_dim 128): TMA map over the pool as rows of 128 elements (see
+  // make_attn_tc_maps) -> K / V blocks staged by TMA instead of cp.async; layer / n_layers
+  // locate the layer in the block-major pool
+  const CUtensorMap* kvmap;
+  int layer, n_layers;
 };
 cudaError_t attn_decode_launch(const DecodeAttnArgs& a, int head_dim, cudaStream_t s);
 

@@ -244,7 +244,7 @@ ecoserve_status ecoserve_op_attention_prefill_tc(const void* q, const void* pool
 ecoserve_status ecoserve_op_attention_decode(const void* q, const void* pool, int32_t n_heads, int32_t n_kv,
                                              int32_t head_dim, const int32_t* ctx_lens, int32_t B,
                                              const int32_t* block_tables, int32_t bt_ld, int32_t n_splits,
-                                             int32_t blocks_per_split, float* workspace, void* out, void* stream) {
+                                             int32_t blocks_per_split, float* workspace, void* out, void* stream, int32_t use_tma) {
   if (!q || !pool || !ctx_lens || !block_tables || !out || B < 1 || n_heads % n_kv || n_splits < 1 ||
       blocks_per_split < 1 || (n_splits > 1 && !workspace))
     return ECOSERVE_ERR_INVALID_ARG;
@@ -266,6 +266,17 @@ ecoserve_status ecoserve_op_attention_decode(const void* q, const void* pool, in
   a.out = (bf16*)out;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)head_dim));
   a.order = nullptr;
+  a.kvmap = nullptr;
+  a.layer = 0;
+  a.n_layers = 1;
+  CUtensorMap kvm;
+  if (head_dim == 128 && use_tma) {  // the engine's TMA staging path (single-layer pool)
+    const int64_t dims[2] = {128, (int64_t)1 << 30};  // rows: an upper bound, accesses stay in the pool
+    const int64_t strides[1] = {256};
+    const int box[2] = {64, 64};
+    if (make_tmap_bf16_nd(&kvm, pool, 2, dims, strides, box)) return ECOSERVE_ERR_CUDA;
+    a.kvmap = &kvm;
+  }
   OPCK(attn_decode_launch(a, head_dim, (cudaStream_t)stream));
   return ECOSERVE_OK;
 }

@@ -119,12 +119,14 @@ def attention_prefill_tc(q, pool, num_blocks, n_heads, n_kv, cu_seqlens, block_t
     return out
 
 
-def attention_decode(q, pool, n_heads, n_kv, head_dim, ctx_lens, block_tables, n_splits, blocks_per_split):
+def attention_decode(q, pool, n_heads, n_kv, head_dim, ctx_lens, block_tables, n_splits, blocks_per_split,
+                     use_tma=False):
+    """use_tma (head_dim 128): K / V staged by TMA, the engine's path."""
     B = q.shape[0]
     out = torch.empty(B, n_heads * head_dim, dtype=torch.bfloat16, device=q.device)
     ws = torch.empty(B * n_heads * n_splits * (head_dim + 2), dtype=torch.float32, device=q.device)
     L.check(L.load().ecoserve_op_attention_decode(q.data_ptr(), pool.data_ptr(), n_heads, n_kv, head_dim,
                                                   ctx_lens.data_ptr(), B, block_tables.data_ptr(),
                                                   block_tables.shape[1], n_splits, blocks_per_split, ws.data_ptr(),
-                                                  out.data_ptr(), _s()))
+                                                  out.data_ptr(), _s(), 1 if use_tma else 0))
     return out

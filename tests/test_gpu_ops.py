@@ -221,9 +221,11 @@ def test_attention_prefill_chunked(ops, tc, M, Mkv):
         assert rel_err(got[cu[i]:cu[i + 1]], ref) < 1e-2, (i, S)
 
 
-@pytest.mark.parametrize("D,M,Mkv,splits,bps", [(128, 32, 8, 1, 64), (128, 32, 8, 4, 5), (32, 8, 2, 3, 7),
-                                                 (128, 64, 8, 2, 9), (64, 4, 4, 1, 64)])
-def test_attention_decode(ops, D, M, Mkv, splits, bps):
+@pytest.mark.parametrize("D,M,Mkv,splits,bps,tma", [(128, 32, 8, 1, 64, False), (128, 32, 8, 4, 5, False),
+                                                     (32, 8, 2, 3, 7, False), (128, 64, 8, 2, 9, False),
+                                                     (64, 4, 4, 1, 64, False), (128, 32, 8, 1, 64, True),
+                                                     (128, 32, 8, 4, 5, True), (128, 64, 8, 2, 9, True)])
+def test_attention_decode(ops, D, M, Mkv, splits, bps, tma):
     rng = np.random.default_rng(D * 3 + splits)
     ctx = [1, 64, 65, 300, 1000][: 5]
     if splits * bps * 64 < max(ctx):
@@ -239,7 +241,7 @@ def test_attention_decode(ops, D, M, Mkv, splits, bps):
         k += b
     q_h, q_d = bf16_rand(rng, (len(ctx), M, D))
     got = ops.attention_decode(q_d, pool_d, M, Mkv, D, torch.tensor(ctx, dtype=torch.int32).cuda(),
-                               torch.from_numpy(bt).cuda(), splits, bps).float().cpu().numpy()
+                               torch.from_numpy(bt).cuda(), splits, bps, use_tma=tma).float().cpu().numpy()
     for i, c in enumerate(ctx):
         ks = np.stack([pool_h[bt[i, t // 64], 0, :, t % 64, :] for t in range(c)])
         vs = np.stack([pool_h[bt[i, t // 64], 1, :, t % 64, :] for t in range(c)])
