@@ -86,8 +86,17 @@ def oracle_sample(prefill_len: int = 1024, n_dec: int = 8, dec_ctx: int = 1024, 
     """Time the fp64 oracle on ONE decoder layer of the 8B shape (bounded sample),
     extrapolated linearly to the model's 32 layers (embed / LM head excluded).
     Returns (prefill tok/s, decode tok/s, seconds spent, threads)."""
+    from threadpoolctl import threadpool_info, threadpool_limits
     from oracle.transformer import ContiguousKV, Model
     from synthetic.shapes import get_shape
+    # all host cores for the BLAS pool (torchrun exports OMP_NUM_THREADS=1 to its workers)
+    ncores = len(os.sched_getaffinity(0))
+    with threadpool_limits(limits=ncores):
+        return _oracle_sample(ContiguousKV, Model, get_shape, prefill_len, n_dec, dec_ctx, dec_steps, seed,
+                              threadpool_info)
+
+
+def _oracle_sample(ContiguousKV, Model, get_shape, prefill_len, n_dec, dec_ctx, dec_steps, seed, threadpool_info):
     from synthetic.weights import LAYER_TENSORS, _draw, _rng, bf16_bits_to_f32, f32_to_bf16_bits, layer_shapes
     full = get_shape("8b")
     shape = full.with_layers(1)
@@ -113,7 +122,7 @@ def oracle_sample(prefill_len: int = 1024, n_dec: int = 8, dec_ctx: int = 1024, 
             m.layer(0, rng.standard_normal((1, shape.hidden)), np.array([dec_ctx + s]), c)
     t_dec = time.perf_counter() - t1
     L = full.n_layers
-    threads = len(os.sched_getaffinity(0))
+    threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     return prefill_len / (t_pre * L), n_dec * dec_steps / (t_dec * L), t_pre + t_dec, threads
 
 
@@ -142,7 +151,7 @@ def run_reference(args, rank: int, world: int):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "8b-padg-cycle (oracle sample)", "shape": "llama3-8b", "sample": sample},
-            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": len(os.sched_getaffinity(0)),
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": thr,
                              "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
