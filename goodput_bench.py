@@ -35,6 +35,9 @@ def main():
     ap.add_argument("--slo-tpot", type=float, default=0.1)
     ap.add_argument("--p", type=float, default=0.9)
     ap.add_argument("--n-req", type=int, default=300)
+    ap.add_argument("--duration", type=float, default=0.0,
+                    help="> 0: requests per probe = max(n_req, rate x duration), so a probe measures a steady "
+                         "state instead of absorbing one burst")
     ap.add_argument("--max-out", type=int, default=1024)
     ap.add_argument("--lo", type=float, default=4.0)
     ap.add_argument("--hi", type=float, default=160.0)
@@ -73,12 +76,12 @@ def main():
     rid0 = [0]
 
     def attain_at(rate: float) -> float:
-        trace = make_trace(args.preset, args.n_req, seed=int(rate * 1000) % 100003, rate_per_s=rate,
-                           vocab=shape.vocab)
+        n_req = max(args.n_req, int(rate * args.duration))
+        trace = make_trace(args.preset, n_req, seed=int(rate * 1000) % 100003, rate_per_s=rate, vocab=shape.vocab)
         for r in trace:
             r.output_len = min(r.output_len, args.max_out)
             r.req_id += rid0[0]
-        rid0[0] += args.n_req
+        rid0[0] += n_req
         srv = PaDGServer(insts, slo_ttft, slo_tpot, reserve_tokens=237, predictor_table=(lens, ns),
                          policy=args.policy, chunk_budget=args.chunk_budget)
         t0 = time.perf_counter()
@@ -90,7 +93,7 @@ def main():
         fin = [x for x in recs if x["finished"]]
         toks = sum(r.G for r in out.values() if r.t_done_ns >= 0)
         per_inst = [sum(1 for r in out.values() if r.inst == i) for i in range(len(insts))]
-        probes.append({"rate": round(rate, 3), "attainment": round(att, 4), "wall_s": round(wall, 2),
+        probes.append({"rate": round(rate, 3), "n_req": n_req, "attainment": round(att, 4), "wall_s": round(wall, 2),
                        "ttft_p90_s": round(float(np.percentile([x["ttft_ns"] for x in fin], 90)) / 1e9, 4) if fin else None,
                        "tpot_p90_ms": round(float(np.percentile([x["tpot_ns"] for x in fin], 90)) / 1e6, 3) if fin else None,
                        "out_tok_s": round(toks / wall, 1), "per_instance": per_inst,
@@ -107,7 +110,8 @@ def main():
         gp = MX.bisect_goodput(attain_at, args.p, args.lo, args.hi, args.iters)
     line = {"metric": "goodput req/s at TTFT/TPOT SLO", "value": gp, "unit": "req/s", "n_gpus": n_gpu,
             "instances": len(insts), "p": args.p, "slo": {"ttft_s": args.slo_ttft, "tpot_s": args.slo_tpot},
-            "config": {"workload": f"{args.preset} Poisson, {args.n_req} req/probe, outputs <= {args.max_out}",
+            "config": {"workload": f"{args.preset} Poisson, max({args.n_req}, rate x {args.duration:g} s) req/probe, "
+                                   f"outputs <= {args.max_out}",
                        "shape": args.shape,
                        "macro": f"{len(insts)} instances, " + {
                            "padg": "rolling activation (Alg. 1/2)", "nodg": "NoDG round-robin separate batching",

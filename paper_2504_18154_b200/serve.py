@@ -201,7 +201,11 @@ class Worker(threading.Thread):
                     self.running += self.waiting
                     self.waiting = []
                 t0 = self.clock.now()
-                toks, _ = self.inst.decode([r.req_id for r in self.running], self.k)
+                ids = [r.req_id for r in self.running]
+                # decode phases of <= max_batch requests (the instance's batch limit)
+                parts = [self.inst.decode(ids[i:i + self.max_batch], self.k)[0]
+                         for i in range(0, len(ids), self.max_batch)]
+                toks = np.concatenate(parts, axis=0) if parts else np.zeros((0, self.k), np.int32)
                 t = self.clock.now()
                 self.timeline.append((t0, t, "decode", len(self.running)))
                 fin, keep = [], []
