@@ -90,6 +90,22 @@ class Worker(threading.Thread):
         self.finished: List[LiveReq] = []
         self.timeline: List[tuple] = []
         self.error: Optional[BaseException] = None
+        # KV admission control (FCFS): a request starts its prefill only when the blocks
+        # its prompt + output can reach fit next to those committed to live requests
+        # (there is no preemption, reading A14), so no policy can exhaust the pool
+        self.total_blocks = int(getattr(inst, "num_blocks", 1 << 30))
+        self.committed: Dict[int, int] = {}
+        self.commit_sum = 0
+
+    def _fits(self, r: LiveReq) -> bool:
+        return r.req_id in self.committed or \
+            self.commit_sum + (r.S + r.G + 63) // 64 <= self.total_blocks
+
+    def _commit(self, r: LiveReq) -> None:
+        if r.req_id not in self.committed:
+            need = (r.S + r.G + 63) // 64
+            self.committed[r.req_id] = need
+            self.commit_sum += need
 
     def push_status(self, fin: Sequence[LiveReq] = ()):
         live = list(self.pending) + self.waiting + self.running
@@ -122,15 +138,16 @@ class Worker(threading.Thread):
         self.phase = DECODE
         while not self.stop_flag.is_set():
             self._drain_inbox(block=False)
-            if not self.pending and not self.running:
+            if not self.running and (not self.pending or not self._fits(self.pending[0])):
                 self._drain_inbox(block=True)
                 continue
             dec = list(self.running)
             budget = self.hybrid_budget - len(dec)
             chunks, taken = [], []
             for r in self.pending:
-                if budget <= 0 or len(chunks) + len(dec) >= self.max_batch:
+                if budget <= 0 or len(chunks) + len(dec) >= self.max_batch or not self._fits(r):
                     break
+                self._commit(r)
                 done = prefilled.get(r.req_id, 0)
                 take = min(budget, r.S - done)
                 chunks.append((r.req_id, r.prompt, r.G, take))
@@ -169,13 +186,14 @@ class Worker(threading.Thread):
     def _loop(self):
         while not self.stop_flag.is_set():
             self._drain_inbox(block=False)
-            if self.pending:
+            if self.pending and self._fits(self.pending[0]):
                 if self.phase != PREFILL:
                     self.phase, self.t_switch = PREFILL, self.clock.now()
                 batch, tok = [], 0
                 while self.pending and len(batch) < self.max_batch and \
-                        (not batch or tok + self.pending[0].S <= self.budget):
+                        (not batch or tok + self.pending[0].S <= self.budget) and self._fits(self.pending[0]):
                     r = self.pending.popleft()
+                    self._commit(r)
                     batch.append(r)
                     tok += r.S
                 t0 = self.clock.now()
@@ -229,6 +247,8 @@ class Worker(threading.Thread):
         if fin:
             self.inst.release([r.req_id for r in fin])
             self.finished += fin
+            for r in fin:
+                self.commit_sum -= self.committed.pop(r.req_id, 0)
 
 
 def profile_prefill(inst, lens=(128, 256, 512, 1024, 2048, 4096), vocab: int = 1000, reps: int = 2):
