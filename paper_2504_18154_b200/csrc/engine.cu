@@ -133,9 +133,8 @@ struct ecoserve_instance {
   // fused TP all-reduce over NVLink peer memory (N2): receive rows / flags written by the peer
   bool tp_fused = false;
   int tp_rows_max = 0, tp_epoch = 0;
-  float* tp_recv = nullptr;      // [2][tp_rows_max][H]
-  int* tp_flags = nullptr;       // [2][tp_rows_max]
-  float* tp_part = nullptr;      // prefill O / down partials [T_max][H]
+  float* tp_recv = nullptr;      // [2 parity][2 rank][tp_rows_max][H]: both ranks' O / down outputs
+  int* tp_flags = nullptr;       // [0]: epoch of the peer's last GEMM push; [64 + par * rows_max + row]: decode row flags
   float* peer_recv = nullptr;    // the peer's tp_recv / tp_flags (peer pointer or IPC mapping)
   int* peer_flags = nullptr;
   bool peer_ipc = false;
@@ -270,10 +269,9 @@ struct TpPeerInfo {
 ecoserve_status tp_setup_peer(ecoserve_instance* inst) {
   inst->tp_rows_max = std::max(inst->T_max, inst->B_max);
   const int64_t rows = inst->tp_rows_max;
-  CK(cudaMalloc(&inst->tp_recv, sizeof(float) * 2 * rows * inst->H));
-  CK(cudaMalloc(&inst->tp_flags, sizeof(int) * 2 * rows));
-  CK(cudaMemset(inst->tp_flags, 0, sizeof(int) * 2 * rows));
-  CK(cudaMalloc(&inst->tp_part, sizeof(float) * (int64_t)inst->T_max * inst->H));
+  CK(cudaMalloc(&inst->tp_recv, sizeof(float) * 4 * rows * inst->H));
+  CK(cudaMalloc(&inst->tp_flags, sizeof(int) * (64 + 2 * rows)));
+  CK(cudaMemset(inst->tp_flags, 0, sizeof(int) * (64 + 2 * rows)));
   TpPeerInfo mine{};
   mine.pid = (int)getpid();
   mine.device = inst->device;
@@ -374,7 +372,7 @@ void ecoserve_instance_destroy(ecoserve_instance* inst) {
     if (inst->peer_recv) cudaIpcCloseMemHandle(inst->peer_recv);
     if (inst->peer_flags) cudaIpcCloseMemHandle(inst->peer_flags);
   }
-  for (void* p : {(void*)inst->tp_recv, (void*)inst->tp_flags, (void*)inst->tp_part, (void*)inst->d_wmaps})
+  for (void* p : {(void*)inst->tp_recv, (void*)inst->tp_flags, (void*)inst->d_wmaps})
     if (p) cudaFree(p);
   if (inst->comm) ncclCommDestroy(inst->comm);
   if (inst->own_stream && inst->stream) cudaStreamDestroy(inst->stream);
@@ -755,7 +753,26 @@ cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const 
   return splitk_reduce_launch(red, inst->part, splits, B, n_out, n_out, e, inst->stream);
 }
 
-// Decode projection as raw f32 partials [splits][B][n_out] in inst->part (TP fused path).
+// TP=2 fused path (N2): the receive plane of rank `r` for the exchange of epoch `ep`
+// on this GPU (mine) or on the peer (over NVLink).
+float* tp_plane(ecoserve_instance* inst, bool peer, int ep, int r) {
+  float* base = peer ? inst->peer_recv : inst->tp_recv;
+  return base + ((int64_t)(ep & 1) * 2 + r) * inst->tp_rows_max * inst->H;
+}
+
+// The epilogue of an O / down projection of a TP rank: its f32 output goes to its own
+// receive plane here and, tile by tile while the GEMM runs, to the peer's (out2).
+GemmEpi tp_push_epi(ecoserve_instance* inst, int ep) {
+  GemmEpi e = epi_base(inst);
+  e.out = tp_plane(inst, false, ep, inst->tp_rank);
+  e.resid = reinterpret_cast<float*>(e.out);
+  e.ldo = e.ldr = inst->H;
+  e.out2 = tp_plane(inst, true, ep, inst->tp_rank);
+  return e;
+}
+
+// Decode O / down projection of a TP rank: raw f32 split partials [splits][B][n_out] in
+// inst->part (bulk-stored, L2-resident), summed and pushed row by row by tp_push_rows.
 cudaError_t decode_partials(ecoserve_instance* inst, const CUtensorMap& wmap, const ActMaps& xm, int n_out, int K,
                             int B, int* splits_out) {
   const int bn = B <= 64 ? 64 : 128;
@@ -770,31 +787,61 @@ cudaError_t decode_partials(ecoserve_instance* inst, const CUtensorMap& wmap, co
                        inst->stream);
 }
 
-// TP=2 fused all-reduce + residual + RMSNorm over the peer's receive rows (N2)
-cudaError_t tp_allreduce(ecoserve_instance* inst, const float* part, int splits, int64_t plane, int64_t ldp, int rows,
-                         const bf16* gamma, bf16* h) {
-  TpAllreduceArgs a;
-  a.part = part;
+cudaError_t tp_push_rows(ecoserve_instance* inst, int ep, int splits, int rows, const bf16* gamma, bf16* h) {
+  TpRowsArgs a;
+  a.part = inst->part;
   a.splits = splits;
-  a.plane = plane;
-  a.ldp = ldp;
+  a.plane = (int64_t)rows * inst->H;
+  a.ldp = inst->H;
   a.x = inst->x;
   a.gamma = gamma;
   a.h = h;
   a.eps = inst->shape.rms_eps;
   a.rows = rows;
-  a.rows_max = inst->tp_rows_max;
   a.H = inst->H;
   a.rank = inst->tp_rank;
-  a.epoch = ++inst->tp_epoch;
-  a.peer_recv = inst->peer_recv;
-  a.peer_flags = inst->peer_flags;
-  a.my_recv = inst->tp_recv;
-  a.my_flags = inst->tp_flags;
+  a.epoch = ep;
+  a.peer_recv = tp_plane(inst, true, ep, 0);
+  a.my_recv = tp_plane(inst, false, ep, 0);
+  a.peer_flags = inst->peer_flags + 64 + (ep & 1) * inst->tp_rows_max;
+  a.my_flags = inst->tp_flags + 64 + (ep & 1) * inst->tp_rows_max;
+  return tp_push_rows_launch(a, inst->num_sms, inst->stream);
+}
+
+// After the push GEMM of epoch `ep`: wait for the peer's push, x = (x + acc_0) + acc_1,
+// and the next RMSNorm (gamma null: x only).
+cudaError_t tp_allreduce(ecoserve_instance* inst, int ep, int rows, const bf16* gamma, bf16* h) {
+  TpAllreduceArgs a;
+  a.recv0 = tp_plane(inst, false, ep, 0);
+  a.recv1 = tp_plane(inst, false, ep, 1);
+  a.x = inst->x;
+  a.gamma = gamma;
+  a.h = h;
+  a.eps = inst->shape.rms_eps;
+  a.rows = rows;
+  a.H = inst->H;
+  a.epoch = ep;
+  a.peer_flag = inst->peer_flags;
+  a.my_flag = inst->tp_flags;
   return tp_allreduce_norm_launch(a, inst->num_sms, inst->stream);
 }
 
 }  // namespace
+
+// Context splits of the decode attention: split only as much as needed for
+// B x Mkv x splits to fill the SMs about twice (uniform 512-token chunks were measured
+// slower: more CTAs, partials, combine). ECOSERVE_ATTN_SPLITS=n forces n (sweeps).
+static int decode_attn_splits(const ecoserve_instance* inst, int B, int max_blocks, int* bps) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("ECOSERVE_ATTN_SPLITS");
+    forced = e ? std::max(0, atoi(e)) : 0;
+  }
+  int n = forced > 0 ? forced : std::max(1, (2 * inst->num_sms + B * inst->Mkv - 1) / (B * inst->Mkv));
+  n = std::max(1, std::min(std::min(n, max_blocks), 64));
+  *bps = (max_blocks + n - 1) / n;
+  return (max_blocks + *bps - 1) / *bps;
+}
 
 // Hybrid (chunked-prefill + decode) batch of ecoserve_hybrid_step: rows [0, Tc) are
 // prompt chunks (prefill attention with per-chunk context offsets), rows [Tc, Tc + n_dec)
@@ -880,14 +927,13 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
       da.n_layers = inst->L;
       LAUNCH(P_ATTN_DECODE, hy->kv_bytes, hy->n_splits > 1 ? 2 : 1, attn_decode_launch(da, D, st));
     }
-    if (inst->tp_fused) {  // partial -> fused all-reduce + residual + RMSNorm over NVLink (N2)
-      GemmEpi eo = epi_base(inst);
+    if (inst->tp_fused) {  // O-proj pushing its tiles to the peer, then all-reduce + residual + RMSNorm (N2)
+      const int ep = ++inst->tp_epoch;
+      GemmEpi eo = tp_push_epi(inst, ep);
       eo.mode = EPI_F32;
-      eo.out = inst->tp_part;
-      eo.ldo = H;
       LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * M * D, 1,
              prefill_gemm(inst, inst->m_ao.a, w.o_a, w.o_b, T, H, M * D, eo));
-      LAUNCH(P_OTHER, 0, 1, tp_allreduce(inst, inst->tp_part, 1, (int64_t)T * H, H, T, w.ffn_norm, inst->h));
+      LAUNCH(P_OTHER, 0, 1, tp_allreduce(inst, ep, T, w.ffn_norm, inst->h));
     } else {
       GemmEpi eo = resid_epi(inst);
       eo.mode = resid_mode_prefill(inst);
@@ -903,16 +949,13 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
     LAUNCH(P_GEMM_PREFILL, 2.0 * T * 2 * F * H, 1,
            prefill_gemm(inst, inst->m_h.a, w.gu_a, w.gu_b, T, 2 * F, H, eg));
     if (inst->tp_fused) {  // the next layer's attention norm rides along (the final norm is the LM head's)
-      GemmEpi ed = epi_base(inst);
+      const int ep = ++inst->tp_epoch;
+      GemmEpi ed = tp_push_epi(inst, ep);
       ed.mode = EPI_F32;
-      ed.out = inst->tp_part;
-      ed.ldo = H;
       LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * F, 1,
              prefill_gemm(inst, inst->m_act.a, w.d_a, w.d_b, T, H, F, ed));
       const bool last = l + 1 == L;
-      LAUNCH(P_OTHER, 0, 1,
-             tp_allreduce(inst, inst->tp_part, 1, (int64_t)T * H, H, T, last ? nullptr : inst->lw[l + 1].attn_norm,
-                          inst->h));
+      LAUNCH(P_OTHER, 0, 1, tp_allreduce(inst, ep, T, last ? nullptr : inst->lw[l + 1].attn_norm, inst->h));
       h_ready = !last;
     } else {
       GemmEpi ed = resid_epi(inst);
@@ -937,12 +980,8 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
   const float eps = inst->shape.rms_eps;
   LAUNCH(P_OTHER, 0, 1, embed_launch(d_ids, inst->embed, inst->x, B, H, st));
   if (inst->debug) CK(cudaMemcpyAsync(inst->dbg, inst->x, sizeof(float) * (int64_t)B * H, cudaMemcpyDeviceToDevice, st));
-  // split the context only as much as needed for B x Mkv x splits to fill the SMs about
-  // twice (uniform 512-token chunks were measured slower: more CTAs, partials, combine)
-  int n_splits = std::max(1, (2 * inst->num_sms + B * inst->Mkv - 1) / (B * inst->Mkv));
-  n_splits = std::min(std::min(n_splits, max_blocks), 64);
-  const int bps = (max_blocks + n_splits - 1) / n_splits;
-  n_splits = (max_blocks + bps - 1) / bps;
+  int bps = 1;
+  int n_splits = decode_attn_splits(inst, B, max_blocks, &bps);
   if ((int64_t)B * M * n_splits * (D + 2) > inst->attn_ws_elems) return ECOSERVE_ERR_INVALID_ARG;
   // RMSNorms fused into the split-K reduction of the preceding O / down projection (TP=1)
   const bool can_fuse = inst->tp == 1;
@@ -982,10 +1021,11 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     a.layer = l;
     a.n_layers = L;
     LAUNCH(P_ATTN_DECODE, kv_bytes, n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
-    if (inst->tp_fused) {  // partials -> fused all-reduce + residual + RMSNorm over NVLink (N2)
+    if (inst->tp_fused) {  // partials -> fused push + all-reduce + residual + RMSNorm over NVLink (N2)
+      const int ep = ++inst->tp_epoch;
       int sp = 1;
       LAUNCH(P_GEMM_DECODE, 2.0 * H * M * D, 1, decode_partials(inst, w.o_a, inst->m_ao, H, M * D, B, &sp));
-      LAUNCH(P_OTHER, 0, 1, tp_allreduce(inst, inst->part, sp, (int64_t)B * H, H, B, w.ffn_norm, inst->h));
+      LAUNCH(P_OTHER, 0, 1, tp_push_rows(inst, ep, sp, B, w.ffn_norm, inst->h));
     } else {
       GemmEpi eo = resid_epi(inst);
       set_prefetch(inst, eo, 4 * l + 2, 2 * F, H, B);  // gate/up next
@@ -1005,11 +1045,12 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     // attention norm, or after the last layer the final norm (into the LM-head input)
     const bool last = l + 1 == L;
     if (inst->tp_fused) {
+      const int ep = ++inst->tp_epoch;
       int sp = 1;
       LAUNCH(P_GEMM_DECODE, 2.0 * H * F, 1, decode_partials(inst, w.d_a, inst->m_act, H, F, B, &sp));
       LAUNCH(P_OTHER, 0, 1,
-             tp_allreduce(inst, inst->part, sp, (int64_t)B * H, H, B,
-                          last ? inst->final_norm : inst->lw[l + 1].attn_norm, last ? inst->hl : inst->h));
+             tp_push_rows(inst, ep, sp, B, last ? inst->final_norm : inst->lw[l + 1].attn_norm,
+                          last ? inst->hl : inst->h));
       fused = true;
     } else {
       GemmEpi ed = resid_epi(inst);
@@ -1355,10 +1396,7 @@ ecoserve_status ecoserve_hybrid_step(ecoserve_instance* inst, const ecoserve_chu
   hy.bt_ld = bt_ld;
   hy.d_order = d + (ord - hm);
   if (n_decode > 0) {
-    int n_splits = std::max(1, (2 * inst->num_sms + n_decode * inst->Mkv - 1) / (n_decode * inst->Mkv));
-    n_splits = std::min(std::min(n_splits, max_blocks), 64);
-    hy.bps = (max_blocks + n_splits - 1) / n_splits;
-    hy.n_splits = (max_blocks + hy.bps - 1) / hy.bps;
+    hy.n_splits = decode_attn_splits(inst, n_decode, max_blocks, &hy.bps);
     if ((int64_t)n_decode * inst->M * hy.n_splits * (inst->D + 2) > inst->attn_ws_elems) return ECOSERVE_ERR_INVALID_ARG;
   }
   hy.kv_bytes = kv_tokens * 2.0 * inst->Mkv * inst->D * 2.0;

@@ -83,11 +83,19 @@ __device__ __forceinline__ void epi_rows(const GemmEpi& e, int m, int n0, int n_
   switch (e.mode) {
     case EPI_F32: {
       float* o = reinterpret_cast<float*>(e.out) + (int64_t)m * e.ldo + n0;
+      float* o2 = e.out2 ? e.out2 + (int64_t)m * e.ldo + n0 : nullptr;  // TP push (peer plane)
       if (ncols == 32) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(f[i], f[i + 1], f[i + 2], f[i + 3]);
+        for (int i = 0; i < 32; i += 4) {
+          const float4 q4 = make_float4(f[i], f[i + 1], f[i + 2], f[i + 3]);
+          *reinterpret_cast<float4*>(o + i) = q4;
+          if (o2) *reinterpret_cast<float4*>(o2 + i) = q4;
+        }
       } else {
-        for (int i = 0; i < ncols; ++i) o[i] = f[i];
+        for (int i = 0; i < ncols; ++i) {
+          o[i] = f[i];
+          if (o2) o2[i] = f[i];
+        }
       }
     } break;
     case EPI_BF16: {
@@ -198,8 +206,11 @@ __device__ __forceinline__ void epi_swap(const GemmEpi& e, int m, int m_rows, in
         for (int i = 0; i < ncols; ++i) e.resid[(int64_t)(n0 + i) * e.ldr + m] += f[i];
     } break;
     case EPI_SWAP_STORE: {
-      if (mv)
+      if (mv) {
         for (int i = 0; i < ncols; ++i) e.resid[(int64_t)(n0 + i) * e.ldr + m] = f[i];
+        if (e.out2)  // TP push: the peer's receive plane (a warp writes 128 contiguous bytes per token)
+          for (int i = 0; i < ncols; ++i) e.out2[(int64_t)(n0 + i) * e.ldr + m] = f[i];
+      }
     } break;
     case EPI_SWAP_SILU: {
       bf16* o = reinterpret_cast<bf16*>(e.out);
@@ -688,6 +699,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       if (threadIdx.x == 64) trace_mark(epi, 4);  // (last) epilogue done
     }
+    if (epi.out2) __threadfence_system();  // TP push complete before the grid ends
   }
   tc_fence_before();
   __syncthreads();
@@ -984,7 +996,8 @@ struct Gemm2Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = 6;
   static constexpr int TMEM_COLS = 512;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int PUSH_STG = 4 * 32 * 32 * 4;  // TP push staging, 16 KB (after the barriers)
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + PUSH_STG;
 };
 
 // Tile order of the persistent pair GEMM: bands of GM token panels (A), weight panels
@@ -1026,6 +1039,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   const int kb_total = (K + BK - 1) / BK;
   const int n_work = m_tiles * n_tiles;
   const int band = epi.band > 0 ? epi.band : 16;  // token panels per band (tile_mn)
+  // TP push epilogue (f32 output to this GPU and the peer): needs 16-byte aligned rows
+  const bool push = epi.out2 && epi.mode == EPI_F32 && n_rows % 32 == 0 && epi.ldo % 4 == 0;
+  uint8_t* push_stg = smem + C::STAGES * C::STAGE_BYTES + 256;  // [4 warps][32][32] f32, after the barriers
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -1129,18 +1145,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_after();
       const int m = mt * 2 * BM + rank * BM + q * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(tbase + c0, v);
-        tc_wait_ld();
-        const int n0 = nt * BN + c0;
-        if (m < m_rows && n0 < n_rows) epi_rows(epi, m, n0, n_rows, v);
+      if (push) {
+        // TP push (N2): this warp's 32 x 32 f32 block goes through smem (16-byte chunks
+        // XOR-swizzled by row) so that every store instruction writes 4 token rows x 128
+        // contiguous bytes -- to this GPU's receive plane and over NVLink to the peer's
+        const int m_w = mt * 2 * BM + rank * BM + q * 32;
+        const uint32_t stg = smem_u32(push_stg) + (uint32_t)(q * 4096);
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tbase + c0, v);
+          tc_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            sts128(stg + (uint32_t)(lane * 128 + ((c ^ (lane & 7)) * 16)),
+                   make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]));
+          __syncwarp();
+          const int n0 = nt * BN + c0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int rr = 4 * j + (lane >> 3), cc = lane & 7;
+            const uint4 val = lds128(stg + (uint32_t)(rr * 128 + ((cc ^ (rr & 7)) * 16)));
+            if (m_w + rr < m_rows && n0 < n_rows) {
+              const int64_t off = (int64_t)(m_w + rr) * epi.ldo + n0 + 4 * cc;
+              *reinterpret_cast<uint4*>(reinterpret_cast<float*>(epi.out) + off) = val;
+              *reinterpret_cast<uint4*>(epi.out2 + off) = val;
+            }
+          }
+          __syncwarp();
+        }
+      } else {
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tbase + c0, v);
+          tc_wait_ld();
+          const int n0 = nt * BN + c0;
+          if (m < m_rows && n0 < n_rows) epi_rows(epi, m, n0, n_rows, v);
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_peer0(&tempty_bar[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (push) __threadfence_system();  // TP push complete before the grid ends
   }
   tc_fence_before();
   __syncthreads();
@@ -1245,12 +1292,31 @@ int gemm_choose_splits(int m_rows, int n_rows, int K, int bn, int num_sms, int m
   return best;
 }
 
+// Split-K factor of a swap-AB decode projection (one 128-row weight tile per work unit,
+// one CTA per SM): the s in 1..4 with the fewest K blocks streamed by the busiest CTA
+// (waves x K blocks per split), plus ~half a block per split for the reduction. This
+// matches the measured sweep on the 8B shapes (QKV 3, O 4, down 4) and avoids
+// the 160-unit second wave the old "tiles x s ~ SMs" rule gave the 70B/TP=2 QKV (40 tiles).
 int gemm_decode_splits(int m_rows, int K, int num_sms) {
   const int tiles = (m_rows + BM - 1) / BM;
+  // tiles covering >= 3/4 of the SMs run unsplit: their epilogue (SiLU, LM-head argmax)
+  // stays in the GEMM, which the sweep measured faster than partials + a reduction
   if (4 * tiles >= 3 * num_sms) return 1;
-  int s = (num_sms + tiles / 2) / tiles;
-  s = s < 2 ? 2 : s > 4 ? 4 : s;
-  return gemm_effective_splits(K, s);
+  const int kb_total = (K + BK - 1) / BK;
+  int best = 1;
+  double best_cost = 1e30;
+  for (int s = 1; s <= 4; ++s) {
+    const int eff = gemm_effective_splits(K, s);
+    if (eff != s) continue;
+    const int kb_per = (kb_total + eff - 1) / eff;
+    const int waves = (tiles * eff + num_sms - 1) / num_sms;
+    const double cost = (double)waves * kb_per + (eff > 1 ? 0.5 * eff : 0.0);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = eff;
+    }
+  }
+  return best;
 }
 
 int gemm_smem_bytes(int bn) {

@@ -68,6 +68,10 @@ struct GemmEpi {
   // global memory; geometry m_rows / K / splits / token tiles of that GEMM)
   const CUtensorMap* pf_map;
   int pf_m_rows, pf_K, pf_splits, pf_n_tiles, pf_kb;
+  // TP push (N2): when set, the f32 epilogues (EPI_F32, EPI_SWAP_STORE) also store every
+  // output element here -- the peer GPU's receive plane over NVLink, same layout as
+  // out / resid -- and the epilogue threads end with fence.sys
+  float* out2;
 };
 
 // Split count for a decode GEMM: minimises waves x K-blocks per CTA (+ a per-split reduction cost).
@@ -162,20 +166,33 @@ cudaError_t attn_decode_launch(const DecodeAttnArgs& a, int head_dim, cudaStream
 
 // ------------------------------------------------------------------ TP=2 fused all-reduce (N2)
 struct TpAllreduceArgs {
-  const float* part;       // this rank's partials [splits][plane] (row stride ldp)
-  int splits;
-  int64_t plane, ldp;
-  float* x;                // residual [rows][H] f32, updated in place
+  const float* recv0;      // rank 0's projection output [rows][H] f32 (this GPU's receive plane)
+  const float* recv1;      // rank 1's
+  float* x;                // residual [rows][H] f32, updated in place: x = (x + recv0) + recv1
   const bf16* gamma;       // next RMSNorm weight, or null (x only)
   bf16* h;                 // rmsnorm(x) * gamma [rows][H]
   float eps;
-  int rows, rows_max, H, rank, epoch;
-  float* peer_recv;        // the peer's receive rows [2][rows_max][H] (P2P)
-  int* peer_flags;         // the peer's flags [2][rows_max] (P2P)
+  int rows, H, epoch;
+  int* peer_flag;          // the peer's flag (P2P): set to epoch once this rank's pushes are done
+  const int* my_flag;      // set by the peer
+};
+cudaError_t tp_allreduce_norm_launch(const TpAllreduceArgs& a, int num_sms, cudaStream_t s);
+// decode variant: sums this rank's split partials per row and pushes the row itself
+struct TpRowsArgs {
+  const float* part;       // this rank's partials [splits][plane] (row stride ldp)
+  int splits;
+  int64_t plane, ldp;
+  float* x;
+  const bf16* gamma;
+  bf16* h;
+  float eps;
+  int rows, H, rank, epoch;
+  float* peer_recv;        // the peer's receive rows of this epoch's parity [rows][H] (P2P)
+  int* peer_flags;         // the peer's row flags of this parity [rows] (P2P)
   const float* my_recv;    // this rank's receive rows, written by the peer
   const int* my_flags;
 };
-cudaError_t tp_allreduce_norm_launch(const TpAllreduceArgs& a, int num_sms, cudaStream_t s);
+cudaError_t tp_push_rows_launch(const TpRowsArgs& a, int num_sms, cudaStream_t s);
 
 // ------------------------------------------------------------------ small kernels
 cudaError_t embed_launch(const int* ids, const bf16* E, float* x, int n, int H, cudaStream_t s);

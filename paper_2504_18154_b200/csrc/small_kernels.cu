@@ -201,13 +201,18 @@ cudaError_t splitk_resid_rmsnorm_launch(const float* part, int splits, int rows,
 }
 
 // TP=2 all-reduce fused with the residual add and the next RMSNorm, over NVLink peer
-// memory. One CTA per token row (grid-stride):
-//   acc_r = sum of this rank's split partials (split order)
-//   push acc_r into the peer's receive row (P2P stores), fence.sys, flag := epoch
-//   wait for the peer's flag, x = (x + acc_0) + acc_1 (rank order -> bitwise identical
-//   on both ranks, the same sum the NCCL path forms), h = rmsnorm(x) * gamma.
-// Receive rows and flags are double-buffered by epoch parity: a rank can run at most
-// one call ahead of its peer (it waits for the peer's flag of every call).
+// memory. The exchange itself rides in the
+// epilogue of the O / down projection: every output tile of rank r is stored both into
+// this rank's receive plane recv[par][r] and, over NVLink, into the peer's recv[par][r]
+// (GemmEpi::out2), tile by tile while the GEMM still runs. This kernel then
+//   1. signals the peer that this rank's GEMM is complete (every CTA: fence.sys,
+//      st.release.sys flag := epoch -- the GEMM grid finished before pdl_wait returns),
+//   2. waits until the peer's flag reaches the epoch (its pushes are in our HBM),
+//   3. x = (x + acc_0) + acc_1 (rank order -> bitwise identical on both ranks, the same
+//      sum the NCCL path forms), h = rmsnorm(x) * gamma.
+// Receive planes are double-buffered by epoch parity; a rank is at most one exchange
+// ahead of its peer (it waits for the peer's flag of every exchange), and epochs only
+// grow, so the wait is `flag >= epoch`.
 __device__ __forceinline__ void st_release_sys(int* p, int v) {
   asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -221,11 +226,82 @@ __global__ void __launch_bounds__(1024) tp_allreduce_norm_kernel(TpAllreduceArgs
   pdl_trigger();
   pdl_wait();
   const int H = a.H;
-  const int par = a.epoch & 1;
-  float* peer_recv = a.peer_recv + (int64_t)par * a.rows_max * H;
-  int* peer_flags = a.peer_flags + par * a.rows_max;
-  const float* my_recv = a.my_recv + (int64_t)par * a.rows_max * H;
-  const int* my_flags = a.my_flags + par * a.rows_max;
+  __shared__ float red[32];
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(a.peer_flag, a.epoch);
+    while (ld_acquire_sys(a.my_flag) < a.epoch) {
+    }
+  }
+  __syncthreads();
+  for (int row = blockIdx.x; row < a.rows; row += gridDim.x) {
+    float4 v[4];
+    float ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = (threadIdx.x + j * blockDim.x) * 4;
+      if (c < H) {
+        const int64_t off = (int64_t)row * H + c;
+        const float4 a0 = __ldcg(reinterpret_cast<const float4*>(a.recv0 + off));
+        const float4 a1 = __ldcg(reinterpret_cast<const float4*>(a.recv1 + off));
+        float4 xv = *reinterpret_cast<const float4*>(a.x + off);
+        xv.x = (xv.x + a0.x) + a1.x;
+        xv.y = (xv.y + a0.y) + a1.y;
+        xv.z = (xv.z + a0.z) + a1.z;
+        xv.w = (xv.w + a0.w) + a1.w;
+        *reinterpret_cast<float4*>(a.x + off) = xv;
+        ss += xv.x * xv.x + xv.y * xv.y + xv.z * xv.z + xv.w * xv.w;
+        v[j] = xv;
+      }
+    }
+    if (!a.gamma) continue;  // block-uniform
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float t = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (threadIdx.x == 0) red[0] = t;
+    }
+    __syncthreads();
+    const float inv = rsqrtf(red[0] / H + a.eps);
+    __syncthreads();  // red[] reused by the next row
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = (threadIdx.x + j * blockDim.x) * 4;
+      if (c < H) {
+        const uint2 gv = *reinterpret_cast<const uint2*>(a.gamma + c);
+        uint2 o;
+        o.x = pack_bf16x2(v[j].x * inv * bf16_lo(gv.x), v[j].y * inv * bf16_hi(gv.x));
+        o.y = pack_bf16x2(v[j].z * inv * bf16_lo(gv.y), v[j].w * inv * bf16_hi(gv.y));
+        *reinterpret_cast<uint2*>(a.h + (int64_t)row * H + c) = o;
+      }
+    }
+  }
+}
+
+cudaError_t tp_allreduce_norm_launch(const TpAllreduceArgs& a, int num_sms, cudaStream_t s) {
+  if (a.rows == 0) return cudaSuccess;
+  const int threads = a.H >= 4096 ? 1024 : (a.H >= 1024 ? 256 : 64);
+  if (a.H % 4 || a.H > threads * 16) return cudaErrorInvalidValue;
+  // every CTA spins on the peer's flag: keep the grid co-resident (rows are grid-strided)
+  const int per_sm = threads >= 1024 ? 1 : 2;
+  const int grid = a.rows < per_sm * num_sms ? a.rows : per_sm * num_sms;
+  return launch_k(tp_allreduce_norm_kernel, dim3(grid), dim3(threads), 0, s, a);
+}
+
+// Decode variant (B rows): the projection's split-K partials stay in this GPU's L2 and
+// one CTA per token row sums them (split order), pushes the row to the peer's receive
+// row (P2P stores), fence.sys + a per-row flag := epoch, waits for the peer's row and
+// forms x = (x + acc_0) + acc_1 and the next RMSNorm. At decode sizes (a 32 KB row per
+// CTA) this beats pushing from the GEMM epilogue, which measured 30.3 vs 24.4 ms per
+// 70B TP=2 step: the in-GEMM split reduction and 128-byte remote stores sit on the tail.
+__global__ void __launch_bounds__(1024) tp_push_rows_kernel(TpRowsArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  const int H = a.H;
   __shared__ float red[32];
   for (int row = blockIdx.x; row < a.rows; row += gridDim.x) {
     float4 v[4];
@@ -240,14 +316,14 @@ __global__ void __launch_bounds__(1024) tp_allreduce_norm_kernel(TpAllreduceArgs
           acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
         }
         v[j] = acc;
-        *reinterpret_cast<float4*>(peer_recv + (int64_t)row * H + c) = acc;
+        *reinterpret_cast<float4*>(a.peer_recv + (int64_t)row * H + c) = acc;
       }
     }
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {
-      st_release_sys(peer_flags + row, a.epoch);
-      while (ld_acquire_sys(my_flags + row) != a.epoch) {
+      st_release_sys(a.peer_flags + row, a.epoch);
+      while (ld_acquire_sys(a.my_flags + row) != a.epoch) {
       }
     }
     __syncthreads();
@@ -257,7 +333,7 @@ __global__ void __launch_bounds__(1024) tp_allreduce_norm_kernel(TpAllreduceArgs
     for (int j = 0; j < 4; ++j) {
       const int c = (threadIdx.x + j * blockDim.x) * 4;
       if (c < H) {
-        const float4 o = __ldcv(reinterpret_cast<const float4*>(my_recv + (int64_t)row * H + c));
+        const float4 o = __ldcv(reinterpret_cast<const float4*>(a.my_recv + (int64_t)row * H + c));
         const float4 a0 = a.rank == 0 ? v[j] : o, a1 = a.rank == 0 ? o : v[j];
         float4 xv = *reinterpret_cast<const float4*>(a.x + (int64_t)row * H + c);
         xv.x = (xv.x + a0.x) + a1.x;
@@ -298,14 +374,14 @@ __global__ void __launch_bounds__(1024) tp_allreduce_norm_kernel(TpAllreduceArgs
   }
 }
 
-cudaError_t tp_allreduce_norm_launch(const TpAllreduceArgs& a, int num_sms, cudaStream_t s) {
+cudaError_t tp_push_rows_launch(const TpRowsArgs& a, int num_sms, cudaStream_t s) {
   if (a.rows == 0) return cudaSuccess;
   const int threads = a.H >= 4096 ? 1024 : (a.H >= 1024 ? 256 : 64);
-  if (a.H % 4 || a.H > threads * 16 || a.rows > a.rows_max) return cudaErrorInvalidValue;
+  if (a.H % 4 || a.H > threads * 16) return cudaErrorInvalidValue;
   // every CTA co-resident (rows are grid-strided): the two ranks wait on each other row by row
   const int per_sm = threads >= 1024 ? 1 : 2;
   const int grid = a.rows < per_sm * num_sms ? a.rows : per_sm * num_sms;
-  return launch_k(tp_allreduce_norm_kernel, dim3(grid), dim3(threads), 0, s, a);
+  return launch_k(tp_push_rows_kernel, dim3(grid), dim3(threads), 0, s, a);
 }
 
 __device__ __forceinline__ float silu_r(float z) { return __fdividef(z, 1.f + __expf(-z)); }
