@@ -184,6 +184,17 @@ struct ecoserve_instance {
   std::unordered_map<int64_t, std::pair<int, int>> dbg_rows;  // req -> (row0, nrows) of the last phase call
   std::unordered_map<int64_t, Req> reqs;
   Prof prof;
+  // decode layer chain (TP=1): per layer the post-attention steps in device memory
+  bool chain = false;
+  ChainStep* d_chain = nullptr;
+  std::vector<int> chain_off, chain_n;
+  CUtensorMap* d_amaps = nullptr;            // [3]: h, ao, act as 128-row B operands
+  unsigned long long* chain_bar = nullptr;   // grid-barrier counter
+  unsigned long long chain_base = 0;
+  int* chain_err = nullptr;
+  int* h_chain_err = nullptr;                // pinned copy, read after every decode step
+  unsigned long long* chain_trace = nullptr;  // ECOSERVE_CHAIN_TRACE=path (debug)
+  double chain_bytes_layer = 0;              // weight bytes streamed per chain launch (O + GU + down + QKV)
 
   bool fail(const char* what, cudaError_t e) {
     err = std::string(what) + ": " + cudaGetErrorString(e);
@@ -322,6 +333,8 @@ ecoserve_status tp_setup_peer(ecoserve_instance* inst) {
 }
 }  // namespace
 
+static ecoserve_status build_chain(ecoserve_instance* inst);
+
 extern "C" {
 
 int64_t ecoserve_kv_pool_bytes(const ecoserve_model_shape* s, int32_t block_tokens, int64_t num_blocks) {
@@ -367,12 +380,14 @@ void ecoserve_instance_destroy(ecoserve_instance* inst) {
     if (p) cudaFree(p);
   if (inst->h_meta) cudaFreeHost(inst->h_meta);
   if (inst->h_tokens) cudaFreeHost(inst->h_tokens);
+  if (inst->h_chain_err) cudaFreeHost(inst->h_chain_err);
   for (cudaEvent_t e : inst->prof.pool) cudaEventDestroy(e);
   if (inst->peer_ipc) {
     if (inst->peer_recv) cudaIpcCloseMemHandle(inst->peer_recv);
     if (inst->peer_flags) cudaIpcCloseMemHandle(inst->peer_flags);
   }
-  for (void* p : {(void*)inst->tp_recv, (void*)inst->tp_flags, (void*)inst->d_wmaps})
+  for (void* p : {(void*)inst->tp_recv, (void*)inst->tp_flags, (void*)inst->d_wmaps, (void*)inst->d_chain,
+                  (void*)inst->d_amaps, (void*)inst->chain_bar, (void*)inst->chain_err, (void*)inst->chain_trace})
     if (p) cudaFree(p);
   if (inst->comm) ncclCommDestroy(inst->comm);
   if (inst->own_stream && inst->stream) cudaStreamDestroy(inst->stream);
@@ -579,6 +594,10 @@ ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, cons
       if (es != ECOSERVE_OK) return es;
     }
   }
+  if (inst->tp == 1) {
+    const ecoserve_status es = build_chain(inst);
+    if (es != ECOSERVE_OK) return es;
+  }
   *out = holder.release();
   return ECOSERVE_OK;
 }
@@ -625,6 +644,110 @@ int resid_mode_decode(const ecoserve_instance* inst) { return inst->tp_rank == 0
 
 bf16* k_layer(ecoserve_instance* inst, int l) { return inst->pool + (int64_t)l * 2 * inst->Mkv * BLOCK * inst->D; }
 bf16* v_layer(ecoserve_instance* inst, int l) { return k_layer(inst, l) + (int64_t)inst->Mkv * BLOCK * inst->D; }
+
+bool chain_enabled() {  // ECOSERVE_CHAIN=1: the decode layer chain (work in progress: off by default)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_CHAIN");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+}  // namespace
+
+// The decode layer chain (kernels.h ChainStep) of every layer, built once: after the
+// attention of layer l, one persistent kernel runs
+//   O GEMM -> x += O, h = rmsnorm(x) * ffn_norm -> gate/up GEMM (+SiLU) -> down GEMM
+//   -> x += down, h = rmsnorm(x) * attn_norm(l+1) (last layer: final norm -> hl)
+//   -> QKV GEMM of layer l+1 -> RoPE, q, paged K / V write
+// The splits and the reduction order are those of the per-kernel path.
+static ecoserve_status build_chain(ecoserve_instance* inst) {
+  const int L = inst->L, H = inst->H, M = inst->M, D = inst->D, F = inst->F, QKV = inst->QKV;
+  inst->chain = false;
+  if (!chain_enabled() || H % 16 || H > 8192 || (2 * F) % 16 || QKV % 16 || (M * D) % 16 || F % 8) return ECOSERVE_OK;
+  {
+    CUtensorMap am[3] = {inst->m_h.b[1], inst->m_ao.b[1], inst->m_act.b[1]};
+    CK(cudaMalloc(&inst->d_amaps, sizeof(am)));
+    CK(cudaMemcpy(inst->d_amaps, am, sizeof(am), cudaMemcpyHostToDevice));
+  }
+  const int ns = inst->num_sms;
+  const int so = gemm_decode_splits(H, M * D, ns), sg = gemm_decode_splits(2 * F, H, ns),
+            sd = gemm_decode_splits(H, F, ns), sq = gemm_decode_splits(QKV, H, ns);
+  std::vector<ChainStep> steps;
+  auto gemm = [&](int map_idx, int amap, int m_rows, int K, int splits, int mode, void* out, int64_t ldo) {
+    ChainStep c;
+    memset(&c, 0, sizeof(c));
+    c.kind = CS_GEMM;
+    c.wmap = inst->d_wmaps + map_idx;
+    c.xmap = inst->d_amaps + amap;
+    c.m_rows = m_rows;
+    c.K = K;
+    c.splits = splits;
+    c.mode = mode;
+    c.out = out;
+    c.ldo = ldo;
+    steps.push_back(c);
+  };
+  auto reduce = [&](int red, int splits, int cols, const bf16* gamma, bf16* h, const GemmEpi* e) {
+    ChainStep c;
+    memset(&c, 0, sizeof(c));
+    c.kind = CS_REDUCE;
+    c.red = red;
+    c.part = inst->part;
+    c.rsplits = splits;
+    c.cols = cols;
+    c.x = inst->x;
+    c.gamma = gamma;
+    c.h = h;
+    c.eps = inst->shape.rms_eps;
+    if (e) c.e = *e;
+    steps.push_back(c);
+  };
+  inst->chain_off.assign(L, 0);
+  inst->chain_n.assign(L, 0);
+  for (int l = 0; l < L; ++l) {
+    const LayerW& w = inst->lw[l];
+    inst->chain_off[l] = (int)steps.size();
+    gemm(4 * l + 1, 1, H, M * D, so, EPI_SWAP_F32, inst->part, H);
+    reduce(CR_RESID_NORM, so, H, w.ffn_norm, inst->h, nullptr);
+    if (sg == 1) {
+      gemm(4 * l + 2, 0, 2 * F, H, 1, EPI_SWAP_SILU, inst->act, F);
+    } else {
+      gemm(4 * l + 2, 0, 2 * F, H, sg, EPI_SWAP_F32, inst->part, 2 * F);
+      GemmEpi e = epi_base(inst);
+      e.out = inst->act;
+      e.ldo = F;
+      reduce(CR_SILU, sg, 2 * F, nullptr, nullptr, &e);
+    }
+    gemm(4 * l + 3, 2, H, F, sd, EPI_SWAP_F32, inst->part, H);
+    const bool last = l + 1 == L;
+    reduce(CR_RESID_NORM, sd, H, last ? inst->final_norm : inst->lw[l + 1].attn_norm, last ? inst->hl : inst->h,
+           nullptr);
+    if (!last) {
+      gemm(4 * (l + 1), 0, QKV, H, sq, EPI_SWAP_F32, inst->part, QKV);
+      GemmEpi e = epi_base(inst);
+      e.k_cache = k_layer(inst, l + 1);
+      e.v_cache = v_layer(inst, l + 1);
+      reduce(CR_QKV, sq, QKV, nullptr, nullptr, &e);
+    }
+    inst->chain_n[l] = (int)steps.size() - inst->chain_off[l];
+  }
+  CK(cudaMalloc(&inst->d_chain, sizeof(ChainStep) * steps.size()));
+  CK(cudaMemcpy(inst->d_chain, steps.data(), sizeof(ChainStep) * steps.size(), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&inst->chain_bar, sizeof(unsigned long long)));
+  CK(cudaMemset(inst->chain_bar, 0, sizeof(unsigned long long)));
+  CK(cudaMalloc(&inst->chain_err, sizeof(int)));
+  CK(cudaMemset(inst->chain_err, 0, sizeof(int)));
+  CK(cudaMallocHost(&inst->h_chain_err, sizeof(int)));
+  *inst->h_chain_err = 0;
+  inst->chain_base = 0;
+  inst->chain_bytes_layer = 2.0 * ((double)H * M * D + 2.0 * F * H + (double)H * F + (double)QKV * H);
+  inst->chain = true;
+  return ECOSERVE_OK;
+}
+
+namespace {
 
 // Prefill projection: CTA-pair 256 x 256 tiles (cta_group::2) unless ECOSERVE_GEMM2=0,
 // then the 1-CTA 128 x 256 kernel. w128 / w256: the weight's tensor maps with 128 / 256-row boxes.
@@ -985,6 +1108,86 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
   if ((int64_t)B * M * n_splits * (D + 2) > inst->attn_ws_elems) return ECOSERVE_ERR_INVALID_ARG;
   // RMSNorms fused into the split-K reduction of the preceding O / down projection (TP=1)
   const bool can_fuse = inst->tp == 1;
+  if (inst->chain) {
+    // layer 0's attention input: norm + QKV (+ RoPE, KV write) as separate kernels, then per
+    // layer the attention and one chain kernel (O ... next layer's QKV, see build_chain)
+    LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, inst->lw[0].attn_norm, inst->h, B, H, eps, st));
+    {
+      GemmEpi e = epi_base(inst);
+      e.pos = d_pos;
+      e.slot = d_slot;
+      e.k_cache = k_layer(inst, 0);
+      e.v_cache = v_layer(inst, 0);
+      int nk = 0;
+      LAUNCH(P_GEMM_DECODE, 2.0 * inst->QKV * H, nk,
+             decode_gemm(inst, inst->lw[0].qkv_a, inst->m_h, inst->QKV, H, B, EPI_SWAP_QKV, e, &nk));
+    }
+    ChainCall cc;
+    cc.n_tok = B;
+    cc.pos = d_pos;
+    cc.slot = d_slot;
+    cc.bar = inst->chain_bar;
+    cc.err = inst->chain_err;
+    cc.trace = nullptr;
+    static const char* trace_path = getenv("ECOSERVE_CHAIN_TRACE");  // debug: marks of layer 1's chain
+    if (trace_path && !inst->chain_trace)
+      CK(cudaMalloc(&inst->chain_trace, sizeof(unsigned long long) * inst->num_sms * 32 * 4));
+    for (int l = 0; l < L; ++l) {
+      DecodeAttnArgs a;
+      a.q = inst->q;
+      a.k_cache = k_layer(inst, l);
+      a.v_cache = v_layer(inst, l);
+      a.blk_stride = inst->blk_stride;
+      a.ctx_lens = d_ctx;
+      a.block_tables = d_bt;
+      a.bt_ld = bt_ld;
+      a.B = B;
+      a.n_heads = M;
+      a.n_kv = inst->Mkv;
+      a.n_splits = n_splits;
+      a.blocks_per_split = bps;
+      a.part_o = inst->attn_ws;
+      a.part_ml = inst->attn_ws + (int64_t)B * M * n_splits * D;
+      a.out = inst->ao;
+      a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
+      a.order = d_order;
+      a.kvmap = inst->attn_tc ? &inst->attn_kvmap : nullptr;
+      a.layer = l;
+      a.n_layers = L;
+      LAUNCH(P_ATTN_DECODE, kv_bytes, n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
+      cc.bar_base = inst->chain_base;
+      cc.trace = (trace_path && l == std::min(1, L - 1)) ? inst->chain_trace : nullptr;
+      const int n = inst->chain_n[l];
+      const double bytes = inst->chain_bytes_layer - (l + 1 == L ? 2.0 * inst->QKV * H : 0.0);
+      LAUNCH(P_GEMM_DECODE, bytes, 1,
+             decode_chain_launch(inst->d_chain + inst->chain_off[l], n, cc, inst->num_sms, st));
+      inst->chain_base += (unsigned long long)n * inst->num_sms;
+      if (inst->debug)
+        CK(cudaMemcpyAsync(inst->dbg + (int64_t)(l + 1) * inst->T_max * H, inst->x, sizeof(float) * (int64_t)B * H,
+                           cudaMemcpyDeviceToDevice, st));
+    }
+    *final_normed = true;
+    if (trace_path) {  // append "cta step k t_ns" lines (relative to the earliest mark)
+      std::vector<unsigned long long> t((size_t)inst->num_sms * 32 * 4);
+      CK(cudaMemcpyAsync(t.data(), inst->chain_trace, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      unsigned long long t0 = ~0ull;
+      for (int c = 0; c < inst->num_sms; ++c) t0 = std::min(t0, t[(size_t)(c * 32) * 4 + 3]);
+      FILE* f = fopen(trace_path, "a");
+      if (f) {
+        fprintf(f, "# B=%d steps=%d\n", B, inst->chain_n[std::min(1, L - 1)]);
+        for (int c = 0; c < inst->num_sms; ++c)
+          for (int si = 0; si < inst->chain_n[std::min(1, L - 1)]; ++si)
+            for (int k = 0; k < 4; ++k) {
+              const unsigned long long v = t[((size_t)c * 32 + si) * 4 + k];
+              if (v >= t0 && v - t0 < 1000000000ull) fprintf(f, "%d %d %d %llu\n", c, si, k, v - t0);
+            }
+        fclose(f);
+      }
+      CK(cudaMemsetAsync(inst->chain_trace, 0, sizeof(unsigned long long) * t.size(), st));
+    }
+    return ECOSERVE_OK;
+  }
   bool h_ready = false, fused = false;
   *final_normed = false;
   for (int l = 0; l < L; ++l) {
@@ -1529,8 +1732,15 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
     if (es != ECOSERVE_OK) return es;
     inst->prof.end(pm, B, st);
     CK(cudaMemcpyAsync(inst->h_tokens, inst->d_tokens, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+    if (inst->chain) CK(cudaMemcpyAsync(inst->h_chain_err, inst->chain_err, sizeof(int), cudaMemcpyDeviceToHost, st));
     const auto t_enq1 = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(st));
+    if (inst->chain && *inst->h_chain_err) {
+      inst->err = "decode chain: grid barrier timed out (CTAs not co-resident; set ECOSERVE_CHAIN=0 when several "
+                  "instances share a GPU)";
+      inst->dead = true;
+      return ECOSERVE_ERR_CUDA;
+    }
     if (host_timing_enabled()) {
       const auto t_sync = std::chrono::steady_clock::now();
       fprintf(stderr, "[ecoserve] decode step B=%d: host enqueue %.1f us, enqueue+gpu %.1f us\n", B,

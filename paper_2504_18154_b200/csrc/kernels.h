@@ -101,6 +101,50 @@ cudaError_t gemm_cluster_launch(const CUtensorMap* mapA, const CUtensorMap* mapB
                                 int bn, int splits, const GemmEpi& epi, cudaStream_t stream);
 // How many clusters of `splits` CTAs of that kernel can be resident at once (0 if unsupported).
 int gemm_cluster_max_active(int bn, int splits);
+
+// ------------------------------------------------------------------ decode layer chain
+// One persistent kernel (one CTA per SM) runs the post-attention part of a decode layer
+// as a sequence of steps -- O GEMM, residual + RMSNorm, gate/up GEMM (+SiLU), down GEMM,
+// residual + next RMSNorm, next layer's QKV GEMM, RoPE + KV write -- with a grid-wide
+// barrier between dependent steps instead of a kernel boundary. The TMA producer keeps
+// streaming the next GEMM's weights into free smem stages while the barrier is pending;
+// only the activation loads wait for it.
+enum ChainStepKind : int { CS_GEMM = 0, CS_REDUCE = 1 };
+enum ChainRedMode : int { CR_RESID_NORM = 0, CR_QKV = 1, CR_SILU = 2 };
+struct ChainStep {
+  int kind;
+  // CS_GEMM (swap-AB, BN 128): D[m][tok] = W[m] . X[tok]; mode EPI_SWAP_F32 (partials
+  // [splits][n_tok][ldo]) or EPI_SWAP_SILU (splits 1: out bf16 [n_tok][ldo] at m/2)
+  const CUtensorMap* wmap;  // weights, 128-row box (device memory)
+  const CUtensorMap* xmap;  // activations, 128-row box (device memory)
+  int m_rows, K, splits, mode;
+  void* out;
+  int64_t ldo;
+  // CS_REDUCE: sum of `rsplits` partial planes [rsplits][n_tok][cols] (split order), then
+  //   CR_RESID_NORM: x += sum; h = bf16(rmsnorm(x) * gamma)          (cols = H)
+  //   CR_QKV:        RoPE on q/k pairs -> e.q_out / paged K, V -> pool (e: QKV epilogue)
+  //   CR_SILU:       e.out[tok][c/2] = silu(sum[c]) * sum[c + 1]
+  int red;
+  const float* part;
+  int rsplits, cols;
+  float* x;
+  const bf16* gamma;
+  bf16* h;
+  float eps;
+  GemmEpi e;  // CR_QKV / CR_SILU parameters; pos / slot come from the call
+};
+struct ChainCall {
+  int n_tok;
+  const int* pos;                 // [n_tok] (CR_QKV)
+  const int* slot;                // [n_tok] (CR_QKV)
+  unsigned long long* bar;        // grid-barrier counter, monotonic across launches
+  unsigned long long bar_base;    // its value when this launch starts
+  int* err;                       // set to 1 if a grid barrier timed out (CTAs not co-resident)
+  unsigned long long* trace;      // optional %globaltimer marks [grid][32 steps][4] (null: off)
+};
+// grid = num_sms CTAs; the counter advances by n_steps * grid per launch
+cudaError_t decode_chain_launch(const ChainStep* d_steps, int n_steps, const ChainCall& c, int num_sms,
+                                cudaStream_t stream);
 // CTA-pair (cta_group::2) 256 x 256-tile variant for the non-swapped (prefill) epilogues.
 // mapA box 128 rows (A), mapB box 128 rows (half of the 256 B rows of a tile).
 cudaError_t gemm2_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K,

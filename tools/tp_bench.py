@@ -62,6 +62,18 @@ def worker(rank, nid, args, q):
             if rep > 0:
                 for k in ("prefill_ms", "decode_ms"):
                     out[k] = min(out.get(k, 1e30), t[k])
+        if args.ncu:  # one decode step inside a profiler range (ncu --profile-from-start off)
+            base = 100000 * (args.reps + 3)
+            for i in range(0, args.batch, 16):
+                inst.prefill([(base + j, rng.integers(0, shape.vocab, args.prompt).astype(np.int32), 512)
+                              for j in ids[i:i + 16]])
+            inst.decode([base + j for j in ids], 1)
+            torch.cuda.synchronize()
+            torch.cuda.cudart().cudaProfilerStart()
+            inst.decode([base + j for j in ids], 1)
+            torch.cuda.synchronize()
+            torch.cuda.cudart().cudaProfilerStop()
+            inst.release([base + j for j in ids])
         if args.profile:  # one more rep with per-kernel-class events (breaks PDL overlap: shares only)
             inst.set_profiling(2)
             base = 100000 * (args.reps + 2)
@@ -88,6 +100,7 @@ def main():
     ap.add_argument("--steps", type=int, default=16)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--profile", action="store_true", help="add a per-kernel-class pass (rank 0's classes)")
+    ap.add_argument("--ncu", action="store_true", help="profiler range around one decode step")
     ap.add_argument("--tp1", action="store_true", help="one rank's shard as a TP=1 instance on one GPU")
     args = ap.parse_args()
     from paper_2504_18154_b200 import build as B
