@@ -194,6 +194,10 @@ struct ecoserve_instance {
   int* chain_err = nullptr;
   int* h_chain_err = nullptr;                // pinned copy, read after every decode step
   unsigned long long* chain_trace = nullptr;  // ECOSERVE_CHAIN_TRACE=path (debug)
+  float* chain_ssp = nullptr;                // [H/128][chain_ss_ld] per-tile sums of squares
+  int chain_ss_ld = 0;
+  float* chain_ws = nullptr;                 // split-tile sums [1024 tiles][128][128] (zeroed)
+  int* chain_cnt = nullptr;                  // [4][1024] tile arrival counters
   double chain_bytes_layer = 0;              // weight bytes streamed per chain launch (O + GU + down + QKV)
 
   bool fail(const char* what, cudaError_t e) {
@@ -387,7 +391,8 @@ void ecoserve_instance_destroy(ecoserve_instance* inst) {
     if (inst->peer_flags) cudaIpcCloseMemHandle(inst->peer_flags);
   }
   for (void* p : {(void*)inst->tp_recv, (void*)inst->tp_flags, (void*)inst->d_wmaps, (void*)inst->d_chain,
-                  (void*)inst->d_amaps, (void*)inst->chain_bar, (void*)inst->chain_err, (void*)inst->chain_trace})
+                  (void*)inst->d_amaps, (void*)inst->chain_bar, (void*)inst->chain_err, (void*)inst->chain_trace,
+                  (void*)inst->chain_ssp, (void*)inst->chain_ws, (void*)inst->chain_cnt})
     if (p) cudaFree(p);
   if (inst->comm) ncclCommDestroy(inst->comm);
   if (inst->own_stream && inst->stream) cudaStreamDestroy(inst->stream);
@@ -657,79 +662,82 @@ bool chain_enabled() {  // ECOSERVE_CHAIN=1: the decode layer chain (work in pro
 }  // namespace
 
 // The decode layer chain (kernels.h ChainStep) of every layer, built once: after the
-// attention of layer l, one persistent kernel runs
-//   O GEMM -> x += O, h = rmsnorm(x) * ffn_norm -> gate/up GEMM (+SiLU) -> down GEMM
-//   -> x += down, h = rmsnorm(x) * attn_norm(l+1) (last layer: final norm -> hl)
-//   -> QKV GEMM of layer l+1 -> RoPE, q, paged K / V write
-// The splits and the reduction order are those of the per-kernel path.
+// attention of layer l, one persistent kernel runs the GEMMs
+//   O (x += o Wo^T; hb = bf16(x * ffn_norm); sum of squares per token and 128-feature tile)
+//   gate/up (x the RMSNorm scale r per token; SiLU * up)
+//   down (x += ...; hb = bf16(x * attn_norm(l+1)) -- the last layer: final_norm into hl)
+//   QKV of layer l+1 (x r; RoPE, q, paged K / V)
+// The RMSNorm is split around the GEMM: gamma is applied to the GEMM input, 1/rms to its
+// output (sum_k bf16(x_k gamma_k) W_jk * r instead of sum_k bf16(x_k r gamma_k) W_jk,
+// the same bf16 rounding per element). The LM head reads bf16(x * final_norm): argmax
+// is invariant to the positive per-token scale r.
 static ecoserve_status build_chain(ecoserve_instance* inst) {
   const int L = inst->L, H = inst->H, M = inst->M, D = inst->D, F = inst->F, QKV = inst->QKV;
   inst->chain = false;
-  if (!chain_enabled() || H % 16 || H > 8192 || (2 * F) % 16 || QKV % 16 || (M * D) % 16 || F % 8) return ECOSERVE_OK;
+  if (!chain_enabled() || H % 128 || (2 * F) % 128 || QKV % 128 || (M * D) % 64 || F % 64 || inst->B_max > 512)
+    return ECOSERVE_OK;
   {
     CUtensorMap am[3] = {inst->m_h.b[1], inst->m_ao.b[1], inst->m_act.b[1]};
     CK(cudaMalloc(&inst->d_amaps, sizeof(am)));
     CK(cudaMemcpy(inst->d_amaps, am, sizeof(am), cudaMemcpyHostToDevice));
   }
-  const int ns = inst->num_sms;
-  const int so = gemm_decode_splits(H, M * D, ns), sg = gemm_decode_splits(2 * F, H, ns),
-            sd = gemm_decode_splits(H, F, ns), sq = gemm_decode_splits(QKV, H, ns);
+  inst->chain_ss_ld = inst->B_max;
+  CK(cudaMalloc(&inst->chain_ssp, sizeof(float) * (H / 128) * inst->chain_ss_ld));
+  CK(cudaMalloc(&inst->chain_ws, sizeof(float) * 1024LL * 128 * 128));
+  CK(cudaMemset(inst->chain_ws, 0, sizeof(float) * 1024LL * 128 * 128));
+  CK(cudaMalloc(&inst->chain_cnt, sizeof(int) * 4 * 1024));
+  CK(cudaMemset(inst->chain_cnt, 0, sizeof(int) * 4 * 1024));
+  const int max_tiles = ((std::max(std::max(2 * F, QKV), H) + 127) / 128) * ((inst->B_max + 127) / 128);
+  if (max_tiles > 1024) return ECOSERVE_OK;
   std::vector<ChainStep> steps;
-  auto gemm = [&](int map_idx, int amap, int m_rows, int K, int splits, int mode, void* out, int64_t ldo) {
+  auto gemm = [&](int map_idx, int amap, int m_rows, int K, int mode) -> ChainStep& {
     ChainStep c;
     memset(&c, 0, sizeof(c));
-    c.kind = CS_GEMM;
     c.wmap = inst->d_wmaps + map_idx;
     c.xmap = inst->d_amaps + amap;
     c.m_rows = m_rows;
     c.K = K;
-    c.splits = splits;
     c.mode = mode;
-    c.out = out;
-    c.ldo = ldo;
-    steps.push_back(c);
-  };
-  auto reduce = [&](int red, int splits, int cols, const bf16* gamma, bf16* h, const GemmEpi* e) {
-    ChainStep c;
-    memset(&c, 0, sizeof(c));
-    c.kind = CS_REDUCE;
-    c.red = red;
-    c.part = inst->part;
-    c.rsplits = splits;
-    c.cols = cols;
-    c.x = inst->x;
-    c.gamma = gamma;
-    c.h = h;
+    c.H = H;
     c.eps = inst->shape.rms_eps;
-    if (e) c.e = *e;
+    c.ssp_tiles = H / 128;
+    c.counters = inst->chain_cnt + 1024 * (int)(steps.size() % 4);
     steps.push_back(c);
+    return steps.back();
   };
   inst->chain_off.assign(L, 0);
   inst->chain_n.assign(L, 0);
   for (int l = 0; l < L; ++l) {
     const LayerW& w = inst->lw[l];
-    inst->chain_off[l] = (int)steps.size();
-    gemm(4 * l + 1, 1, H, M * D, so, EPI_SWAP_F32, inst->part, H);
-    reduce(CR_RESID_NORM, so, H, w.ffn_norm, inst->h, nullptr);
-    if (sg == 1) {
-      gemm(4 * l + 2, 0, 2 * F, H, 1, EPI_SWAP_SILU, inst->act, F);
-    } else {
-      gemm(4 * l + 2, 0, 2 * F, H, sg, EPI_SWAP_F32, inst->part, 2 * F);
-      GemmEpi e = epi_base(inst);
-      e.out = inst->act;
-      e.ldo = F;
-      reduce(CR_SILU, sg, 2 * F, nullptr, nullptr, &e);
-    }
-    gemm(4 * l + 3, 2, H, F, sd, EPI_SWAP_F32, inst->part, H);
     const bool last = l + 1 == L;
-    reduce(CR_RESID_NORM, sd, H, last ? inst->final_norm : inst->lw[l + 1].attn_norm, last ? inst->hl : inst->h,
-           nullptr);
+    inst->chain_off[l] = (int)steps.size();
+    {
+      ChainStep& c = gemm(4 * l + 1, 1, H, M * D, CE_RESID_SS);
+      c.x = inst->x;
+      c.gamma = w.ffn_norm;
+      c.hb = inst->h;
+      c.ssp_out = inst->chain_ssp;
+    }
+    {
+      ChainStep& c = gemm(4 * l + 2, 0, 2 * F, H, CE_SILU_R);
+      c.ssp_in = inst->chain_ssp;
+      c.e = epi_base(inst);
+      c.e.out = inst->act;
+      c.e.ldo = F;
+    }
+    {
+      ChainStep& c = gemm(4 * l + 3, 2, H, F, CE_RESID_SS);
+      c.x = inst->x;
+      c.gamma = last ? inst->final_norm : inst->lw[l + 1].attn_norm;
+      c.hb = last ? inst->hl : inst->h;
+      c.ssp_out = inst->chain_ssp;
+    }
     if (!last) {
-      gemm(4 * (l + 1), 0, QKV, H, sq, EPI_SWAP_F32, inst->part, QKV);
-      GemmEpi e = epi_base(inst);
-      e.k_cache = k_layer(inst, l + 1);
-      e.v_cache = v_layer(inst, l + 1);
-      reduce(CR_QKV, sq, QKV, nullptr, nullptr, &e);
+      ChainStep& c = gemm(4 * (l + 1), 0, QKV, H, CE_QKV_R);
+      c.ssp_in = inst->chain_ssp;
+      c.e = epi_base(inst);
+      c.e.k_cache = k_layer(inst, l + 1);
+      c.e.v_cache = v_layer(inst, l + 1);
     }
     inst->chain_n[l] = (int)steps.size() - inst->chain_off[l];
   }
@@ -1124,6 +1132,8 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     }
     ChainCall cc;
     cc.n_tok = B;
+    cc.ss_ld = inst->chain_ss_ld;
+    cc.ws = inst->chain_ws;
     cc.pos = d_pos;
     cc.slot = d_slot;
     cc.bar = inst->chain_bar;

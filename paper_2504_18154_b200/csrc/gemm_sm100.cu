@@ -1378,14 +1378,15 @@ cudaError_t gemm_launch(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_
 }
 
 // ---------------------------------------------------------------- decode layer chain
-// (kernels.h: ChainStep). One CTA per SM, the 1-CTA GEMM's warp roles (warp 0 TMA
-// producer, warp 1 MMA issuer, warps 2..5 epilogue) kept across all steps: the smem
-// ring and the two TMEM accumulators carry over from one GEMM step to the next.
-// Dependencies between steps go through a grid barrier (monotonic global counter; the
-// epilogue warps of every CTA arrive after each step). The producer issues the next
-// GEMM's weight loads into free stages first and waits for the barrier only before its
-// activation loads, so HBM keeps streaming weights through barriers and reduction passes.
+// (kernels.h: ChainStep). One CTA per SM with the 1-CTA GEMM's warp roles (warp 0 TMA
+// producer, warp 1 MMA issuer, warps 2..5 epilogue); the smem ring and the two TMEM
+// accumulators carry over from one GEMM step to the next.
 using ChainCfg = GemmCfg<128, 1>;
+constexpr int CH_SILU_STG = 0;                 // [64 tok][128 B] SiLU output staging
+constexpr int CH_RVEC = 64 * 128;              // [512] f32 RMSNorm scales of the step's tokens
+constexpr int CH_RED = CH_RVEC + 512 * 4;      // [4 warps][32] f32 sum-of-squares partials
+constexpr int CH_FLAG = CH_RED + 4 * 32 * 4;   // last-arriver flag
+static_assert(CH_FLAG + 16 <= ChainCfg::STAGING, "chain scratch fits the staging buffer");
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -1412,138 +1413,49 @@ __device__ __noinline__ void chain_grid_wait(const ChainCall& c, unsigned long l
   }
 }
 
-// Reduction passes, executed by the 128 epilogue threads of every CTA. Latency-bound
-// (only the rows / pairs of one CTA per SM): every thread issues all of its loads before
-// it uses any (no stores in between), so one or two L2 round trips cover a row.
-constexpr int CHAIN_NV = 16;  // float4 per thread per row: H <= 128 * 4 * 16 = 8192
+// stream-K partition of T flattened iterations over G CTAs
+__device__ __forceinline__ long long sk_begin(int c, long long T, int G) { return (long long)c * T / G; }
+__device__ __forceinline__ int sk_cta_of(long long i, long long T, int G) { return (int)(((i + 1) * G - 1) / T); }
 
-__device__ __forceinline__ void chain_resid_norm(const ChainStep& S, const ChainCall& c, int ep_tid, float* red) {
-  const int H = S.cols;
-  const int64_t plane = (int64_t)c.n_tok * H;
-  for (int row = blockIdx.x; row < c.n_tok; row += gridDim.x) {
-    float* xr = S.x + (int64_t)row * H;
-    const float* pr = S.part + (int64_t)row * H;
-    float4 v[CHAIN_NV];
+// 32 values per lane -> lane i holds the sum over the warp's lanes of value i (31 shuffles)
+__device__ __forceinline__ float warp_transpose_sum(float (&v)[32], int lane) {
 #pragma unroll
-    for (int j = 0; j < CHAIN_NV; ++j) {
-      const int col = (ep_tid + j * 128) * 4;
-      v[j] = col < H ? __ldcg(reinterpret_cast<const float4*>(xr + col)) : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool hi = lane & off;
+#pragma unroll
+    for (int j = 0; j < off; ++j) {
+      const float send = hi ? v[j] : v[j + off];
+      const float keep = hi ? v[j + off] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
     }
-    for (int sp = 0; sp < S.rsplits; ++sp) {  // fixed split order: x + p0 + p1 + ...
-      float4 p[CHAIN_NV];
-#pragma unroll
-      for (int j = 0; j < CHAIN_NV; ++j) {
-        const int col = (ep_tid + j * 128) * 4;
-        p[j] = col < H ? __ldcg(reinterpret_cast<const float4*>(pr + sp * plane + col)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int j = 0; j < CHAIN_NV; ++j) {
-        v[j].x += p[j].x; v[j].y += p[j].y; v[j].z += p[j].z; v[j].w += p[j].w;
-      }
-    }
-    float ss = 0.f;
-#pragma unroll
-    for (int j = 0; j < CHAIN_NV; ++j) {
-      const int col = (ep_tid + j * 128) * 4;
-      if (col < H) {
-        *reinterpret_cast<float4*>(xr + col) = v[j];
-        ss += v[j].x * v[j].x + v[j].y * v[j].y + v[j].z * v[j].z + v[j].w * v[j].w;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    if ((ep_tid & 31) == 0) red[ep_tid >> 5] = ss;
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    const float inv = rsqrtf(((red[0] + red[1]) + (red[2] + red[3])) / H + S.eps);
-    bf16* hr = S.h + (int64_t)row * H;
-#pragma unroll
-    for (int j = 0; j < CHAIN_NV; ++j) {
-      const int col = (ep_tid + j * 128) * 4;
-      if (col < H) {
-        const uint2 gv = *reinterpret_cast<const uint2*>(S.gamma + col);
-        uint2 o;
-        o.x = pack_bf16x2(v[j].x * inv * bf16_lo(gv.x), v[j].y * inv * bf16_hi(gv.x));
-        o.y = pack_bf16x2(v[j].z * inv * bf16_lo(gv.y), v[j].w * inv * bf16_hi(gv.y));
-        *reinterpret_cast<uint2*>(hr + col) = o;
-      }
-    }
-    asm volatile("bar.sync 1, 128;" ::: "memory");  // red[] reused by the next row
   }
+  return v[0];
 }
 
-// QKV / SiLU pass: 4 column pairs (two float4 per split) per thread and step, 4 steps'
-// loads in flight
-__device__ __forceinline__ void chain_pair_out(const ChainStep& S, const ChainCall& c, int row, int col, float a,
-                                               float b) {
-  const GemmEpi& e = S.e;
-  if (S.red == CR_SILU) {
-    reinterpret_cast<bf16*>(e.out)[(int64_t)row * e.ldo + col / 2] = __float2bfloat16_rn(silu_f(a) * b);
+
+// 32 accumulator columns (tokens c0..c0+31 of the tile) of this thread's TMEM lane, or --
+// for a tile split between CTAs -- of the tile's f32 sum that the CTAs accumulated in
+// `acc_tile` ([128 tok][128 m]); the reader (the last CTA) zeroes it for the next use.
+__device__ __forceinline__ void chain_src(bool from_ws, float* acc_tile, uint32_t tbase, int c0, int row, int n_valid,
+                                          float (&f)[32]) {
+  if (!from_ws) {
+    uint32_t v[32];
+    tmem_ld32(tbase + c0, v);
+    tc_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
     return;
   }
-  // CR_QKV: pair-interleaved q / k rows -> rotate-half RoPE, q -> q_out, k / v -> pool
-  const int D = e.head_dim, half = D / 2;
-  const int qd = e.n_heads * D, kd = e.n_kv * D;
-  const int sl = c.slot[row];
-  if (col < qd + kd) {
-    const bool is_q = col < qd;
-    const int head = is_q ? col / D : (col - qd) / D;
-    const int j = (col % D) / 2;
-    const int p = c.pos[row];
-    const float cs = e.rope_cos[(int64_t)p * half + j], sn = e.rope_sin[(int64_t)p * half + j];
-    bf16* dst = is_q ? e.q_out + ((int64_t)row * e.n_heads + head) * D
-                     : e.k_cache + (int64_t)(sl >> 6) * e.blk_stride + ((int64_t)head * 64 + (sl & 63)) * D;
-    dst[j] = __float2bfloat16_rn(a * cs - b * sn);
-    dst[j + half] = __float2bfloat16_rn(b * cs + a * sn);
-  } else {
-    const int cc = col - qd - kd;
-    const int head = cc / D, d = cc % D;
-    bf16* dst = e.v_cache + (int64_t)(sl >> 6) * e.blk_stride + ((int64_t)head * 64 + (sl & 63)) * D + d;
-    *reinterpret_cast<uint32_t*>(dst) = pack_bf16x2(a, b);
-  }
+  float* src = acc_tile + (int64_t)c0 * 128 + row;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) f[i] = (c0 + i < n_valid) ? __ldcg(src + i * 128) : 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (c0 + i < n_valid) src[i * 128] = 0.f;
 }
 
-__device__ __forceinline__ void chain_pairs(const ChainStep& S, const ChainCall& c, int ep_tid) {
-  const int oct = S.cols / 8;  // 8-column groups per token row (cols % 8 == 0)
-  const int64_t plane = (int64_t)c.n_tok * S.cols;
-  const int64_t total = (int64_t)c.n_tok * oct;
-  const int64_t stride = (int64_t)gridDim.x * 128;
-  constexpr int U = 4;
-  for (int64_t g0 = (int64_t)blockIdx.x * 128 + ep_tid; g0 < total; g0 += U * stride) {
-    float4 acc[U][2];
-#pragma unroll
-    for (int u = 0; u < U; ++u) acc[u][0] = acc[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int sp = 0; sp < S.rsplits; ++sp) {  // fixed split order
-      float4 p[U][2];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t g = g0 + u * stride;
-        if (g < total) {
-          const float* src = S.part + sp * plane + (g / oct) * S.cols + (g % oct) * 8;
-          p[u][0] = __ldcg(reinterpret_cast<const float4*>(src));
-          p[u][1] = __ldcg(reinterpret_cast<const float4*>(src + 4));
-        } else {
-          p[u][0] = p[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          acc[u][h2].x += p[u][h2].x; acc[u][h2].y += p[u][h2].y;
-          acc[u][h2].z += p[u][h2].z; acc[u][h2].w += p[u][h2].w;
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t g = g0 + u * stride;
-      if (g >= total) continue;
-      const int row = (int)(g / oct), col = (int)(g % oct) * 8;
-      chain_pair_out(S, c, row, col, acc[u][0].x, acc[u][0].y);
-      chain_pair_out(S, c, row, col + 2, acc[u][0].z, acc[u][0].w);
-      chain_pair_out(S, c, row, col + 4, acc[u][1].x, acc[u][1].y);
-      chain_pair_out(S, c, row, col + 6, acc[u][1].z, acc[u][1].w);
-    }
-  }
+__device__ __forceinline__ void red_add_f32(float* p, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -1563,6 +1475,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int n_tok = call.n_tok;
   const int n_tiles = (n_tok + BN - 1) / BN;
   const unsigned long long grid = gridDim.x;
+  const int G = gridDim.x, me = blockIdx.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -1589,53 +1502,39 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       for (int si = 0; si < n_steps; ++si) {
         const ChainStep& S = steps[si];
-        if (S.kind != CS_GEMM) continue;
         const CUtensorMap* wm = S.wmap;
         const CUtensorMap* xm = S.xmap;
-        const int m_rows = S.m_rows, splits = S.splits;
-        const int m_tiles = (m_rows + BM - 1) / BM;
-        const int kb_total = (S.K + BK - 1) / BK;
-        const int kb_per = (kb_total + splits - 1) / splits;
-        const int n_work = m_tiles * n_tiles * splits;
-        int w = blockIdx.x, kb = -1, kb1 = 0, mt = 0, nt = 0;
-        auto next = [&]() -> bool {
-          if (kb >= 0 && kb + 1 < kb1) { ++kb; return true; }
-          if (kb >= 0) w += gridDim.x;
-          if (w >= n_work) return false;
-          const int ks = w % splits, t = w / splits;
-          mt = t / n_tiles;
-          nt = t % n_tiles;
-          kb = ks * kb_per;
-          kb1 = min(kb_total, kb + kb_per);
-          return true;
-        };
+        const int kpt = (S.K + BK - 1) / BK;
+        const long long T = (long long)((S.m_rows + BM - 1) / BM) * n_tiles * kpt;
+        const long long i0 = sk_begin(me, T, G), i1 = sk_begin(me + 1, T, G);
         // 1) weights (independent of the previous steps) into free stages
         int pre_st[C::STAGES], pre_kb[C::STAGES], pre_nt[C::STAGES], npre = 0;
-        bool more = true;
-        while (npre < C::STAGES && (more = next())) {
+        long long i = i0;
+        for (; i < i1 && npre < C::STAGES; ++i) {
+          const int t = (int)(i / kpt), kb = (int)(i % kpt);
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * C::STAGE_BYTES;
           mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
-          tma_load_2d(sa, wm, &full_bar[stage], kb * BK, mt * BM);
-          pre_st[npre] = stage; pre_kb[npre] = kb; pre_nt[npre] = nt;
+          tma_load_2d(smem + stage * C::STAGE_BYTES, wm, &full_bar[stage], kb * BK, (t / n_tiles) * BM);
+          pre_st[npre] = stage; pre_kb[npre] = kb; pre_nt[npre] = t % n_tiles;
           ++npre;
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
         // 2) the activations: produced by the previous step on every CTA
         if (si == 0) pdl_wait();
         else chain_grid_wait(call, call.bar_base + (unsigned long long)si * grid);
-        if (call.trace) call.trace[(blockIdx.x * 32 + si) * 4 + 0] = gtime_ns();
+        if (call.trace) call.trace[(me * 32 + si) * 4 + 0] = gtime_ns();
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        for (int i = 0; i < npre; ++i)
-          tma_load_2d(smem + pre_st[i] * C::STAGE_BYTES + C::A_BYTES, xm, &full_bar[pre_st[i]], pre_kb[i] * BK,
-                      pre_nt[i] * BN);
+        for (int k = 0; k < npre; ++k)
+          tma_load_2d(smem + pre_st[k] * C::STAGE_BYTES + C::A_BYTES, xm, &full_bar[pre_st[k]], pre_kb[k] * BK,
+                      pre_nt[k] * BN);
         // 3) steady state
-        while (more && next()) {
+        for (; i < i1; ++i) {
+          const int t = (int)(i / kpt), kb = (int)(i % kpt);
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
-          tma_load_2d(sa, wm, &full_bar[stage], kb * BK, mt * BM);
-          tma_load_2d(sa + C::A_BYTES, xm, &full_bar[stage], kb * BK, nt * BN);
+          tma_load_2d(sa, wm, &full_bar[stage], kb * BK, (t / n_tiles) * BM);
+          tma_load_2d(sa + C::A_BYTES, xm, &full_bar[stage], kb * BK, (t % n_tiles) * BN);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -1648,126 +1547,224 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0, acc_phase = 0;
       for (int si = 0; si < n_steps; ++si) {
         const ChainStep& S = steps[si];
-        if (S.kind != CS_GEMM) continue;
-        const int splits = S.splits;
-        const int m_tiles = (S.m_rows + BM - 1) / BM;
-        const int kb_total = (S.K + BK - 1) / BK;
-        const int kb_per = (kb_total + splits - 1) / splits;
-        const int n_work = m_tiles * n_tiles * splits;
-        for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-          const int ks = w % splits;
-          const int kb0 = ks * kb_per, kb1 = min(kb_total, kb0 + kb_per);
+        const int kpt = (S.K + BK - 1) / BK;
+        const long long T = (long long)((S.m_rows + BM - 1) / BM) * n_tiles * kpt;
+        const long long i1 = sk_begin(me + 1, T, G);
+        for (long long j = sk_begin(me, T, G); j < i1;) {  // one segment = this CTA's part of one tile
+          const long long seg_end = min(i1, (j / kpt + 1) * kpt);
           mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
-          for (int kb = kb0; kb < kb1; ++kb) {
+          for (long long jj = j; jj < seg_end; ++jj) {
             mbar_wait(&full_bar[stage], phase);
             tc_fence_after();
             const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
             const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + C::A_BYTES);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              tc_mma_f16(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+              tc_mma_f16(d_tmem, da + 2 * k, db + 2 * k, idesc, (jj > j || k > 0) ? 1u : 0u);
             tc_commit(&empty_bar[stage]);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           }
           tc_commit(&tfull_bar[acc]);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          j = seg_end;
         }
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue + reduction passes
-    if (call.trace && threadIdx.x == 64) call.trace[(blockIdx.x * 32 + 0) * 4 + 3] = gtime_ns();  // CTA start
+    // ------------------------------------------------------------ epilogues
+    if (call.trace && threadIdx.x == 64) call.trace[(me * 32 + 0) * 4 + 3] = gtime_ns();  // CTA start
     pdl_wait();
     const int q = warp & 3;
     const int ep_tid = (warp - 2) * 32 + lane;
     const int row = q * 32 + lane;  // accumulator row (TMEM lane)
-    const uint32_t stg_base = smem_u32(staging);
-    float* red = reinterpret_cast<float*>(staging);
+    const uint32_t stg_base = smem_u32(staging + CH_SILU_STG);
+    float* rvec = reinterpret_cast<float*>(staging + CH_RVEC);
+    float* red = reinterpret_cast<float*>(staging + CH_RED);
+    int* s_last = reinterpret_cast<int*>(staging + CH_FLAG);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int si = 0; si < n_steps; ++si) {
       const ChainStep& S = steps[si];
-      if (S.kind == CS_GEMM) {
-        const int m_rows = S.m_rows, splits = S.splits;
-        const int m_tiles = (m_rows + BM - 1) / BM;
-        const int n_work = m_tiles * n_tiles * splits;
-        const bool silu = S.mode == EPI_SWAP_SILU;
-        for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-          const int ks = w % splits, t = w / splits;
-          const int mt = t / n_tiles, nt = t % n_tiles;
-          mbar_wait(&tfull_bar[acc], acc_phase);
-          tc_fence_after();
-          if (call.trace && ep_tid == 0 && w == (int)blockIdx.x) call.trace[(blockIdx.x * 32 + si) * 4 + 1] = gtime_ns();
-          const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::ACC_COLS;
-          // accumulator -> smem transposed to [token][feature] -> 16-byte coalesced rows
-          constexpr int HALF = BN / 2;
-          const int m0 = mt * BM;
-          const int mcount = min(BM, m_rows - m0);
-          const int vec_per_row = silu ? mcount / 16 : mcount / 4;
-          const int stg_row = silu ? BM : BM * 4;
-          char* gbase = silu ? reinterpret_cast<char*>(reinterpret_cast<bf16*>(S.out) + m0 / 2)
-                             : reinterpret_cast<char*>(reinterpret_cast<float*>(S.out) +
-                                                       (int64_t)ks * n_tok * S.ldo + m0);
-          const int64_t gstride = silu ? S.ldo * 2 : S.ldo * 4;
-          for (int hh = 0; hh < 2; ++hh) {
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // staging free
+      const int mode = S.mode;
+      const int m_rows = S.m_rows;
+      const int kpt = (S.K + BK - 1) / BK;
+      const long long T = (long long)((m_rows + BM - 1) / BM) * n_tiles * kpt;
+      // the step's inputs (previous steps of every CTA) are in memory
+      if (si > 0) {
+        if (ep_tid == 0) chain_grid_wait(call, call.bar_base + (unsigned long long)si * grid);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+      if (mode != CE_RESID_SS) {  // the RMSNorm scale of every token of the step
+        for (int n = ep_tid; n < n_tok; n += 128) {
+          float ssum = 0.f;
+          for (int t = 0; t < S.ssp_tiles; ++t) ssum += __ldcg(S.ssp_in + (int64_t)t * call.ss_ld + n);
+          rvec[n] = rsqrtf(ssum / S.H + S.eps);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+      GemmEpi eq;
+      if (mode == CE_QKV_R) {
+        eq = S.e;
+        eq.pos = call.pos;
+        eq.slot = call.slot;
+      }
+      const long long i1 = sk_begin(me + 1, T, G);
+      const int first_tile = (int)(sk_begin(me, T, G) / kpt);
+      for (long long j = sk_begin(me, T, G); j < i1;) {
+        const int t = (int)(j / kpt);
+        const long long seg_end = min(i1, (long long)(t + 1) * kpt);
+        const int mt = t / n_tiles, nt = t % n_tiles;
+        const int n_valid = min(BN, n_tok - nt * BN);  // tokens of this tile
+        bool from_ws = false;
+        float* acc_tile = call.ws + (int64_t)t * 128 * 128;
+        const bool full = j == (long long)t * kpt && seg_end == (long long)(t + 1) * kpt;
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        if (call.trace && ep_tid == 0 && j == sk_begin(me, T, G)) call.trace[(me * 32 + si) * 4 + 1] = gtime_ns();
+        const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::ACC_COLS;
+        bool run_epi = full;
+        if (!full) {
+          // partial tile: this CTA's K range is added (f32 atomics in L2) to the tile's sum --
+          // for the residual modes straight into x -- and the last CTA to arrive finishes it
+          const int m = mt * BM + row;
+          for (int c0 = 0; c0 < n_valid; c0 += 32) {  // warp-uniform
+            uint32_t v[32];
+            tmem_ld32(tbase + c0, v);
+            tc_wait_ld();
+            if (m < m_rows) {
+              if (mode == CE_RESID_SS) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (c0 + i < n_valid) red_add_f32(S.x + (int64_t)(nt * BN + c0 + i) * m_rows + m, __uint_as_float(v[i]));
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (c0 + i < n_valid) red_add_f32(acc_tile + (int64_t)(c0 + i) * 128 + row, __uint_as_float(v[i]));
+              }
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+          const int c_lo = sk_cta_of((long long)t * kpt, T, G), c_hi = sk_cta_of((long long)(t + 1) * kpt - 1, T, G);
+          int nseg = 0;  // CTAs with a non-empty part of the tile
+          for (int c = c_lo; c <= c_hi; ++c) nseg += sk_begin(c + 1, T, G) > sk_begin(c, T, G) ? 1 : 0;
+          __threadfence();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (ep_tid == 0) {
+            const int old = atomicAdd(&S.counters[t], 1);
+            *s_last = old == nseg - 1;
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          run_epi = *s_last != 0;
+          if (run_epi) {
+            __threadfence();
+            from_ws = true;
+            if (ep_tid == 0) S.counters[t] = 0;
+          }
+        }
+        if (run_epi) {
+          const int m = mt * BM + row;
+          const bool mv = m < m_rows;
+          if (mode == CE_SILU_R) {
+            // SiLU(gate) * up with the RMSNorm scale, staged to 16-byte coalesced token rows
+            constexpr int HALF = BN / 2;
+            const int mcount = min(BM, m_rows - mt * BM);
+            const int vec_per_row = mcount / 16;
+            char* gbase = reinterpret_cast<char*>(reinterpret_cast<bf16*>(S.e.out) + mt * BM / 2);
+            const int64_t gstride = S.e.ldo * 2;
+            for (int hh = 0; hh < 2; ++hh) {
+              asm volatile("bar.sync 1, 128;" ::: "memory");  // staging free
 #pragma unroll 1
-            for (int cc = 0; cc < HALF; cc += 32) {
-              uint32_t v[32];
-              tmem_ld32(tbase + hh * HALF + cc, v);
-              tc_wait_ld();
-              if (silu) {
+              for (int cc = 0; cc < HALF; cc += 32) {
+                float f[32];
+                chain_src(from_ws, acc_tile, tbase, hh * HALF + cc, row, n_valid, f);
                 const bool odd = lane & 1;
                 const uint32_t sbase = stg_base + (uint32_t)(row / 2) * 2u;
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) {
-                  const float send = odd ? __uint_as_float(v[i]) : __uint_as_float(v[i + 1]);
+                  const int n = nt * BN + hh * HALF + cc + i;
+                  const float r0 = n < n_tok ? rvec[n] : 0.f, r1 = n + 1 < n_tok ? rvec[n + 1] : 0.f;
+                  const float send = odd ? f[i] * r0 : f[i + 1] * r1;
                   const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
-                  const float g = odd ? recv : __uint_as_float(v[i]);
-                  const float u = odd ? __uint_as_float(v[i + 1]) : recv;
+                  const float g = odd ? recv : f[i] * r0;
+                  const float u = odd ? f[i + 1] * r1 : recv;
                   const int tok = cc + i + (odd ? 1 : 0);
-                  sts_u16(sbase + (uint32_t)(tok * stg_row), __bfloat16_as_ushort(__float2bfloat16_rn(silu_f(g) * u)));
+                  sts_u16(sbase + (uint32_t)(tok * 128), __bfloat16_as_ushort(__float2bfloat16_rn(silu_f(g) * u)));
                 }
-              } else {
-                const uint32_t sbase = stg_base + (uint32_t)row * 4u;
-#pragma unroll
-                for (int i = 0; i < 32; ++i) sts_f32(sbase + (uint32_t)((cc + i) * stg_row), __uint_as_float(v[i]));
+              }
+              if (hh == 1 && !from_ws) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+              }
+              asm volatile("bar.sync 1, 128;" ::: "memory");  // staging complete
+              const int n0 = nt * BN + hh * HALF;
+              const int rows = min(HALF, n_tok - n0);
+              for (int idx = ep_tid; idx < rows * vec_per_row; idx += 128) {
+                const int r = idx / vec_per_row, cv = idx % vec_per_row;
+                const uint4 val = lds128(stg_base + (uint32_t)(r * 128 + cv * 16));
+                *reinterpret_cast<uint4*>(gbase + (int64_t)(n0 + r) * gstride + cv * 16) = val;
               }
             }
-            if (hh == 1) {
+          } else {
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+              const int n0 = nt * BN + c0;
+              if (n0 >= n_tok) break;  // block-uniform
+              float f[32];
+              if (mode == CE_RESID_SS && from_ws) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) f[i] = 0.f;  // the partials are already in x
+              } else {
+                chain_src(from_ws, acc_tile, tbase, c0, row, n_valid, f);
+              }
+              if (mode == CE_RESID_SS) {
+                float xv[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  xv[i] = (mv && n0 + i < n_tok) ? __ldcg(S.x + (int64_t)(n0 + i) * m_rows + m) : 0.f;
+                const float gm = mv ? __bfloat162float(S.gamma[m]) : 0.f;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  xv[i] += f[i];
+                  if (mv && n0 + i < n_tok) {
+                    S.x[(int64_t)(n0 + i) * m_rows + m] = xv[i];
+                    S.hb[(int64_t)(n0 + i) * m_rows + m] = __float2bfloat16_rn(xv[i] * gm);
+                  }
+                  xv[i] = (mv && n0 + i < n_tok) ? xv[i] * xv[i] : 0.f;
+                }
+                const float wsum = warp_transpose_sum(xv, lane);  // token n0 + lane, this warp's 32 rows
+                red[q * 32 + lane] = wsum;
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (ep_tid < 32 && n0 + ep_tid < n_tok)  // fixed order over the 4 row quarters
+                  S.ssp_out[(int64_t)mt * call.ss_ld + n0 + ep_tid] =
+                      ((red[ep_tid] + red[32 + ep_tid]) + red[64 + ep_tid]) + red[96 + ep_tid];
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+              } else {  // CE_QKV_R
+#pragma unroll
+                for (int i = 0; i < 32; ++i) f[i] *= (n0 + i < n_tok) ? rvec[n0 + i] : 0.f;
+                eq.mode = EPI_SWAP_QKV;
+                epi_swap(eq, m, m_rows, n0, n_tok, lane, f);
+              }
+            }
+            if (!from_ws) {
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(&tempty_bar[acc]);
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // staging complete
-            const int n0 = nt * BN + hh * HALF;
-            const int rows = min(HALF, n_tok - n0);
-            for (int idx = ep_tid; idx < rows * vec_per_row; idx += 128) {
-              const int r = idx / vec_per_row, cv = idx % vec_per_row;
-              const uint4 val = lds128(stg_base + (uint32_t)(r * stg_row + cv * 16));
-              *reinterpret_cast<uint4*>(gbase + (int64_t)(n0 + r) * gstride + cv * 16) = val;
-            }
           }
-          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
-      } else {
-        if (ep_tid == 0) chain_grid_wait(call, call.bar_base + (unsigned long long)si * grid);
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (S.red == CR_RESID_NORM) chain_resid_norm(S, call, ep_tid, red);
-        else chain_pairs(S, call, ep_tid);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        j = seg_end;
       }
-      // arrive: this CTA's part of step si is in memory. A CTA without work units in a
-      // GEMM step must still observe the step's own barrier first, or its arrival could
-      // stand in for a slower CTA's arrival of the previous step (the counter only counts)
-      if (S.kind == CS_GEMM && si > 0 && ep_tid == 0)
-        chain_grid_wait(call, call.bar_base + (unsigned long long)si * grid);
+      // arrive: this CTA's part of step si is in memory
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (ep_tid == 0) {
         __threadfence();
         atomicAdd(call.bar, 1ull);
-        if (call.trace) call.trace[(blockIdx.x * 32 + si) * 4 + 2] = gtime_ns();
+        if (call.trace) call.trace[(me * 32 + si) * 4 + 2] = gtime_ns();
       }
     }
   }
@@ -1785,6 +1782,7 @@ cudaError_t decode_chain_launch(const ChainStep* d_steps, int n_steps, const Cha
   cudaError_t e = ensure_smem(decode_chain_kernel, ChainCfg::SMEM);
   if (e != cudaSuccess) return e;
   if (c.n_tok <= 0 || n_steps <= 0) return cudaSuccess;
+  if (c.n_tok > 512) return cudaErrorInvalidValue;
   return launch_k(decode_chain_kernel, dim3(num_sms), dim3(GEMM_THREADS), ChainCfg::SMEM, stream, d_steps, n_steps,
                   c);
 }

@@ -103,40 +103,41 @@ cudaError_t gemm_cluster_launch(const CUtensorMap* mapA, const CUtensorMap* mapB
 int gemm_cluster_max_active(int bn, int splits);
 
 // ------------------------------------------------------------------ decode layer chain
-// One persistent kernel (one CTA per SM) runs the post-attention part of a decode layer
-// as a sequence of steps -- O GEMM, residual + RMSNorm, gate/up GEMM (+SiLU), down GEMM,
-// residual + next RMSNorm, next layer's QKV GEMM, RoPE + KV write -- with a grid-wide
-// barrier between dependent steps instead of a kernel boundary. The TMA producer keeps
-// streaming the next GEMM's weights into free smem stages while the barrier is pending;
-// only the activation loads wait for it.
-enum ChainStepKind : int { CS_GEMM = 0, CS_REDUCE = 1 };
-enum ChainRedMode : int { CR_RESID_NORM = 0, CR_QKV = 1, CR_SILU = 2 };
+// One persistent kernel (one CTA per SM) runs the post-attention GEMMs of a decode layer
+// -- O, gate/up, down and the next layer's QKV -- with a grid-wide barrier between them
+// instead of kernel boundaries. Every GEMM is partitioned stream-K: CTA c owns an equal
+// contiguous range of the flattened (tile, K-block) iterations; the CTAs sharing a tile
+// add their f32 partials with L2 atomics (into x for the residual modes, else into a
+// zeroed tile buffer) and the last one to arrive (counter) applies the epilogue -- the
+// sum order of a split tile is therefore not fixed (fp32 rounding may differ run to
+// run); the epilogues carry the rest of the layer:
+//   CE_RESID_SS  x += acc; hb = bf16(x * gamma) (the next RMSNorm's input before its
+//                1/rms); ssp[m-tile][tok] = sum of x^2 over the tile's 128 features
+//   CE_SILU_R    acc *= r_tok (r = rsqrt(sum_t ssp[t][tok] / H + eps)): the RMSNorm
+//                scale applied after the GEMM; out = silu(gate) * up
+//   CE_QKV_R     acc *= r_tok; RoPE on the pair-interleaved q / k rows; q, paged K / V
+// The producer streams a GEMM's weights into free smem stages before the barrier and
+// waits only before its activation loads.
+enum ChainEpi : int { CE_RESID_SS = 0, CE_SILU_R = 1, CE_QKV_R = 2 };
 struct ChainStep {
-  int kind;
-  // CS_GEMM (swap-AB, BN 128): D[m][tok] = W[m] . X[tok]; mode EPI_SWAP_F32 (partials
-  // [splits][n_tok][ldo]) or EPI_SWAP_SILU (splits 1: out bf16 [n_tok][ldo] at m/2)
-  const CUtensorMap* wmap;  // weights, 128-row box (device memory)
-  const CUtensorMap* xmap;  // activations, 128-row box (device memory)
-  int m_rows, K, splits, mode;
-  void* out;
-  int64_t ldo;
-  // CS_REDUCE: sum of `rsplits` partial planes [rsplits][n_tok][cols] (split order), then
-  //   CR_RESID_NORM: x += sum; h = bf16(rmsnorm(x) * gamma)          (cols = H)
-  //   CR_QKV:        RoPE on q/k pairs -> e.q_out / paged K, V -> pool (e: QKV epilogue)
-  //   CR_SILU:       e.out[tok][c/2] = silu(sum[c]) * sum[c + 1]
-  int red;
-  const float* part;
-  int rsplits, cols;
-  float* x;
-  const bf16* gamma;
-  bf16* h;
+  const CUtensorMap* wmap;  // weights [m_rows][K], 128-row box (device memory)
+  const CUtensorMap* xmap;  // activations [tok][K], 128-row box (device memory)
+  int m_rows, K, mode;
+  float* x;                 // CE_RESID_SS: residual [tok][m_rows] f32
+  const bf16* gamma;        //   next RMSNorm weight [m_rows]
+  bf16* hb;                 //   bf16(x * gamma) [tok][m_rows]
+  float* ssp_out;           //   [m_rows / 128][ss_ld]
+  const float* ssp_in;      // CE_SILU_R / CE_QKV_R: [ssp_tiles][ss_ld] of the previous step
+  int ssp_tiles, H;
   float eps;
-  GemmEpi e;  // CR_QKV / CR_SILU parameters; pos / slot come from the call
+  GemmEpi e;                // SILU_R: e.out bf16 [tok][e.ldo]; QKV_R: RoPE / q / pool geometry
+  int* counters;            // per-tile arrivals of this step (zero on entry, left zero)
 };
 struct ChainCall {
-  int n_tok;
-  const int* pos;                 // [n_tok] (CR_QKV)
-  const int* slot;                // [n_tok] (CR_QKV)
+  int n_tok, ss_ld;               // tokens (<= 512); row stride of the ssp buffers
+  const int* pos;                 // [n_tok] (CE_QKV_R)
+  const int* slot;                // [n_tok] (CE_QKV_R)
+  float* ws;                      // split tiles' f32 sums [tiles][128 tok][128] (zero on entry, left zero)
   unsigned long long* bar;        // grid-barrier counter, monotonic across launches
   unsigned long long bar_base;    // its value when this launch starts
   int* err;                       // set to 1 if a grid barrier timed out (CTAs not co-resident)
