@@ -776,12 +776,12 @@ cudaError_t prefill_gemm(ecoserve_instance* inst, const CUtensorMap& amap, const
 
 // Skinny decode GEMM (swap-AB): weights on the MMA M side, the B tokens on N, K split so
 // the grid fills the SMs; the epilogue (and the split reduction) run inside the kernel.
-int decode_variant() {  // 1: 1-CTA/SM GEMM (default); 3: lean (co-resident with the next kernel)
+int decode_variant() {  // 1: one A+B ring (default); 3: lean (co-resident); 4: split weight / activation rings
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("ECOSERVE_DEC_VARIANT");
     v = e ? atoi(e) : 1;
-    if (v != 1 && v != 3) v = 1;
+    if (v != 1 && v != 3 && v != 4) v = 1;
   }
   return v;
 }

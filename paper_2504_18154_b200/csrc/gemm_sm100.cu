@@ -33,9 +33,14 @@ static constexpr int GEMM_THREADS = 192;
 // R = 3 selects the "lean" single-tile variant: 3 smem stages (< 114 KB of smem) so a
 // CTA of the next kernel on the stream can be resident beside it -- with PDL its
 // prologue and weight prefetch then overlap this kernel's tail.
+// R = 4 selects split rings (decode): the weight (A) tiles and the activation (B) tiles
+// get separate smem rings with their own barriers -- SA = 9-10 weight stages, SB = 3-4
+// activation stages -- so ~150 KB of weights are in flight per SM instead of 96 KB. The
+// activations come from L2 (short latency) and no longer take half of every stage.
 template <int BN, int R = 1>
 struct GemmCfg {
-  static constexpr int RT = R == 3 ? 1 : R;  // A tiles per unit
+  static constexpr bool SPLIT = R == 4;
+  static constexpr int RT = (R == 3 || R == 4) ? 1 : R;  // A tiles per unit
   static constexpr int A_BYTES = RT * BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -52,7 +57,16 @@ struct GemmCfg {
   static constexpr int ACC_COLS = RT * BN;  // one accumulator stage
   static constexpr int TMEM_COLS = (2 * ACC_COLS) <= 32 ? 32 : (2 * ACC_COLS) <= 64 ? 64 : (2 * ACC_COLS) <= 128 ? 128
                                  : (2 * ACC_COLS) <= 256 ? 256 : 512;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + STAGING + 1024 /*align*/ + 256 /*barriers*/;
+  // split rings (R = 4)
+  static constexpr int SB = BN >= 128 ? 3 : 4;
+  static constexpr int BAR_BYTES = SPLIT ? 512 : 256;
+  static constexpr int SA_FIT = (SMEM_MAX - 1024 - BAR_BYTES - STAGING - SB * B_BYTES) / A_BYTES;
+  static constexpr int SA = SA_FIT > 12 ? 12 : SA_FIT;
+  static constexpr int NA = SPLIT ? SA : STAGES;  // full/empty barrier pairs of the (A or A+B) ring
+  static constexpr int NB = SPLIT ? SB : 0;       // ... of the B ring
+  static constexpr int RING = SPLIT ? SA * A_BYTES + SB * B_BYTES : STAGES * STAGE_BYTES;
+  static constexpr int SMEM = RING + STAGING + 1024 /*align*/ + BAR_BYTES /*barriers*/;
+  static_assert((2 * NA + 2 * NB + 4) * 8 + 8 <= BAR_BYTES, "barriers fit");
   static_assert(4 * BN * 8 <= STAGING, "argmax scratch lives in the staging buffer");
   static_assert(2 * ACC_COLS <= 512, "two accumulator stages must fit the 512 TMEM columns");
 };
@@ -271,15 +285,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   constexpr int R = C::RT;  // 128-row A tiles per work unit
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* staging = smem + C::STAGES * C::STAGE_BYTES;
+  uint8_t* staging = smem + C::RING;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(staging + C::STAGING);
-  uint64_t* empty_bar = full_bar + C::STAGES;
-  uint64_t* tfull_bar = empty_bar + C::STAGES;
+  uint64_t* empty_bar = full_bar + C::NA;
+  uint64_t* full_b = empty_bar + C::NA;   // split rings: the B ring's barriers
+  uint64_t* empty_b = full_b + C::NB;
+  uint64_t* tfull_bar = empty_b + C::NB;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_base_ptr = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   int& s_last = *reinterpret_cast<int*>(tmem_base_ptr + 1);
   auto am_v = reinterpret_cast<float(*)[BN]>(staging);               // [4][BN] argmax scratch
   auto am_i = reinterpret_cast<int(*)[BN]>(staging + 4 * BN * 4);
+  uint8_t* ring_b = smem + C::SA * C::A_BYTES;  // split rings: B ring after the SA weight stages
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int m_tiles = (m_rows + BM * R - 1) / (BM * R);  // work units of R x 128 rows
@@ -295,9 +312,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     trace_mark(epi, 0);  // CTA start
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < C::NA; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < C::NB; ++s) {
+      mbar_init(&full_b[s], 1);
+      mbar_init(&empty_b[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
@@ -319,7 +340,83 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   pdl_trigger();
   if (threadIdx.x == 0) trace_mark(epi, 1);  // prologue done
 
-  if (warp == 0) {
+  if (C::SPLIT && warp == 0) {
+    // ------------------------------------------------------------ TMA producer (split rings)
+    if (lane == 0) {
+      // two cursors over this CTA's (work unit, K block) sequence: the weights run SA
+      // iterations ahead of the MMA, the activations SB; the MMA of iteration j frees
+      // weight slot j % SA and activation slot j % SB
+      struct Cur {
+        int w, kb, kb1, mt, nt;
+      };
+      auto next = [&](Cur& c) -> bool {
+        if (c.kb >= 0 && c.kb + 1 < c.kb1) { ++c.kb; return true; }
+        if (c.kb >= 0) c.w += gridDim.x;
+        if (c.w >= n_work) return false;
+        const int ks = c.w % splits, t = c.w / splits;
+        c.mt = t / n_tiles;
+        c.nt = t % n_tiles;
+        c.kb = ks * kb_per;
+        c.kb1 = min(kb_total, c.kb + kb_per);
+        return true;
+      };
+      Cur ca{(int)blockIdx.x, -1, 0, 0, 0}, cb{(int)blockIdx.x, -1, 0, 0, 0};
+      bool a_more = true, b_more = true;
+      int na = 0, nb = 0;
+      for (; na < C::SA && (a_more = next(ca)); ++na) {  // weights: before the PDL wait
+        mbar_arrive_expect_tx(&full_bar[na], C::A_BYTES);
+        tma_load_2d(smem + na * C::A_BYTES, &mapA, &full_bar[na], ca.kb * BK, ca.mt * BM);
+      }
+      pdl_wait();
+      for (; nb < C::SB && (b_more = next(cb)); ++nb) {
+        mbar_arrive_expect_tx(&full_b[nb], C::B_BYTES);
+        tma_load_2d(ring_b + nb * C::B_BYTES, &mapB, &full_b[nb], cb.kb * BK, cb.nt * BN);
+      }
+      for (int j = 0; a_more || b_more; ++j) {
+        if (a_more && (a_more = next(ca))) {
+          const int s = j % C::SA;
+          mbar_wait(&empty_bar[s], (j / C::SA) & 1);
+          mbar_arrive_expect_tx(&full_bar[s], C::A_BYTES);
+          tma_load_2d(smem + s * C::A_BYTES, &mapA, &full_bar[s], ca.kb * BK, ca.mt * BM);
+        }
+        if (b_more && (b_more = next(cb))) {
+          const int s = j % C::SB;
+          mbar_wait(&empty_b[s], (j / C::SB) & 1);
+          mbar_arrive_expect_tx(&full_b[s], C::B_BYTES);
+          tma_load_2d(ring_b + s * C::B_BYTES, &mapB, &full_b[s], cb.kb * BK, cb.nt * BN);
+        }
+      }
+    }
+  } else if (C::SPLIT && warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (split rings)
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      int acc = 0, j = 0;
+      uint32_t acc_phase = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        const int ks = w % splits;
+        const int kb0 = ks * kb_per, kb1 = min(kb_total, kb0 + kb_per);
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
+        for (int kb = kb0; kb < kb1; ++kb, ++j) {
+          const int sa = j % C::SA, sb = j % C::SB;
+          mbar_wait(&full_bar[sa], (j / C::SA) & 1);
+          mbar_wait(&full_b[sb], (j / C::SB) & 1);
+          tc_fence_after();
+          const uint64_t da = umma_desc_sw128(smem_u32(smem + sa * C::A_BYTES));
+          const uint64_t db = umma_desc_sw128(smem_u32(ring_b + sb * C::B_BYTES));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            tc_mma_f16(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          tc_commit(&empty_bar[sa]);
+          tc_commit(&empty_b[sb]);
+        }
+        tc_commit(&tfull_bar[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int stage = 0;
@@ -1353,6 +1450,13 @@ cudaError_t gemm_launch_r(const CUtensorMap* mapA, const CUtensorMap* mapB, int 
     switch (bn) {
       case 64: return launch_bn<64, 2>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
       case 128: return launch_bn<128, 2>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  if (r == 4) {  // split weight / activation rings (decode)
+    switch (bn) {
+      case 64: return launch_bn<64, 4>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
+      case 128: return launch_bn<128, 4>(mapA, mapB, m_rows, n_rows, K, splits, epi, num_sms, stream);
       default: return cudaErrorInvalidValue;
     }
   }
