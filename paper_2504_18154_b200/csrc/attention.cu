@@ -212,7 +212,6 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(PrefillAttnArgs a) {
 }
 
 // ------------------------------------------------------------------ decode
-static constexpr int DEC_STAGES = 3;
 
 // byte offset of 16-byte chunk c (0..15) of row r in a [64][128] bf16 tile staged by
 // TMA with 128B swizzle as two [64][64] panels (chunk c%8 of a panel row at c ^ (r%8))
@@ -222,7 +221,9 @@ __device__ __forceinline__ uint32_t tma_swz(int r, int c) {
 
 // TMA: K/V tiles arrive by cp.async.bulk.tensor (one elected thread, mbarrier per
 // stage) into 128B-swizzled panels; otherwise cp.async into the XOR-swizzled layout.
-template <int D, bool TMA>
+// DEC_STAGES = 3 (2 CTAs per SM) or 2 (68 KB of smem: 3 CTAs per SM, one block of
+// prefetch per CTA; more CTAs in flight when the grid is a few waves of uniform lengths)
+template <int D, bool TMA, int DEC_STAGES = 3>
 __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a, const __grid_constant__ CUtensorMap kvmap) {
   constexpr int NK = D / 16, ND = D / 8;
   extern __shared__ __align__(128) uint8_t sm_raw[];
@@ -467,14 +468,15 @@ cudaError_t attn_prefill_launch(const PrefillAttnArgs& a, int head_dim, cudaStre
   }
 }
 
-template <int D>
-static cudaError_t decode_d(const DecodeAttnArgs& a, cudaStream_t s) {
+template <int D, int ST>
+static cudaError_t decode_st(const DecodeAttnArgs& a, cudaStream_t s) {
   const bool tma = D == 128 && a.kvmap != nullptr;
-  int smem = (2 * DEC_STAGES * 64 * D + 16 * D) * 2;
+  int smem = (2 * ST * 64 * D + 16 * D) * 2;
   const int red_bytes = 4 * 16 * (D + 2) * 4;
   if (smem < red_bytes) smem = red_bytes;
   if (tma) smem += 1024 + 64;  // 1 KB alignment slack + stage barriers
-  cudaError_t e = tma ? ensure_smem(attn_decode_kernel<D, true>, smem) : ensure_smem(attn_decode_kernel<D, false>, smem);
+  cudaError_t e = tma ? ensure_smem(attn_decode_kernel<D, true, ST>, smem)
+                      : ensure_smem(attn_decode_kernel<D, false, ST>, smem);
   if (e != cudaSuccess) return e;
   if (a.B == 0) return cudaSuccess;
   if (a.n_heads / a.n_kv > 16) return cudaErrorInvalidValue;
@@ -482,11 +484,21 @@ static cudaError_t decode_d(const DecodeAttnArgs& a, cudaStream_t s) {
   memset(&dummy, 0, sizeof(dummy));
   const CUtensorMap& map = tma ? *a.kvmap : dummy;
   if (tma)
-    e = launch_k(attn_decode_kernel<D, true>, dim3(a.B * a.n_kv, 1, a.n_splits), dim3(128), smem, s, a, map);
+    e = launch_k(attn_decode_kernel<D, true, ST>, dim3(a.B * a.n_kv, 1, a.n_splits), dim3(128), smem, s, a, map);
   else
-    e = launch_k(attn_decode_kernel<D, false>, dim3(a.B * a.n_kv, 1, a.n_splits), dim3(128), smem, s, a, map);
+    e = launch_k(attn_decode_kernel<D, false, ST>, dim3(a.B * a.n_kv, 1, a.n_splits), dim3(128), smem, s, a, map);
   if (e != cudaSuccess || a.n_splits == 1) return e;
   return launch_k(attn_combine_kernel<D>, dim3(a.B, a.n_heads), dim3(D), 0, s, a);
+}
+
+template <int D>
+static cudaError_t decode_d(const DecodeAttnArgs& a, cudaStream_t s) {
+  static int st = -1;  // ECOSERVE_ATTN_STAGES=2: 3 CTAs per SM
+  if (st < 0) {
+    const char* e = getenv("ECOSERVE_ATTN_STAGES");
+    st = (e && e[0] == '2') ? 2 : 3;
+  }
+  return st == 2 ? decode_st<D, 2>(a, s) : decode_st<D, 3>(a, s);
 }
 
 cudaError_t attn_decode_launch(const DecodeAttnArgs& a, int head_dim, cudaStream_t s) {

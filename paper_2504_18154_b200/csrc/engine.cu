@@ -837,9 +837,21 @@ void set_prefetch(ecoserve_instance* inst, GemmEpi& e, int map_idx, int n_out, i
 // norm_gamma / norm_out (optional): when the projection is a residual add split over K,
 // its reduction is fused with the following RMSNorm (one kernel: x += sum of partials,
 // out = rmsnorm(x) * gamma); *fused reports whether that happened.
+// ECOSERVE_PAIR_TILES=1: gate/up decode GEMM with two 128-row weight tiles per CTA (one wave
+// of 112 CTAs for 224 tiles) instead of one tile per CTA (148 + 76); measured neutral
+// (8B decode 15.36k vs 15.46k tok/s, 70B shard 20.99 vs 21.16 ms/step), so off by default
+bool pair_tiles_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_PAIR_TILES");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const ActMaps& xm, int n_out, int K, int B,
                         int mode, GemmEpi e, int* nk, const bf16* norm_gamma = nullptr, bf16* norm_out = nullptr,
-                        bool* fused = nullptr) {
+                        bool* fused = nullptr, const CUtensorMap* wmap256 = nullptr) {
   const int bn = B <= 64 ? 64 : 128;  // B > 128: several 128-token tiles; weight re-reads hit L2
   const int splits = gemm_decode_splits(n_out, K, inst->num_sms);
   const int var = decode_variant();
@@ -848,6 +860,12 @@ cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const 
   if (splits == 1) {  // epilogue in the GEMM
     e.mode = mode;
     *nk = 1;
+    const int tiles = (n_out + 127) / 128;
+    // more tiles than SMs: two weight tiles (a 256-row box) per CTA behind one activation
+    // tile, so all units run in one wave (gate/up: 112 units instead of 148 + 76)
+    if (wmap256 && mode == EPI_SWAP_SILU && pair_tiles_enabled() && tiles > inst->num_sms &&
+        (tiles + 1) / 2 <= inst->num_sms && (B + bn - 1) / bn == 1)
+      return gemm_launch_r(wmap256, &xm.b[bn_index(bn)], n_out, B, K, bn, 2, 1, e, inst->num_sms, inst->stream);
     return gemm_launch_r(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, var, 1, e, inst->num_sms, inst->stream);
   }
   // split-K over a thread-block cluster, reduced in distributed shared memory with the
@@ -1253,7 +1271,7 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     eg.ldo = F;
     set_prefetch(inst, eg, 4 * l + 3, H, F, B);  // down next
     LAUNCH(P_GEMM_DECODE, 2.0 * 2 * F * H, nk,
-           decode_gemm(inst, w.gu_a, inst->m_h, 2 * F, H, B, EPI_SWAP_SILU, eg, &nk));
+           decode_gemm(inst, w.gu_a, inst->m_h, 2 * F, H, B, EPI_SWAP_SILU, eg, &nk, nullptr, nullptr, nullptr, &w.gu_b));
     // the down projection's reduction also applies the next RMSNorm: the next layer's
     // attention norm, or after the last layer the final norm (into the LM-head input)
     const bool last = l + 1 == L;

@@ -46,7 +46,7 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // epilogue staging: half an accumulator tile in f32 (BN/2 tokens x 128 features) for
   // the bulk-store epilogues (BN <= 128, one A tile); otherwise just the argmax scratch
-  static constexpr bool BULK_EPI = BN <= 128 && RT == 1;
+  static constexpr bool BULK_EPI = BN <= 128 && RT <= 2;
   // (argmax epilogue: 4 x BN (max, idx) + one padded [32][BM + 1] f32 chunk)
   static constexpr int ARGMAX_STG = 4 * BN * 8 + 32 * (BM + 1) * 4;
   static constexpr int STAGING = BULK_EPI ? ((BN / 2) * BM * 4 > ARGMAX_STG ? (BN / 2) * BM * 4 : ARGMAX_STG)
@@ -540,7 +540,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int row = q * 32 + lane;  // accumulator row (TMEM lane)
       const int m = mt * BM * R + row;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::ACC_COLS;
-      if (epi.mode == EPI_SWAP_ARGMAX && C::BULK_EPI) {
+      if (epi.mode == EPI_SWAP_ARGMAX && C::BULK_EPI && R == 1) {
         // per 32-token chunk: the 128 x 32 accumulator slice goes to smem transposed
         // ([token][row], padded row stride), then thread t scans rows 32*(t/32).. of token
         // t%32 -- 32 compares per thread instead of a 5-round shuffle argmax per token
@@ -629,65 +629,68 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // stores (instead of 128 scattered 4-byte stores per thread), half a tile at a time
         const bool silu = epi.mode == EPI_SWAP_SILU;
         constexpr int HALF = BN / 2;
-        const int m0 = mt * BM;
-        const int mcount = min(BM, m_rows - m0);
-        const int vec_per_row = silu ? mcount / 16 : mcount / 4;     // 16-byte vectors per token row
-        const int stg_row = silu ? BM / 2 * 2 : BM * 4;              // staging row bytes
-        char* gbase = silu ? reinterpret_cast<char*>(reinterpret_cast<bf16*>(epi.out) + m0 / 2)
-                           : reinterpret_cast<char*>(reinterpret_cast<float*>(epi.out) +
-                                                     (int64_t)ks * n_rows * epi.ldo + m0);
-        const int64_t gstride = silu ? epi.ldo * 2 : epi.ldo * 4;
-        const uint32_t stg_base = smem_u32(staging);
         long long c_wr = 0, c_ld = 0, c_math = 0, c_out = 0, c0_ = 0;
-        for (int h = 0; h < 2; ++h) {
-          c0_ = clk();
-          asm volatile("bar.sync 1, 128;" ::: "memory");  // staging free (previous copy-out done)
-          c_wr += clk() - c0_;
 #pragma unroll 1
-          for (int cc = 0; cc < HALF; cc += 32) {
-            uint32_t v[32];
+        for (int rt = 0; rt < R; ++rt) {  // the unit's 128-row weight tiles (R = 2: one wave for gate/up)
+          const int m0 = (mt * R + rt) * BM;
+          const int mcount = max(0, min(BM, m_rows - m0));             // (R = 2: the 2nd tile may be empty)
+          const int vec_per_row = silu ? mcount / 16 : mcount / 4;     // 16-byte vectors per token row
+          const int stg_row = silu ? BM / 2 * 2 : BM * 4;              // staging row bytes
+          char* gbase = silu ? reinterpret_cast<char*>(reinterpret_cast<bf16*>(epi.out) + m0 / 2)
+                             : reinterpret_cast<char*>(reinterpret_cast<float*>(epi.out) +
+                                                       (int64_t)ks * n_rows * epi.ldo + m0);
+          const int64_t gstride = silu ? epi.ldo * 2 : epi.ldo * 4;
+          const uint32_t stg_base = smem_u32(staging);
+          for (int h = 0; h < 2; ++h) {
             c0_ = clk();
-            tmem_ld32(tbase + h * HALF + cc, v);
-            tc_wait_ld();
-            const long long c1_ = clk();
-            c_ld += c1_ - c0_;
-            c0_ = c1_;
-            if (silu) {
-              // lanes 2j / 2j+1 hold gate_j / up_j; one exchange per token pair gives the
-              // even lane (gate, up) of token i and the odd lane those of token i + 1
-              const bool odd = lane & 1;
-              const uint32_t sbase = stg_base + (uint32_t)(row / 2) * 2u;
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // staging free (previous copy-out done)
+            c_wr += clk() - c0_;
+#pragma unroll 1
+            for (int cc = 0; cc < HALF; cc += 32) {
+              uint32_t v[32];
+              c0_ = clk();
+              tmem_ld32(tbase + rt * BN + h * HALF + cc, v);
+              tc_wait_ld();
+              const long long c1_ = clk();
+              c_ld += c1_ - c0_;
+              c0_ = c1_;
+              if (silu) {
+                // lanes 2j / 2j+1 hold gate_j / up_j; one exchange per token pair gives the
+                // even lane (gate, up) of token i and the odd lane those of token i + 1
+                const bool odd = lane & 1;
+                const uint32_t sbase = stg_base + (uint32_t)(row / 2) * 2u;
 #pragma unroll
-              for (int i = 0; i < 32; i += 2) {
-                const float send = odd ? __uint_as_float(v[i]) : __uint_as_float(v[i + 1]);
-                const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
-                const float g = odd ? recv : __uint_as_float(v[i]);
-                const float u = odd ? __uint_as_float(v[i + 1]) : recv;
-                const int tok = cc + i + (odd ? 1 : 0);
-                sts_u16(sbase + (uint32_t)(tok * stg_row), __bfloat16_as_ushort(__float2bfloat16_rn(silu_f(g) * u)));
+                for (int i = 0; i < 32; i += 2) {
+                  const float send = odd ? __uint_as_float(v[i]) : __uint_as_float(v[i + 1]);
+                  const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
+                  const float g = odd ? recv : __uint_as_float(v[i]);
+                  const float u = odd ? __uint_as_float(v[i + 1]) : recv;
+                  const int tok = cc + i + (odd ? 1 : 0);
+                  sts_u16(sbase + (uint32_t)(tok * stg_row), __bfloat16_as_ushort(__float2bfloat16_rn(silu_f(g) * u)));
+                }
+              } else {
+                const uint32_t sbase = stg_base + (uint32_t)row * 4u;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) sts_f32(sbase + (uint32_t)((cc + i) * stg_row), __uint_as_float(v[i]));
               }
-            } else {
-              const uint32_t sbase = stg_base + (uint32_t)row * 4u;
-#pragma unroll
-              for (int i = 0; i < 32; ++i) sts_f32(sbase + (uint32_t)((cc + i) * stg_row), __uint_as_float(v[i]));
+              c_math += clk() - c0_;
             }
-            c_math += clk() - c0_;
+            c0_ = clk();
+            if (h == 1 && rt == R - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // staging complete
+            const int n0 = nt * BN + h * HALF;
+            const int rows = max(0, min(HALF, n_rows - n0));
+            for (int idx = ep_tid; idx < rows * vec_per_row; idx += 128) {
+              const int r = idx / vec_per_row, c = idx % vec_per_row;
+              const uint4 val = lds128(stg_base + (uint32_t)(r * stg_row + c * 16));
+              *reinterpret_cast<uint4*>(gbase + (int64_t)(n0 + r) * gstride + c * 16) = val;
+            }
+            c_out += clk() - c0_;
           }
-          c0_ = clk();
-          if (h == 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty_bar[acc]);
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");  // staging complete
-          const int n0 = nt * BN + h * HALF;
-          const int rows = min(HALF, n_rows - n0);
-          for (int idx = ep_tid; idx < rows * vec_per_row; idx += 128) {
-            const int r = idx / vec_per_row, c = idx % vec_per_row;
-            const uint4 val = lds128(stg_base + (uint32_t)(r * stg_row + c * 16));
-            *reinterpret_cast<uint4*>(gbase + (int64_t)(n0 + r) * gstride + c * 16) = val;
-          }
-          c_out += clk() - c0_;
         }
         if (threadIdx.x == 64) {
           trace_put(epi, 8, c_wr);

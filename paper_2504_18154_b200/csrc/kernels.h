@@ -76,8 +76,10 @@ struct GemmEpi {
 
 // Split count for a decode GEMM: minimises waves x K-blocks per CTA (+ a per-split reduction cost).
 int gemm_choose_splits(int m_rows, int n_rows, int K, int bn, int num_sms, int max_splits);
-// Split count of the engine's decode GEMMs (measured on B200, tools/gemm_decode_sweep.py):
-// no split once the weight tiles cover most SMs, else ~SMs/tiles (2..4) splits.
+// Split count of the engine's decode GEMMs: no split once the weight tiles cover 3/4 of
+// the SMs, else the s in 1..4 with the fewest K blocks on the busiest CTA (waves x K blocks
+// per split + a reduction cost) -- the 8B choices of the measured sweep
+// (tools/gemm_decode_sweep.py), and 3 instead of 4 for the 70B/TP=2 QKV (40 tiles).
 int gemm_decode_splits(int m_rows, int K, int num_sms);
 
 // Creates a 2D bf16 tensor map (rows x cols, row-major, 128B swizzle, box 64 x box_rows).
