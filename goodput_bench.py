@@ -25,6 +25,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 
+def srv_prefill(args, n: int) -> int:
+    return args.fudg_prefill if 0 < args.fudg_prefill < n else n // 2
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -44,9 +48,11 @@ def main():
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--blocks", type=int, default=8000)
     ap.add_argument("--rates", type=str, default="", help="comma list: fixed probes instead of bisection")
-    ap.add_argument("--policy", choices=("padg", "nodg", "sarathi"), default="padg",
+    ap.add_argument("--policy", choices=("padg", "nodg", "sarathi", "fudg"), default="padg",
                     help="padg: macro routing + rolling activation; nodg: round-robin separate batching; "
-                         "sarathi: round-robin hybrid (chunked-prefill) batching")
+                         "sarathi: round-robin hybrid (chunked-prefill) batching; fudg: prefill-only and "
+                         "decode-only instances with the KV moved over NVLink")
+    ap.add_argument("--fudg-prefill", type=int, default=0, help="fudg: prefill instances (default half)")
     ap.add_argument("--chunk-budget", type=int, default=1024, help="sarathi: tokens per hybrid iteration")
     args = ap.parse_args()
 
@@ -83,7 +89,7 @@ def main():
             r.req_id += rid0[0]
         rid0[0] += n_req
         srv = PaDGServer(insts, slo_ttft, slo_tpot, reserve_tokens=237, predictor_table=(lens, ns),
-                         policy=args.policy, chunk_budget=args.chunk_budget)
+                         policy=args.policy, chunk_budget=args.chunk_budget, fudg_prefill=args.fudg_prefill)
         t0 = time.perf_counter()
         out = srv.run(trace, timeout_s=900)
         wall = time.perf_counter() - t0
@@ -115,7 +121,9 @@ def main():
                        "shape": args.shape,
                        "macro": f"{len(insts)} instances, " + {
                            "padg": "rolling activation (Alg. 1/2)", "nodg": "NoDG round-robin separate batching",
-                           "sarathi": f"NoDG round-robin hybrid batching, {args.chunk_budget}-token iterations"}[
+                           "sarathi": f"NoDG round-robin hybrid batching, {args.chunk_budget}-token iterations",
+                           "fudg": f"FuDG: {srv_prefill(args, len(insts))} prefill + "
+                                   f"{len(insts) - srv_prefill(args, len(insts))} decode instances, KV over NVLink"}[
                            args.policy]},
             "policy": args.policy,
             "predictor": {"lens": lens, "ns": ns}, "probes": probes}

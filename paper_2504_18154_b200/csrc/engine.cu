@@ -936,6 +936,33 @@ cudaError_t decode_partials(ecoserve_instance* inst, const CUtensorMap& wmap, co
                        inst->stream);
 }
 
+// Decode O / down projection of a TP rank whose bulk f32 epilogue writes its split
+// partials [splits][B][H] both to this GPU's receive plane and, over NVLink, to the
+// peer's; tp_allreduce then sums both ranks' partials locally (same order and bits as
+// the per-row push). ECOSERVE_TP_DECODE_PUSH=0: per-row push (tp_push_rows).
+bool tp_decode_push_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_TP_DECODE_PUSH");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+cudaError_t decode_partials_push(ecoserve_instance* inst, const CUtensorMap& wmap, const ActMaps& xm, int n_out, int K,
+                                 int B, int ep, int* splits_out) {
+  const int bn = B <= 64 ? 64 : 128;
+  const int splits = gemm_effective_splits(K, gemm_decode_splits(n_out, K, inst->num_sms));
+  GemmEpi ge = epi_base(inst);
+  ge.mode = EPI_SWAP_F32;
+  ge.out = tp_plane(inst, false, ep, inst->tp_rank);
+  ge.out2 = tp_plane(inst, true, ep, inst->tp_rank);
+  ge.ldo = n_out;
+  ge.indep = 1;
+  *splits_out = splits;
+  return gemm_launch_r(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, 1, splits, ge, inst->num_sms, inst->stream);
+}
+
 cudaError_t tp_push_rows(ecoserve_instance* inst, int ep, int splits, int rows, const bf16* gamma, bf16* h) {
   TpRowsArgs a;
   a.part = inst->part;
@@ -959,10 +986,11 @@ cudaError_t tp_push_rows(ecoserve_instance* inst, int ep, int splits, int rows, 
 
 // After the push GEMM of epoch `ep`: wait for the peer's push, x = (x + acc_0) + acc_1,
 // and the next RMSNorm (gamma null: x only).
-cudaError_t tp_allreduce(ecoserve_instance* inst, int ep, int rows, const bf16* gamma, bf16* h) {
+cudaError_t tp_allreduce(ecoserve_instance* inst, int ep, int rows, const bf16* gamma, bf16* h, int splits = 1) {
   TpAllreduceArgs a;
   a.recv0 = tp_plane(inst, false, ep, 0);
   a.recv1 = tp_plane(inst, false, ep, 1);
+  a.splits = splits;
   a.x = inst->x;
   a.gamma = gamma;
   a.h = h;
@@ -1255,8 +1283,14 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     if (inst->tp_fused) {  // partials -> fused push + all-reduce + residual + RMSNorm over NVLink (N2)
       const int ep = ++inst->tp_epoch;
       int sp = 1;
-      LAUNCH(P_GEMM_DECODE, 2.0 * H * M * D, 1, decode_partials(inst, w.o_a, inst->m_ao, H, M * D, B, &sp));
-      LAUNCH(P_OTHER, 0, 1, tp_push_rows(inst, ep, sp, B, w.ffn_norm, inst->h));
+      if (tp_decode_push_enabled() && 4 * B <= inst->tp_rows_max) {  // [splits <= 4][B][H] fits a plane
+        LAUNCH(P_GEMM_DECODE, 2.0 * H * M * D, 1,
+               decode_partials_push(inst, w.o_a, inst->m_ao, H, M * D, B, ep, &sp));
+        LAUNCH(P_OTHER, 0, 1, tp_allreduce(inst, ep, B, w.ffn_norm, inst->h, sp));
+      } else {
+        LAUNCH(P_GEMM_DECODE, 2.0 * H * M * D, 1, decode_partials(inst, w.o_a, inst->m_ao, H, M * D, B, &sp));
+        LAUNCH(P_OTHER, 0, 1, tp_push_rows(inst, ep, sp, B, w.ffn_norm, inst->h));
+      }
     } else {
       GemmEpi eo = resid_epi(inst);
       set_prefetch(inst, eo, 4 * l + 2, 2 * F, H, B);  // gate/up next
@@ -1278,10 +1312,15 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     if (inst->tp_fused) {
       const int ep = ++inst->tp_epoch;
       int sp = 1;
-      LAUNCH(P_GEMM_DECODE, 2.0 * H * F, 1, decode_partials(inst, w.d_a, inst->m_act, H, F, B, &sp));
-      LAUNCH(P_OTHER, 0, 1,
-             tp_push_rows(inst, ep, sp, B, last ? inst->final_norm : inst->lw[l + 1].attn_norm,
-                          last ? inst->hl : inst->h));
+      const bf16* g_next = last ? inst->final_norm : inst->lw[l + 1].attn_norm;
+      bf16* h_next = last ? inst->hl : inst->h;
+      if (tp_decode_push_enabled() && 4 * B <= inst->tp_rows_max) {  // [splits <= 4][B][H] fits a plane
+        LAUNCH(P_GEMM_DECODE, 2.0 * H * F, 1, decode_partials_push(inst, w.d_a, inst->m_act, H, F, B, ep, &sp));
+        LAUNCH(P_OTHER, 0, 1, tp_allreduce(inst, ep, B, g_next, h_next, sp));
+      } else {
+        LAUNCH(P_GEMM_DECODE, 2.0 * H * F, 1, decode_partials(inst, w.d_a, inst->m_act, H, F, B, &sp));
+        LAUNCH(P_OTHER, 0, 1, tp_push_rows(inst, ep, sp, B, g_next, h_next));
+      }
       fused = true;
     } else {
       GemmEpi ed = resid_epi(inst);

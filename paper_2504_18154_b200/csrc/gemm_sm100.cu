@@ -640,6 +640,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                              : reinterpret_cast<char*>(reinterpret_cast<float*>(epi.out) +
                                                        (int64_t)ks * n_rows * epi.ldo + m0);
           const int64_t gstride = silu ? epi.ldo * 2 : epi.ldo * 4;
+          // TP push (N2): the f32 partials also go to the peer's receive plane over NVLink
+          char* gbase2 = (!silu && epi.out2) ? reinterpret_cast<char*>(epi.out2 + (int64_t)ks * n_rows * epi.ldo + m0)
+                                             : nullptr;
           const uint32_t stg_base = smem_u32(staging);
           for (int h = 0; h < 2; ++h) {
             c0_ = clk();
@@ -688,6 +691,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               const int r = idx / vec_per_row, c = idx % vec_per_row;
               const uint4 val = lds128(stg_base + (uint32_t)(r * stg_row + c * 16));
               *reinterpret_cast<uint4*>(gbase + (int64_t)(n0 + r) * gstride + c * 16) = val;
+              if (gbase2) *reinterpret_cast<uint4*>(gbase2 + (int64_t)(n0 + r) * gstride + c * 16) = val;
             }
             c_out += clk() - c0_;
           }

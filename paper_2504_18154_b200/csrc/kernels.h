@@ -213,8 +213,9 @@ cudaError_t attn_decode_launch(const DecodeAttnArgs& a, int head_dim, cudaStream
 
 // ------------------------------------------------------------------ TP=2 fused all-reduce (N2)
 struct TpAllreduceArgs {
-  const float* recv0;      // rank 0's projection output [rows][H] f32 (this GPU's receive plane)
+  const float* recv0;      // rank 0's projection output [splits][rows][H] f32 (this GPU's receive plane)
   const float* recv1;      // rank 1's
+  int splits;              // split-K partials per rank, summed in split order (prefill: 1)
   float* x;                // residual [rows][H] f32, updated in place: x = (x + recv0) + recv1
   const bf16* gamma;       // next RMSNorm weight, or null (x only)
   bf16* h;                 // rmsnorm(x) * gamma [rows][H]

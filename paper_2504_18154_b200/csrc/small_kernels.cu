@@ -241,9 +241,15 @@ __global__ void __launch_bounds__(1024) tp_allreduce_norm_kernel(TpAllreduceArgs
     for (int j = 0; j < 4; ++j) {
       const int c = (threadIdx.x + j * blockDim.x) * 4;
       if (c < H) {
-        const int64_t off = (int64_t)row * H + c;
-        const float4 a0 = __ldcg(reinterpret_cast<const float4*>(a.recv0 + off));
-        const float4 a1 = __ldcg(reinterpret_cast<const float4*>(a.recv1 + off));
+        const int64_t off = (int64_t)row * H + c, plane = (int64_t)a.rows * H;
+        float4 a0 = __ldcg(reinterpret_cast<const float4*>(a.recv0 + off));
+        float4 a1 = __ldcg(reinterpret_cast<const float4*>(a.recv1 + off));
+        for (int sp = 1; sp < a.splits; ++sp) {  // split order, as the per-row path sums them
+          const float4 p0 = __ldcg(reinterpret_cast<const float4*>(a.recv0 + sp * plane + off));
+          const float4 p1 = __ldcg(reinterpret_cast<const float4*>(a.recv1 + sp * plane + off));
+          a0.x += p0.x; a0.y += p0.y; a0.z += p0.z; a0.w += p0.w;
+          a1.x += p1.x; a1.y += p1.y; a1.z += p1.z; a1.w += p1.w;
+        }
         float4 xv = *reinterpret_cast<const float4*>(a.x + off);
         xv.x = (xv.x + a0.x) + a1.x;
         xv.y = (xv.y + a0.y) + a1.y;

@@ -184,6 +184,27 @@ class Instance:
     def block_bytes(self) -> int:
         return self.lib.ecoserve_kv_pool_bytes(C.byref(self.cshape), 64, 1)
 
+    def export_kv(self, req_id: int, device) -> tuple:
+        """First half of a KV move: copy request `req_id`'s blocks into a staging
+        buffer on `device` (peer copy over NVLink) and release it here. Returns the
+        handle that `import_kv` of the destination instance takes (FuDG hand-off,
+        SURVEY 8(f) N4(i); the destination may import from its own thread)."""
+        st = L.ReqState()
+        _, reqs = self.status()
+        info = next(r for r in reqs if r["req_id"] == req_id)
+        stage = torch.empty(max(1, info["n_blocks"]) * self.block_bytes, dtype=torch.uint8, device=device)
+        prompt = np.zeros(info["prompt_len"], dtype=np.int32)
+        L.check(self.lib.ecoserve_kv_export(self.h, int(req_id), C.c_void_p(stage.data_ptr()), stage.numel(),
+                                            prompt.ctypes.data_as(L.PI32), len(prompt), C.byref(st)), self.h)
+        self.release([req_id])
+        return st, prompt, stage
+
+    def import_kv(self, handle: tuple) -> None:
+        """Second half of a KV move (see export_kv): place the staged blocks in this pool."""
+        st, prompt, stage = handle
+        L.check(self.lib.ecoserve_kv_import(self.h, C.byref(st), prompt.ctypes.data_as(L.PI32),
+                                            C.c_void_p(stage.data_ptr())), self.h)
+
     def migrate_to(self, other: "Instance", req_id: int) -> dict:
         """Move a running request with its paged KV to `other` (any GPU): export
         into a staging buffer on the destination device (peer copy over NVLink),

@@ -23,6 +23,14 @@ prefill-priority loop: every arrival is routed immediately, round-robin, with no
 constraint check and no deferral, so every instance interleaves prefills into
 its decode stream (no rolling activation).
 
+policy="fudg" is the fully disaggregated baseline (DistServe-style FuDG, P:321-354;
+SURVEY 8(f) N4(i)) on the same kernels: the first `fudg_prefill` instances only
+prefill (arrivals round-robin over them), every prefilled request's paged KV is
+exported over NVLink into a staging buffer on a decode instance (round-robin over
+the others), which imports it on its own thread and only decodes. The KV transfer
+the paper's PaDG avoids is on the critical path between the first token and the
+first decode step (it counts as switch wait).
+
 policy="sarathi" is the NoDG hybrid-batching baseline (Sarathi-Serve):
 round-robin routing, and every worker iteration is ONE forward pass
 (Instance.hybrid_step) that decodes every running request by one token and fills
@@ -73,9 +81,13 @@ class Clock:
 
 class Worker(threading.Thread):
     def __init__(self, idx: int, inst, clock: Clock, status_q: "queue.Queue", token_budget: int,
-                 decode_steps_per_poll: int = 1, max_batch: int = 256, hybrid_budget: int = 0):
+                 decode_steps_per_poll: int = 1, max_batch: int = 256, hybrid_budget: int = 0,
+                 role: str = "both", handoff=None):
         super().__init__(daemon=True)
         self.hybrid_budget = hybrid_budget   # > 0: Sarathi-style hybrid iterations
+        self.role = role                     # "both" | "prefill" | "decode" (FuDG)
+        self.handoff = handoff               # FuDG prefill role: () -> the decode Worker for the next request
+        self.imports: deque = deque()        # FuDG decode role: (req, kv handle) waiting for blocks
         self.idx, self.inst, self.clock = idx, inst, clock
         self.inbox: "queue.Queue" = queue.Queue()
         self.status_q = status_q
@@ -126,6 +138,8 @@ class Worker(threading.Thread):
         try:
             if self.hybrid_budget > 0:
                 self._loop_hybrid()
+            elif self.role == "decode":
+                self._loop_decode_only()
             else:
                 self._loop()
         except BaseException as e:  # surfaced by the server
@@ -207,6 +221,11 @@ class Worker(threading.Thread):
                     if r.G <= 1:
                         r.t_decode_begin_ns = r.t_done_ns = t
                         fin.append(r)
+                    elif self.role == "prefill":  # FuDG: the KV moves to a decode instance
+                        dst = self.handoff()
+                        handle = self.inst.export_kv(r.req_id, dst.inst.device)
+                        self.commit_sum -= self.committed.pop(r.req_id, 0)
+                        dst.inbox.put((r, handle))
                     else:
                         self.waiting.append(r)
                 self._finish(fin)
@@ -243,6 +262,47 @@ class Worker(threading.Thread):
             else:
                 self._drain_inbox(block=True)
 
+    def _loop_decode_only(self):
+        """FuDG decode instance: imports handed-off requests (KV already prefilled on a
+        prefill instance) as blocks allow, and runs decode steps over its running set."""
+        self.phase = DECODE
+        while not self.stop_flag.is_set():
+            try:
+                while True:
+                    self.imports.append(self.inbox.get_nowait())
+            except queue.Empty:
+                pass
+            while self.imports and len(self.running) < self.max_batch and self._fits(self.imports[0][0]):
+                r, handle = self.imports.popleft()
+                self.inst.import_kv(handle)
+                self._commit(r)
+                r.t_decode_begin_ns = self.clock.now()
+                self.running.append(r)
+            if not self.running:
+                try:
+                    self.imports.append(self.inbox.get(timeout=0.002))
+                except queue.Empty:
+                    pass
+                continue
+            t0 = self.clock.now()
+            toks, _ = self.inst.decode([r.req_id for r in self.running], self.k)
+            t = self.clock.now()
+            self.timeline.append((t0, t, "decode", len(self.running)))
+            fin, keep = [], []
+            for i, r in enumerate(self.running):
+                for s_ in range(self.k):
+                    if toks[i, s_] >= 0:
+                        r.tokens.append(int(toks[i, s_]))
+                        r.n_gen += 1
+                if r.n_gen >= r.G:
+                    r.t_done_ns = t
+                    fin.append(r)
+                else:
+                    keep.append(r)
+            self.running = keep
+            self._finish(fin)
+            self.push_status(fin)
+
     def _finish(self, fin):
         if fin:
             self.inst.release([r.req_id for r in fin])
@@ -276,16 +336,34 @@ class PaDGServer:
 
     def __init__(self, instances: Sequence, slo_ttft_ns: int, slo_tpot_ns: int, reserve_tokens: int,
                  predictor_table=None, token_budget: int = 16384, decode_steps_per_poll: int = 1,
-                 probe_printed: bool = False, policy: str = "padg", chunk_budget: int = 1024):
-        if policy not in ("padg", "nodg", "sarathi"):
+                 probe_printed: bool = False, policy: str = "padg", chunk_budget: int = 1024,
+                 fudg_prefill: int = 0):
+        if policy not in ("padg", "nodg", "sarathi", "fudg"):
             raise ValueError(f"unknown policy {policy!r}")
         self.policy = policy
         self._rr = 0
         self.clock = Clock()
         self.status_q: "queue.Queue" = queue.Queue()
         hb = chunk_budget if policy == "sarathi" else 0
+        n = len(instances)
+        self.n_prefill = n
+        roles = ["both"] * n
+        if policy == "fudg":
+            if n < 2:
+                raise ValueError("fudg needs >= 2 instances (prefill and decode roles)")
+            self.n_prefill = fudg_prefill if 0 < fudg_prefill < n else n // 2
+            roles = ["prefill"] * self.n_prefill + ["decode"] * (n - self.n_prefill)
+        self._rr_dec = 0
+
+        def handoff():
+            dec = self.workers[self.n_prefill:]
+            w = dec[self._rr_dec % len(dec)]
+            self._rr_dec += 1
+            return w
+
         self.workers = [Worker(i, inst, self.clock, self.status_q, token_budget, decode_steps_per_poll,
-                               hybrid_budget=hb) for i, inst in enumerate(instances)]
+                               hybrid_budget=hb, role=roles[i], handoff=handoff)
+                        for i, inst in enumerate(instances)]
         blocks = [inst.num_blocks for inst in instances]
         self.macro = MacroScheduler(SchedConfig(len(instances), slo_ttft_ns, slo_tpot_ns, reserve_tokens, blocks,
                                                 probe_printed=probe_printed, table=predictor_table))
@@ -326,8 +404,8 @@ class PaDGServer:
             now = self.clock.now()
             while pending and pending[0].arrival_ns <= now:
                 lr = pending.popleft()
-                if self.policy != "padg":  # immediate round-robin dispatch (NoDG baselines)
-                    i, self._rr = self._rr, (self._rr + 1) % len(self.workers)
+                if self.policy != "padg":  # immediate round-robin dispatch (NoDG / FuDG prefill instances)
+                    i, self._rr = self._rr, (self._rr + 1) % self.n_prefill
                     self._send(lr, i)
                     continue
                 i, _ = self.macro.route(lr.req_id, lr.arrival_ns, lr.S, now)

@@ -124,7 +124,7 @@ def test_nodg_policy_round_robin_no_deferral(S):
     assert [r.inst for r in by_arrival] == [i % 3 for i in range(len(by_arrival))]
     assert sorted(order) == sorted(r.inst for r in out.values())
     with pytest.raises(ValueError):
-        S.PaDGServer(insts, 1, 1, 1, policy="fudg")
+        S.PaDGServer(insts, 1, 1, 1, policy="tdpipe")
 
 
 def test_sarathi_policy_hybrid_iterations(S):
@@ -180,3 +180,41 @@ def test_worker_prefers_prefill_after_decode_step(S):
     i = seq.index("prefill", 1)
     assert seq[:i] == ["prefill"] + ["decode"] * (i - 1) and i > 1
     assert out[1].t_first_ns < out[0].t_done_ns
+
+
+class FakeKVInstance(FakeInstance):
+    """+ export_kv / import_kv (FuDG hand-off) with a per-request generation counter."""
+
+    device = "cpu"
+
+    def export_kv(self, rid, device):
+        state = self.gen.pop(rid)
+        self.calls.append(("export", 1))
+        return (rid, state)
+
+    def import_kv(self, handle):
+        rid, state = handle
+        assert rid not in self.gen
+        self.gen[rid] = state
+        self.calls.append(("import", 1))
+
+
+def test_fudg_prefill_and_decode_roles(S):
+    """FuDG baseline: prefill instances only prefill and hand every request's KV to a
+    decode instance, which only decodes; every request completes with G tokens."""
+    from paper_2504_18154_b200.serve import PaDGServer
+    insts = [FakeKVInstance() for _ in range(3)]
+    trace = make_trace("sharegpt", 40, seed=5, rate_per_s=200.0, vocab=1000)
+    for r in trace:
+        r.output_len = min(r.output_len, 24)
+    srv = PaDGServer(insts, 5 * SEC, SEC // 10, reserve_tokens=64, policy="fudg", fudg_prefill=1)
+    out = srv.run(trace, timeout_s=60)
+    assert all(r.t_done_ns >= 0 and len(r.tokens) == r.G for r in out.values())
+    assert {k for k, *_ in insts[0].calls} <= {"prefill", "export"}
+    for d in insts[1:]:
+        assert {k for k, *_ in d.calls} <= {"import", "decode"}
+    n_multi = sum(1 for r in out.values() if r.G > 1)
+    assert sum(1 for c in insts[0].calls if c[0] == "export") == n_multi
+    assert sum(sum(1 for c in d.calls if c[0] == "import") for d in insts[1:]) == n_multi
+    for r in out.values():
+        assert r.t_first_ns <= r.t_decode_begin_ns <= r.t_done_ns
