@@ -939,12 +939,14 @@ cudaError_t decode_partials(ecoserve_instance* inst, const CUtensorMap& wmap, co
 // Decode O / down projection of a TP rank whose bulk f32 epilogue writes its split
 // partials [splits][B][H] both to this GPU's receive plane and, over NVLink, to the
 // peer's; tp_allreduce then sums both ranks' partials locally (same order and bits as
-// the per-row push). ECOSERVE_TP_DECODE_PUSH=0: per-row push (tp_push_rows).
+// the per-row push). Measured slower than the per-row push (70B TP=2 decode 26.0 vs
+// 25.0 ms/step: the remote stores stretch the GEMM's tail), so ECOSERVE_TP_DECODE_PUSH=1
+// opts in.
 bool tp_decode_push_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("ECOSERVE_TP_DECODE_PUSH");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
 }
