@@ -51,6 +51,7 @@ import numpy as np
 from .macro import MacroScheduler, SchedConfig
 
 IDLE, PREFILL, DECODE = 0, 1, 2
+FUDG_BACKLOG = 64  # staged (exported, not yet imported) requests per FuDG decode instance
 
 
 @dataclass
@@ -88,6 +89,7 @@ class Worker(threading.Thread):
         self.role = role                     # "both" | "prefill" | "decode" (FuDG)
         self.handoff = handoff               # FuDG prefill role: () -> the decode Worker for the next request
         self.imports: deque = deque()        # FuDG decode role: (req, kv handle) waiting for blocks
+        self.decode_full = lambda: False     # FuDG prefill role: set by the server
         self.idx, self.inst, self.clock = idx, inst, clock
         self.inbox: "queue.Queue" = queue.Queue()
         self.status_q = status_q
@@ -197,9 +199,18 @@ class Worker(threading.Thread):
             self._finish(fin)
             self.push_status(fin)
 
+    def backlog(self) -> int:
+        """FuDG decode role: handed-off requests not yet imported (their KV sits in staging)."""
+        return len(self.imports) + self.inbox.qsize()
+
     def _loop(self):
         while not self.stop_flag.is_set():
             self._drain_inbox(block=False)
+            if self.role == "prefill" and self.decode_full():
+                # back-pressure: the decode instances have FUDG_BACKLOG staged requests each
+                # (their KV waits in staging buffers on the decode GPUs); prefill again later
+                self._drain_inbox(block=True)
+                continue
             if self.pending and self._fits(self.pending[0]):
                 if self.phase != PREFILL:
                     self.phase, self.t_switch = PREFILL, self.clock.now()
@@ -364,6 +375,12 @@ class PaDGServer:
         self.workers = [Worker(i, inst, self.clock, self.status_q, token_budget, decode_steps_per_poll,
                                hybrid_budget=hb, role=roles[i], handoff=handoff)
                         for i, inst in enumerate(instances)]
+        if policy == "fudg":
+            def decode_full():
+                dec = self.workers[self.n_prefill:]
+                return sum(w.backlog() for w in dec) >= FUDG_BACKLOG * len(dec)
+            for w in self.workers[:self.n_prefill]:
+                w.decode_full = decode_full
         blocks = [inst.num_blocks for inst in instances]
         self.macro = MacroScheduler(SchedConfig(len(instances), slo_ttft_ns, slo_tpot_ns, reserve_tokens, blocks,
                                                 probe_printed=probe_printed, table=predictor_table))
