@@ -233,9 +233,13 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a, cons
   bf16* sV = sK + DEC_STAGES * 64 * D;
   bf16* sQ = sV + DEC_STAGES * 64 * D;                     // [16][D]
   uint64_t* full = reinterpret_cast<uint64_t*>(sQ + 16 * D);  // [STAGES] (TMA)
+  uint64_t* empty = full + DEC_STAGES;                         // [STAGES]: the 4 warps consumed the stage
   float* red = reinterpret_cast<float*>(sm);               // reused after the main loop
   if (TMA && threadIdx.x == 0) {
-    for (int s = 0; s < DEC_STAGES; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < DEC_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
     fence_barrier_init();
     tma_prefetch(&kvmap);
   }
@@ -309,6 +313,9 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a, cons
     const int it = blk - blk0;
     {
       const int nb = blk + DEC_STAGES - 1;
+      // TMA: the stage was read in iteration it - 1; wait until all 4 warps released it
+      // (per-stage empty barrier instead of a CTA-wide barrier every block)
+      if (TMA && tid == 0 && nb < blk1 && it >= 1) mbar_wait(&empty[(it - 1) % DEC_STAGES], ((it - 1) / DEC_STAGES) & 1);
       if (nb < blk1) issue(nb, (it + DEC_STAGES - 1) % DEC_STAGES);
       if (!TMA) cp_async_commit();
     }
@@ -377,7 +384,12 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a, cons
       mma_bf16_16816(o[dn], af, b0, b1);
       mma_bf16_16816(o[dn + 1], af, b2, b3);
     }
-    __syncthreads();
+    if constexpr (TMA) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    } else {
+      __syncthreads();
+    }
   }
   if (!TMA) cp_async_wait<0>();
   __syncthreads();

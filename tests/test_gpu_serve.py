@@ -46,3 +46,30 @@ def test_live_macro_on_gpu_matches_oracle():
         assert a["ok"] == b.ok and a["ttft_ns"] == b.ttft_ns
     for i in insts:
         i.close()
+
+
+def test_fudg_on_gpu_same_tokens_as_padg():
+    """FuDG baseline (prefill-only + decode-only instance, KV moved by export/import):
+    every request completes and its greedy tokens equal those PaDG serves for the same
+    trace -- the KV hand-off is bit-exact and a token's GEMM / attention arithmetic does
+    not depend on its batch."""
+    from paper_2504_18154_b200.instance import Instance, device_weights_from_host
+    from paper_2504_18154_b200.serve import PaDGServer
+    shape = get_shape("tiny-gqa")
+    w = make_weights(shape, seed=0)
+    dw = device_weights_from_host(w, "cuda:0")
+    insts = [Instance(shape, dw, 256, 0, token_budget=2048, max_batch=64, max_positions=2048) for _ in range(2)]
+    trace = make_trace("tiny", 24, seed=11, rate_per_s=300.0, vocab=shape.vocab)
+    got = {}
+    for policy in ("padg", "fudg"):
+        srv = PaDGServer(insts, slo_ttft_ns=10 ** 10, slo_tpot_ns=10 ** 9, reserve_tokens=16, token_budget=2048,
+                         policy=policy)
+        out = srv.run(trace, timeout_s=120)
+        assert all(r.t_done_ns >= 0 and len(r.tokens) == r.G for r in out.values())
+        got[policy] = {rid: list(r.tokens) for rid, r in out.items()}
+        for i in insts:
+            _, rs = i.status()
+            assert not rs, "every request released"
+    assert got["padg"] == got["fudg"]
+    for i in insts:
+        i.close()
