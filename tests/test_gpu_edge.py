@@ -70,3 +70,20 @@ def test_decode_batch_sizes(setup, B):
         assert tokens_match(model, prompts[i], [first[i]] + list(toks[i])) >= 1
     inst.release([5000 + i for i in range(B)])
     assert inst.status()[0]["blocks_used"] == 0
+
+
+@pytest.mark.parametrize("env", ["ECOSERVE_CHAIN=1", "ECOSERVE_DEC_VARIANT=4", "ECOSERVE_PAIR_TILES=1",
+                                 "ECOSERVE_ATTN_STAGES=2", "ECOSERVE_PDL=0"])
+@pytest.mark.parametrize("shape", ["tiny", "tiny-d128"])
+def test_opt_in_decode_variants_match_oracle(env, shape):
+    """The opt-in decode variants keep the per-layer A19 bar:
+    decode hidden states, teacher-forced on the GPU's own tokens, within 1e-2 of the
+    oracle over 3 decode steps (fresh process: the switches are read once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    k, v = env.split("=")
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "chain_diag.py"), shape, "3", "1e-2"],
+                       env={**os.environ, k: v}, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

@@ -33,6 +33,7 @@ def main():
         kv, out = model.prefill(list(r.prompt))
         state[r.req_id] = [kv, int(first[i]), r.prompt_len]
     ids = [r.req_id for r in reqs]
+    worst_all = 0.0
     for s in range(steps):
         toks, _ = inst.decode(ids, 1)
         worst = np.zeros(shape.n_layers + 1)
@@ -45,7 +46,12 @@ def main():
                 worst[l] = max(worst[l], float(np.max(np.abs(got - ref)) / np.max(np.abs(ref))))
             state[rid] = [kv, int(toks[i, 0]), pos + 1]
         print(f"step {s}: worst per-layer rel err {np.array2string(worst, precision=4)}", flush=True)
+        worst_all = max(worst_all, float(worst.max()))
+    inst.close()
+    print(f"WORST {worst_all:.6f}", flush=True)
+    return worst_all
 
 
 if __name__ == "__main__":
-    main()
+    tol = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-2
+    sys.exit(0 if main() <= tol else 1)
