@@ -849,14 +849,57 @@ bool pair_tiles_enabled() {
   return v == 1;
 }
 
+// ECOSERVE_DEC_R2=1: every decode projection streams two 128-row weight tiles per work
+// unit behind one activation tile (256-row weight box). The TMA probe
+// (profiles/r01_tma_stream_probe.jsonl) caps one SM's TMA streaming at ~94 GB/s; with
+// one weight and one activation tile per stage only half of it is weights, with two
+// weight tiles two thirds. Splits are re-chosen for 256-row units (up to 8).
+bool dec_r2_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_DEC_R2");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+int decode_splits_r2(int n_out, int K, int num_sms) {
+  const int units = (n_out + 255) / 256;
+  if (4 * units >= 3 * num_sms) return 1;
+  const int kb_total = (K + 63) / 64;
+  int best = 1;
+  double best_cost = 1e30;
+  for (int s = 1; s <= 8; ++s) {
+    const int eff = gemm_effective_splits(K, s);
+    if (eff != s) continue;
+    const int kb_per = (kb_total + eff - 1) / eff;
+    const int waves = (units * eff + num_sms - 1) / num_sms;
+    const double cost = (double)waves * kb_per * 2 + (eff > 1 ? 0.5 * eff : 0.0);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = eff;
+    }
+  }
+  return best;
+}
+
 cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const ActMaps& xm, int n_out, int K, int B,
                         int mode, GemmEpi e, int* nk, const bf16* norm_gamma = nullptr, bf16* norm_out = nullptr,
                         bool* fused = nullptr, const CUtensorMap* wmap256 = nullptr) {
   const int bn = B <= 64 ? 64 : 128;  // B > 128: several 128-token tiles; weight re-reads hit L2
-  const int splits = gemm_decode_splits(n_out, K, inst->num_sms);
-  const int var = decode_variant();
+  const bool r2 = wmap256 && dec_r2_enabled() && (B + bn - 1) / bn == 1 && n_out >= 256;
+  const int splits = r2 ? decode_splits_r2(n_out, K, inst->num_sms) : gemm_decode_splits(n_out, K, inst->num_sms);
+  const CUtensorMap* wm = r2 ? wmap256 : &wmap;
+  const int rr = r2 ? 2 : decode_variant();
+  const int var = rr;
   if (fused) *fused = false;
   e.indep = 1;  // weights (A) prefetch before the PDL wait
+  if (r2) e.pf_map = nullptr;  // (the L2 prefetch assumes 128-row units)
+  if (splits == 1 && r2) {
+    e.mode = mode;
+    *nk = 1;
+    return gemm_launch_r(wm, &xm.b[bn_index(bn)], n_out, B, K, bn, 2, 1, e, inst->num_sms, inst->stream);
+  }
   if (splits == 1) {  // epilogue in the GEMM
     e.mode = mode;
     *nk = 1;
@@ -888,7 +931,7 @@ cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const 
   ge.out = inst->part;
   ge.ldo = n_out;
   cudaError_t r =
-      gemm_launch_r(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, var, splits, ge, inst->num_sms, inst->stream);
+      gemm_launch_r(wm, &xm.b[bn_index(bn)], n_out, B, K, bn, var, splits, ge, inst->num_sms, inst->stream);
   if (r != cudaSuccess) return r;
   if (norm_gamma && mode == EPI_SWAP_RESID && n_out == inst->H) {
     *nk = 2;
@@ -1176,7 +1219,8 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
       e.v_cache = v_layer(inst, 0);
       int nk = 0;
       LAUNCH(P_GEMM_DECODE, 2.0 * inst->QKV * H, nk,
-             decode_gemm(inst, inst->lw[0].qkv_a, inst->m_h, inst->QKV, H, B, EPI_SWAP_QKV, e, &nk));
+             decode_gemm(inst, inst->lw[0].qkv_a, inst->m_h, inst->QKV, H, B, EPI_SWAP_QKV, e, &nk, nullptr, nullptr,
+                         nullptr, &inst->lw[0].qkv_b));
     }
     ChainCall cc;
     cc.n_tok = B;
@@ -1259,7 +1303,8 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     e.v_cache = v_layer(inst, l);
     int nk = 0;
     LAUNCH(P_GEMM_DECODE, 2.0 * inst->QKV * H, nk,
-           decode_gemm(inst, w.qkv_a, inst->m_h, inst->QKV, H, B, EPI_SWAP_QKV, e, &nk));
+           decode_gemm(inst, w.qkv_a, inst->m_h, inst->QKV, H, B, EPI_SWAP_QKV, e, &nk, nullptr, nullptr, nullptr,
+                       &w.qkv_b));
     DecodeAttnArgs a;
     a.q = inst->q;
     a.k_cache = k_layer(inst, l);
@@ -1298,7 +1343,7 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
       set_prefetch(inst, eo, 4 * l + 2, 2 * F, H, B);  // gate/up next
       LAUNCH(P_GEMM_DECODE, 2.0 * H * M * D, nk,
              decode_gemm(inst, w.o_a, inst->m_ao, H, M * D, B, resid_mode_decode(inst), eo, &nk,
-                         can_fuse ? w.ffn_norm : nullptr, inst->h, &fused));
+                         can_fuse ? w.ffn_norm : nullptr, inst->h, &fused, &w.o_b));
       ALLREDUCE_X(B);
       if (!fused) LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, B, H, eps, st));
     }
@@ -1330,7 +1375,7 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
       LAUNCH(P_GEMM_DECODE, 2.0 * H * F, nk,
              decode_gemm(inst, w.d_a, inst->m_act, H, F, B, resid_mode_decode(inst), ed, &nk,
                          can_fuse ? (last ? inst->final_norm : inst->lw[l + 1].attn_norm) : nullptr,
-                         last ? inst->hl : inst->h, &fused));
+                         last ? inst->hl : inst->h, &fused, &w.d_b));
       ALLREDUCE_X(B);
     }
     h_ready = fused && !last;

@@ -117,7 +117,7 @@ int main() {
   }
   const int mt = N / 128, kb = K / 64;
   const double gb = (double)N * K * 2 / 1e9;
-  for (int grid : {148, 296}) {
+  for (int grid : {38, 76, 112, 148, 296}) {  // fewer CTAs: the per-SM streaming cap
     printf("{\"grid\": %d, \"rowmajor_s6\": %.1f, \"tiled_s6\": %.1f, \"rowmajor_s12\": %.1f, \"tiled_s12\": %.1f}\n", grid,
            gb / run<6, false>(m2, mt, kb, grid, sink) * 1e3, gb / run<6, true>(m4, mt, kb, grid, sink) * 1e3,
            gb / run<12, false>(m2, mt, kb, grid, sink) * 1e3, gb / run<12, true>(m4, mt, kb, grid, sink) * 1e3);
