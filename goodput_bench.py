@@ -88,6 +88,9 @@ def main():
             r.output_len = min(r.output_len, args.max_out)
             r.req_id += rid0[0]
         rid0[0] += n_req
+        for i, inst in enumerate(insts):  # the previous probe released everything it left behind
+            st, _ = inst.status()
+            assert st["alive"] and st["n_requests"] == 0, f"instance {i} not empty before the probe: {st}"
         srv = PaDGServer(insts, slo_ttft, slo_tpot, reserve_tokens=237, predictor_table=(lens, ns),
                          policy=args.policy, chunk_budget=args.chunk_budget, fudg_prefill=args.fudg_prefill)
         t0 = time.perf_counter()

@@ -37,7 +37,10 @@ typedef enum {
   ECOSERVE_ERR_STATE = 3,        /* unknown or duplicate req_id, decode before prefill, dead instance */
   ECOSERVE_ERR_UNSUPPORTED = 4,  /* shape/feature this build does not implement */
   ECOSERVE_ERR_CUDA = 5,         /* sticky CUDA error */
-  ECOSERVE_ERR_NCCL = 6
+  ECOSERVE_ERR_NCCL = 6,
+  ECOSERVE_ERR_NUMERIC = 7       /* NaN logits (reading A6: greedy sampling of NaN is an error);
+                                    sticky like CUDA errors: the instance is marked dead, since
+                                    its weights or KV can no longer be trusted */
 } ecoserve_status;
 
 /* Model shape, Table 1 notation: L, H, M, D plus the GQA

@@ -12,8 +12,9 @@ import os
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libecoserve.so")
 
-OK, ERR_INVALID_ARG, ERR_KV_EXHAUSTED, ERR_STATE, ERR_UNSUPPORTED, ERR_CUDA, ERR_NCCL = range(7)
-STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "KV_EXHAUSTED", 3: "STATE", 4: "UNSUPPORTED", 5: "CUDA", 6: "NCCL"}
+OK, ERR_INVALID_ARG, ERR_KV_EXHAUSTED, ERR_STATE, ERR_UNSUPPORTED, ERR_CUDA, ERR_NCCL, ERR_NUMERIC = range(8)
+STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "KV_EXHAUSTED", 3: "STATE", 4: "UNSUPPORTED", 5: "CUDA", 6: "NCCL",
+                7: "NUMERIC"}
 
 
 class EcoError(RuntimeError):

@@ -133,6 +133,9 @@ struct ecoserve_instance {
   // fused TP all-reduce over NVLink peer memory (N2): receive rows / flags written by the peer
   bool tp_fused = false;
   int tp_rows_max = 0, tp_epoch = 0;
+  int* tp_err = nullptr;         // device flag: a TP exchange wait timed out (peer gone)
+  int* h_tp_err = nullptr;       // pinned copy, read after every step
+  unsigned long long tp_timeout_ns = 0;
   float* tp_recv = nullptr;      // [2 parity][2 rank][tp_rows_max][H]: both ranks' O / down outputs
   int* tp_flags = nullptr;       // [0]: epoch of the peer's last GEMM push; [64 + par * rows_max + row]: decode row flags
   float* peer_recv = nullptr;    // the peer's tp_recv / tp_flags (peer pointer or IPC mapping)
@@ -174,7 +177,6 @@ struct ecoserve_instance {
   int* am_idx = nullptr;
   int am_ld = 0;
   int* d_tokens = nullptr;
-  int* d_nan = nullptr;
   float *rope_cos = nullptr, *rope_sin = nullptr;
   int* d_meta = nullptr;
   int* h_meta = nullptr;         // pinned
@@ -379,12 +381,14 @@ void ecoserve_instance_destroy(ecoserve_instance* inst) {
   if (inst->stream) cudaStreamSynchronize(inst->stream);
   void* dev[] = {inst->x, inst->h, inst->q, inst->ao, inst->act, inst->hl, inst->part, inst->counters, inst->attn_ws,
                  inst->am_val,
-                 inst->am_idx, inst->d_tokens, inst->d_nan, inst->rope_cos, inst->rope_sin, inst->d_meta, inst->dbg};
+                 inst->am_idx, inst->d_tokens, inst->rope_cos, inst->rope_sin, inst->d_meta, inst->dbg};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (inst->h_meta) cudaFreeHost(inst->h_meta);
   if (inst->h_tokens) cudaFreeHost(inst->h_tokens);
   if (inst->h_chain_err) cudaFreeHost(inst->h_chain_err);
+  if (inst->h_tp_err) cudaFreeHost(inst->h_tp_err);
+  if (inst->tp_err) cudaFree(inst->tp_err);
   for (cudaEvent_t e : inst->prof.pool) cudaEventDestroy(e);
   if (inst->peer_ipc) {
     if (inst->peer_recv) cudaIpcCloseMemHandle(inst->peer_recv);
@@ -562,7 +566,6 @@ ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, cons
   CK(cudaMalloc(&inst->am_val, sizeof(float) * (int64_t)inst->B_max * inst->am_ld));
   CK(cudaMalloc(&inst->am_idx, sizeof(int) * (int64_t)inst->B_max * inst->am_ld));
   CK(cudaMalloc(&inst->d_tokens, sizeof(int) * inst->B_max));
-  CK(cudaMalloc(&inst->d_nan, sizeof(int)));
   inst->meta_cap = 6LL * T + 4 + (int64_t)inst->B_max * (max_blocks_seq + 8) + 2LL * (T / 64 + inst->B_max);
   CK(cudaMalloc(&inst->d_meta, sizeof(int) * inst->meta_cap));
   CK(cudaMallocHost(&inst->h_meta, sizeof(int) * inst->meta_cap));
@@ -597,6 +600,14 @@ ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, cons
     if (tp_fused_enabled()) {
       const ecoserve_status es = tp_setup_peer(inst);
       if (es != ECOSERVE_OK) return es;
+      // bound on one exchange wait (the peer may legitimately be a whole prefill GEMM
+      // or a host-side hiccup behind); ECOSERVE_TP_TIMEOUT_MS overrides
+      const char* e = getenv("ECOSERVE_TP_TIMEOUT_MS");
+      inst->tp_timeout_ns = 1000000ull * (unsigned long long)(e ? std::max(1, atoi(e)) : 30000);
+      CK(cudaMalloc(&inst->tp_err, sizeof(int)));
+      CK(cudaMemset(inst->tp_err, 0, sizeof(int)));
+      CK(cudaMallocHost(&inst->h_tp_err, sizeof(int)));
+      *inst->h_tp_err = 0;
     }
   }
   if (inst->tp == 1) {
@@ -1026,6 +1037,8 @@ cudaError_t tp_push_rows(ecoserve_instance* inst, int ep, int splits, int rows, 
   a.my_recv = tp_plane(inst, false, ep, 0);
   a.peer_flags = inst->peer_flags + 64 + (ep & 1) * inst->tp_rows_max;
   a.my_flags = inst->tp_flags + 64 + (ep & 1) * inst->tp_rows_max;
+  a.err = inst->tp_err;
+  a.timeout_ns = inst->tp_timeout_ns;
   return tp_push_rows_launch(a, inst->num_sms, inst->stream);
 }
 
@@ -1045,6 +1058,8 @@ cudaError_t tp_allreduce(ecoserve_instance* inst, int ep, int rows, const bf16* 
   a.epoch = ep;
   a.peer_flag = inst->peer_flags;
   a.my_flag = inst->tp_flags;
+  a.err = inst->tp_err;
+  a.timeout_ns = inst->tp_timeout_ns;
   return tp_allreduce_norm_launch(a, inst->num_sms, inst->stream);
 }
 
@@ -1087,7 +1102,7 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
   cudaStream_t st = inst->stream;
   const int L = inst->L, H = inst->H, M = inst->M, D = inst->D, F = inst->F;
   const float eps = inst->shape.rms_eps;
-  LAUNCH(P_OTHER, 0, 1, embed_launch(d_ids, inst->embed, inst->x, T, H, st));
+  LAUNCH(P_OTHER, 0, 1, embed_launch(d_ids, inst->embed, inst->x, T, H, inst->V, st));
   if (inst->debug) CK(cudaMemcpyAsync(inst->dbg, inst->x, sizeof(float) * (int64_t)T * H, cudaMemcpyDeviceToDevice, st));
   bool h_ready = false;  // the previous layer's fused TP all-reduce already wrote this layer's norm
   for (int l = 0; l < L; ++l) {
@@ -1200,7 +1215,7 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
   cudaStream_t st = inst->stream;
   const int L = inst->L, H = inst->H, M = inst->M, D = inst->D, F = inst->F;
   const float eps = inst->shape.rms_eps;
-  LAUNCH(P_OTHER, 0, 1, embed_launch(d_ids, inst->embed, inst->x, B, H, st));
+  LAUNCH(P_OTHER, 0, 1, embed_launch(d_ids, inst->embed, inst->x, B, H, inst->V, st));
   if (inst->debug) CK(cudaMemcpyAsync(inst->dbg, inst->x, sizeof(float) * (int64_t)B * H, cudaMemcpyDeviceToDevice, st));
   int bps = 1;
   int n_splits = decode_attn_splits(inst, B, max_blocks, &bps);
@@ -1406,7 +1421,32 @@ static ecoserve_status lm_head_argmax(ecoserve_instance* inst, const int* d_rows
   LAUNCH(gemm_cls, gemm_cls == P_GEMM_DECODE ? 2.0 * inst->V * H : 2.0 * inst->V * H * n, 1,
          gemm_launch(&inst->lm_a, &inst->m_hl.b[bn_index(bn)], inst->V, n, H, bn, 1, e, inst->num_sms, st));
   LAUNCH(P_OTHER, 0, 1,
-         argmax_reduce_launch(inst->am_val, inst->am_idx, n, inst->am_ld, inst->am_ld, inst->d_tokens, inst->d_nan, st));
+         argmax_reduce_launch(inst->am_val, inst->am_idx, n, inst->am_ld, inst->am_ld, inst->d_tokens, st));
+  return ECOSERVE_OK;
+}
+
+// Enqueued with the token copy-back: the TP exchange's timeout flag.
+static cudaError_t copy_step_flags(ecoserve_instance* inst) {
+  if (!inst->tp_err) return cudaSuccess;
+  return cudaMemcpyAsync(inst->h_tp_err, inst->tp_err, sizeof(int), cudaMemcpyDeviceToHost, inst->stream);
+}
+
+// After the step synchronised: a TP exchange that timed out (the peer stopped
+// mid-phase) and NaN rows, whose argmax is ECO_TOKEN_NAN (reading A6; feeding it back
+// would embed a garbage id), both mark the instance dead.
+static ecoserve_status check_tokens(ecoserve_instance* inst, int n) {
+  if (inst->h_tp_err && *inst->h_tp_err) {
+    inst->err = "TP=2 exchange: the peer rank's flag did not arrive within the timeout (peer failed or "
+                "stopped mid-phase); instance marked dead";
+    inst->dead = true;
+    return ECOSERVE_ERR_NCCL;
+  }
+  for (int i = 0; i < n; ++i)
+    if (inst->h_tokens[i] < 0 || inst->h_tokens[i] >= inst->V) {
+      inst->err = "NaN logits in LM-head row " + std::to_string(i) + " (reading A6); instance marked dead";
+      inst->dead = true;
+      return ECOSERVE_ERR_NUMERIC;
+    }
   return ECOSERVE_OK;
 }
 
@@ -1523,11 +1563,13 @@ ecoserve_status ecoserve_prefill_phase(ecoserve_instance* inst, const ecoserve_r
     if (s != ECOSERVE_OK) return s;
     inst->prof.end(pm, tok, st);
     CK(cudaMemcpyAsync(inst->h_tokens, inst->d_tokens, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
+    CK(copy_step_flags(inst));
     CK(cudaStreamSynchronize(st));
     inst->prof.resolve();
     inst->prof.tokens[0] += tok;
     inst->prof.h2d += sizeof(int) * used;
     inst->prof.d2h += sizeof(int) * ns;
+    if (ecoserve_status ts = check_tokens(inst, ns); ts != ECOSERVE_OK) return ts;
     for (int i = i0; i < i1; ++i) {
       Req* r = rs[i];
       r->last_token = inst->h_tokens[i - i0];
@@ -1734,12 +1776,14 @@ ecoserve_status ecoserve_hybrid_step(ecoserve_instance* inst, const ecoserve_chu
   }
   inst->prof.end(pm, T, st);
   if (nl > 0) CK(cudaMemcpyAsync(inst->h_tokens, inst->d_tokens, sizeof(int) * nl, cudaMemcpyDeviceToHost, st));
+  CK(copy_step_flags(inst));
   CK(cudaStreamSynchronize(st));
   inst->prof.resolve();
   inst->prof.tokens[0] += Tc;
   inst->prof.tokens[1] += n_decode;
   inst->prof.h2d += sizeof(int) * used;
   inst->prof.d2h += sizeof(int) * nl;
+  if (ecoserve_status ts = check_tokens(inst, nl); ts != ECOSERVE_OK) return ts;
   int li = 0;
   for (int i = 0; i < n_chunks; ++i) {
     Req* r = cs[i];
@@ -1770,7 +1814,13 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
   if (n > inst->B_max) return ECOSERVE_ERR_INVALID_ARG;
   CK(cudaSetDevice(inst->device));
   std::vector<Req*> rs(n);
+  std::unordered_map<int64_t, int> seen;
   for (int i = 0; i < n; ++i) {
+    if (seen.count(req_ids[i])) {  // two rows of one request would share a KV slot
+      inst->err = "duplicate req_id " + std::to_string(req_ids[i]) + " in the decode set";
+      return ECOSERVE_ERR_INVALID_ARG;
+    }
+    seen[req_ids[i]] = i;
     auto it = inst->reqs.find(req_ids[i]);
     if (it == inst->reqs.end() || it->second.n_gen < 1) {
       inst->err = "decode of unknown or unprefilled req_id " + std::to_string(req_ids[i]);
@@ -1847,6 +1897,7 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
     inst->prof.end(pm, B, st);
     CK(cudaMemcpyAsync(inst->h_tokens, inst->d_tokens, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
     if (inst->chain) CK(cudaMemcpyAsync(inst->h_chain_err, inst->chain_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(copy_step_flags(inst));
     const auto t_enq1 = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(st));
     if (inst->chain && *inst->h_chain_err) {
@@ -1865,6 +1916,7 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
     inst->prof.tokens[1] += B;
     inst->prof.h2d += sizeof(int) * used;
     inst->prof.d2h += sizeof(int) * B;
+    if (ecoserve_status ts = check_tokens(inst, B); ts != ECOSERVE_OK) return ts;
     for (int k = 0; k < B; ++k) {
       Req* r = rs[live[k]];
       r->last_token = inst->h_tokens[k];

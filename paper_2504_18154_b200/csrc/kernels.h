@@ -223,6 +223,8 @@ struct TpAllreduceArgs {
   int rows, H, epoch;
   int* peer_flag;          // the peer's flag (P2P): set to epoch once this rank's pushes are done
   const int* my_flag;      // set by the peer
+  int* err;                // set to 1 when the peer's flag did not arrive within timeout_ns
+  unsigned long long timeout_ns;
 };
 cudaError_t tp_allreduce_norm_launch(const TpAllreduceArgs& a, int num_sms, cudaStream_t s);
 // decode variant: sums this rank's split partials per row and pushes the row itself
@@ -239,11 +241,14 @@ struct TpRowsArgs {
   int* peer_flags;         // the peer's row flags of this parity [rows] (P2P)
   const float* my_recv;    // this rank's receive rows, written by the peer
   const int* my_flags;
+  int* err;                // as TpAllreduceArgs
+  unsigned long long timeout_ns;
 };
 cudaError_t tp_push_rows_launch(const TpRowsArgs& a, int num_sms, cudaStream_t s);
 
 // ------------------------------------------------------------------ small kernels
-cudaError_t embed_launch(const int* ids, const bf16* E, float* x, int n, int H, cudaStream_t s);
+// x[t] = E[clamp(ids[t], 0, V-1)] (fp32)
+cudaError_t embed_launch(const int* ids, const bf16* E, float* x, int n, int H, int V, cudaStream_t s);
 cudaError_t rmsnorm_launch(const float* x, int64_t ldx, const int* rows, const bf16* gamma, bf16* out, int n, int H,
                            float eps, cudaStream_t s);
 // dst[r] = src_sel[r][row[r]] (row copy of `cols` bf16), sel in {0,1,2} -> s0/s1/s2.
@@ -252,8 +257,11 @@ cudaError_t row_gather_launch(const bf16* s0, const bf16* s1, const bf16* s2, co
 // x[row] += sum_s part[s][row] (split order); out[row] = bf16(rmsnorm(x[row]) * gamma). part plane = rows x H.
 cudaError_t splitk_resid_rmsnorm_launch(const float* part, int splits, int rows, float* x, const bf16* gamma,
                                         bf16* out, int H, float eps, cudaStream_t s);
+// tokens[i] = argmax over the [n][parts] (val, idx) partials; NaN wins, and a NaN row
+// yields ECO_TOKEN_NAN (reading A6) instead of a token id.
+constexpr int ECO_TOKEN_NAN = -2;
 cudaError_t argmax_reduce_launch(const float* val, const int* idx, int n, int parts, int ld, int* tokens,
-                                 int* nan_flag, cudaStream_t s);
+                                 cudaStream_t s);
 // Decode epilogues (after a split-K swap GEMM): sum partial[split][row][col] in fixed split order, then
 enum RedMode : int { RED_BF16 = 0, RED_RESID = 1, RED_SILU = 2, RED_QKV = 3, RED_F32 = 4 };
 cudaError_t splitk_reduce_launch(int mode, const float* part, int splits, int rows, int cols, int64_t ld_part,

@@ -148,7 +148,7 @@ ecoserve_status ecoserve_op_lm_argmax(const void* W, const void* X, int32_t V, i
   e.am_idx = ws_idx;
   e.am_ld = parts;
   OPCK(gemm_launch(&ma, &mb, V, n, k, bn, 1, e, num_sms(), (cudaStream_t)stream));
-  OPCK(argmax_reduce_launch(ws_val, ws_idx, n, parts, parts, tokens, nullptr, (cudaStream_t)stream));
+  OPCK(argmax_reduce_launch(ws_val, ws_idx, n, parts, parts, tokens, (cudaStream_t)stream));
   return ECOSERVE_OK;
 }
 

@@ -12,11 +12,16 @@
 
 namespace eco {
 
-__global__ void embed_kernel(const int* __restrict__ ids, const bf16* __restrict__ E, float* __restrict__ x, int H) {
+__global__ void embed_kernel(const int* __restrict__ ids, const bf16* __restrict__ E, float* __restrict__ x, int H,
+                             int V) {
   pdl_trigger();
   pdl_wait();
   const int t = blockIdx.x;
-  const bf16* src = E + (int64_t)ids[t] * H;
+  // ids are range-checked on the host (prompts) or come from the argmax, whose NaN
+  // sentinel the host rejects before it is fed back; clamp anyway so a bad id can
+  // never read outside the table
+  const int id = min(max(ids[t], 0), V - 1);
+  const bf16* src = E + (int64_t)id * H;
   float* dst = x + (int64_t)t * H;
   for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8) {
     uint4 v = *reinterpret_cast<const uint4*>(src + i);
@@ -27,9 +32,9 @@ __global__ void embed_kernel(const int* __restrict__ ids, const bf16* __restrict
   }
 }
 
-cudaError_t embed_launch(const int* ids, const bf16* E, float* x, int n, int H, cudaStream_t s) {
+cudaError_t embed_launch(const int* ids, const bf16* E, float* x, int n, int H, int V, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  return launch_k(embed_kernel, dim3(n), dim3(128), 0, s, ids, E, x, H);
+  return launch_k(embed_kernel, dim3(n), dim3(128), 0, s, ids, E, x, H, V);
 }
 
 // out[i] = bf16( x[row_i] * rsqrt(mean(x[row_i]^2) + eps) * gamma ), row_i = rows ? rows[i] : i
@@ -96,46 +101,48 @@ cudaError_t row_gather_launch(const bf16* s0, const bf16* s1, const bf16* s2, co
 }
 
 // tokens[i] = argmax over parts of (val, idx): largest value, lowest index on ties.
+// One NaN rule with the LM-head epilogue (gemm_sm100.cu, EPI_SWAP_ARGMAX): a NaN
+// logit wins every comparison, and a row whose winner is NaN gets the token
+// ECO_TOKEN_NAN (reading A6: NaN logits are an error), which the host rejects.
+__device__ __forceinline__ bool am_better(float v, int x, float bv, int bi) {
+  if (isnan(v)) return !isnan(bv) || x < bi;
+  if (isnan(bv)) return false;
+  return v > bv || (v == bv && x < bi);
+}
+
 __global__ void argmax_reduce_kernel(const float* __restrict__ val, const int* __restrict__ idx, int parts, int ld,
-                                     int* __restrict__ tokens, int* __restrict__ nan_flag) {
+                                     int* __restrict__ tokens) {
   pdl_trigger();
   pdl_wait();
   const int i = blockIdx.x;
   float bv = -INFINITY;
   int bi = 0x7fffffff;
-  bool nan = false;
   for (int p = threadIdx.x; p < parts; p += blockDim.x) {
     const float v = val[(int64_t)i * ld + p];
     const int x = idx[(int64_t)i * ld + p];
-    if (isnan(v)) nan = true;
-    if (v > bv || (v == bv && x < bi)) { bv = v; bi = x; }
+    if (am_better(v, x, bv, bi)) { bv = v; bi = x; }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
     const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    if (am_better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
   }
   __shared__ float sv[32];
   __shared__ int si[32];
-  __shared__ int sn;
-  if (threadIdx.x == 0) sn = 0;
-  __syncthreads();
-  if (nan) atomicOr(&sn, 1);
   if ((threadIdx.x & 31) == 0) { sv[threadIdx.x >> 5] = bv; si[threadIdx.x >> 5] = bi; }
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x / 32); ++w)
-      if (sv[w] > bv || (sv[w] == bv && si[w] < bi)) { bv = sv[w]; bi = si[w]; }
-    tokens[i] = bi;
-    if (sn && nan_flag) atomicOr(nan_flag, 1);
+      if (am_better(sv[w], si[w], bv, bi)) { bv = sv[w]; bi = si[w]; }
+    tokens[i] = isnan(bv) ? ECO_TOKEN_NAN : bi;
   }
 }
 
-cudaError_t argmax_reduce_launch(const float* val, const int* idx, int n, int parts, int ld, int* tokens, int* nan_flag,
+cudaError_t argmax_reduce_launch(const float* val, const int* idx, int n, int parts, int ld, int* tokens,
                                  cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  return launch_k(argmax_reduce_kernel, dim3(n), dim3(128), 0, s, val, idx, parts, ld, tokens, nan_flag);
+  return launch_k(argmax_reduce_kernel, dim3(n), dim3(128), 0, s, val, idx, parts, ld, tokens);
 }
 
 // Decode O / down projection tail fused with the next RMSNorm: per row,
@@ -222,6 +229,32 @@ __device__ __forceinline__ int ld_acquire_sys(const int* p) {
   return v;
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Spin until *flag >= epoch (ge) or == epoch. Bounded: if the peer never signals (it
+// returned early on an error, so the epochs diverged) the wait gives up after
+// timeout_ns, sets *err and lets the kernel finish; the host reads err after the step,
+// marks the instance dead and reports it instead of hanging the GPU.
+__device__ __forceinline__ void tp_wait_flag(const int* flag, int epoch, bool ge, int* err,
+                                             unsigned long long timeout_ns) {
+  unsigned long long t0 = 0;
+  for (int it = 0;; ++it) {
+    const int v = ld_acquire_sys(flag);
+    if (ge ? v >= epoch : v == epoch) return;
+    if ((it & 255) == 0) {
+      const unsigned long long t = global_ns();
+      if (it == 0) t0 = t;
+      else if (t - t0 > timeout_ns) {
+        atomicExch(err, 1);
+        return;
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(1024) tp_allreduce_norm_kernel(TpAllreduceArgs a) {
   pdl_trigger();
   pdl_wait();
@@ -230,8 +263,7 @@ __global__ void __launch_bounds__(1024) tp_allreduce_norm_kernel(TpAllreduceArgs
   if (threadIdx.x == 0) {
     __threadfence_system();
     st_release_sys(a.peer_flag, a.epoch);
-    while (ld_acquire_sys(a.my_flag) < a.epoch) {
-    }
+    tp_wait_flag(a.my_flag, a.epoch, true, a.err, a.timeout_ns);
   }
   __syncthreads();
   for (int row = blockIdx.x; row < a.rows; row += gridDim.x) {
@@ -329,8 +361,7 @@ __global__ void __launch_bounds__(1024) tp_push_rows_kernel(TpRowsArgs a) {
     __syncthreads();
     if (threadIdx.x == 0) {
       st_release_sys(a.peer_flags + row, a.epoch);
-      while (ld_acquire_sys(a.my_flags + row) != a.epoch) {
-      }
+      tp_wait_flag(a.my_flags + row, a.epoch, false, a.err, a.timeout_ns);
     }
     __syncthreads();
     // 2) x = (x + acc_0) + acc_1

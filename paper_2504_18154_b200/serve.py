@@ -365,11 +365,13 @@ class PaDGServer:
             self.n_prefill = fudg_prefill if 0 < fudg_prefill < n else n // 2
             roles = ["prefill"] * self.n_prefill + ["decode"] * (n - self.n_prefill)
         self._rr_dec = 0
+        self._rr_lock = threading.Lock()  # several prefill workers hand off concurrently
 
         def handoff():
             dec = self.workers[self.n_prefill:]
-            w = dec[self._rr_dec % len(dec)]
-            self._rr_dec += 1
+            with self._rr_lock:
+                w = dec[self._rr_dec % len(dec)]
+                self._rr_dec += 1
             return w
 
         self.workers = [Worker(i, inst, self.clock, self.status_q, token_budget, decode_steps_per_poll,
@@ -441,4 +443,28 @@ class PaDGServer:
             w.stop_flag.set()
         for w in self.workers:
             w.join(timeout=30)
+        self._release_leftovers()
         return self.reqs
+
+    def _release_leftovers(self):
+        """A run that stops early (timeout, worker error) leaves requests resident:
+        unfinished decodes, partly chunked prompts, FuDG requests exported but never
+        imported. Release them and drop staged KV handles so the instances (reused by
+        the next goodput probe) start from an empty pool."""
+        for w in self.workers:
+            if w.is_alive():
+                continue  # still inside a phase call; the instance is not safe to touch
+            w.imports.clear()
+            while True:
+                try:
+                    w.inbox.get_nowait()
+                except queue.Empty:
+                    break
+            try:
+                st, recs = w.inst.status()
+            except Exception:  # a dead instance: nothing to release
+                continue
+            if recs:
+                w.inst.release([r["req_id"] for r in recs])
+            w.committed.clear()
+            w.commit_sum = 0

@@ -87,3 +87,40 @@ def test_opt_in_decode_variants_match_oracle(env, shape):
     r = subprocess.run([sys.executable, os.path.join(root, "tools", "chain_diag.py"), shape, "3", "1e-2"],
                        env={**os.environ, k: v}, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_decode_rejects_duplicate_ids(setup):
+    """Two rows of one request in a decode set would share a KV slot: INVALID_ARG,
+    nothing changes (the request decodes normally afterwards)."""
+    from paper_2504_18154_b200 import _lib as L
+    shape, _, model, inst = setup
+    p = random_prompts(77, [40], shape.vocab)[0]
+    first = inst.prefill([(9100, p, 4)])
+    with pytest.raises(L.EcoError) as ei:
+        inst.decode([9100, 9100], 1)
+    assert ei.value.status == L.ERR_INVALID_ARG
+    toks, nf = inst.decode([9100], 3)
+    assert nf == 1 and tokens_match(model, p, [first[0]] + list(toks[0])) >= 1
+    inst.release([9100])
+
+
+def test_nan_logits_mark_instance_dead():
+    """Reading A6: NaN logits are an error, never a token. A NaN final-norm weight makes
+    every logit NaN: the prefill phase returns ECOSERVE_ERR_NUMERIC, the instance
+    reports dead, and later calls fail instead of embedding a garbage id."""
+    import torch
+    from paper_2504_18154_b200 import _lib as L
+    from paper_2504_18154_b200.instance import Instance, device_weights_from_host
+    shape = get_shape("tiny")
+    dw = device_weights_from_host(make_weights(shape, seed=0), "cuda:0")
+    dw["final_norm"] = torch.full_like(dw["final_norm"], float("nan"))
+    inst = Instance(shape, dw, 64, 0, token_budget=1024, max_batch=16, max_positions=1024)
+    try:
+        with pytest.raises(L.EcoError) as ei:
+            inst.prefill([(1, random_prompts(3, [20], shape.vocab)[0], 4)])
+        assert ei.value.status == L.ERR_NUMERIC
+        assert not inst.status()[0]["alive"]
+        with pytest.raises(L.EcoError):
+            inst.decode([1], 1)
+    finally:
+        inst.close()

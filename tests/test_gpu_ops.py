@@ -124,6 +124,22 @@ def test_lm_argmax_ties_lowest_index(ops):
     assert (got == 17).all()
 
 
+def test_lm_argmax_nan_row_is_flagged(ops):
+    """Reading A6: NaN logits are an error. A row whose logits contain NaN (here one
+    NaN input element poisons every logit of that row) gets the sentinel -2 from
+    both the epilogue and the reduction (NaN wins everywhere); clean rows are exact."""
+    rng = np.random.default_rng(5)
+    w, W = bf16_rand(rng, (4097, 256), 2.0 / 16)
+    x, X = bf16_rand(rng, (6, 256))
+    X[2, 7] = float("nan")
+    got = ops.lm_argmax(W, X).cpu().numpy()
+    assert got[2] == -2
+    logits = x @ w.T
+    for i in (0, 1, 3, 4, 5):
+        if T.top2_margin(logits[i]) > 1e-3:
+            assert got[i] == T.greedy(logits[i])
+
+
 @pytest.mark.parametrize("n,H", [(1, 256), (37, 4096), (5, 8192)])
 def test_rmsnorm(ops, n, H):
     rng = np.random.default_rng(H)
