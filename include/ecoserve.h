@@ -358,7 +358,13 @@ ecoserve_status ecoserve_handler_deserialize(const uint8_t* in, int32_t n, ecose
  * instances under the integer cost model (decision-parity mode):
  * prefill batch = sum of predicted prefill ns; decode step =
  * d + e*B + (f * sum(context))/1000 ns. Outputs per request (host arrays of n_req):
- * instance, t_first, t_decode_begin, t_done (-1 if never admitted). */
+ * instance, t_first, t_decode_begin, t_done (-1 if never admitted), and n_preempt
+ * (may be NULL): how often the request was preempted for recompute under KV
+ * pressure (reading A14: when the reservation R is below the true output length, a
+ * decode step preempts the latest-arrived batch members until the grown batch fits
+ * the pool; they are re-prefilled with prompt + generated tokens from the front of
+ * the queue, TD-Pipe P:1112). ECOSERVE_ERR_KV_EXHAUSTED if one request needs more
+ * blocks than a whole instance pool (the outputs are then partial). */
 typedef struct {
   int64_t cost_d_ns, cost_e_ns, cost_f_ps;
   int32_t token_budget;
@@ -368,7 +374,7 @@ ecoserve_status ecoserve_des_run(const ecoserve_macro_config* mcfg, const ecoser
                                  const int64_t* arrival_ns, const int32_t* prompt_len, const int32_t* output_len,
                                  int32_t n_req, int32_t* inst, int64_t* t_first, int64_t* t_decode_begin,
                                  int64_t* t_done, int64_t* route_log /* host [cap][3]: (t_ns, req, inst), may be NULL */,
-                                 int32_t route_log_cap, int32_t* n_route_log);
+                                 int32_t route_log_cap, int32_t* n_route_log, int32_t* n_preempt);
 
 #ifdef __cplusplus
 }

@@ -30,6 +30,7 @@ def tick_simulate(reqs, n_inst: int, total_blocks: int, cfg, cost, token_budget:
     done = [-1] * n
     ngen = [0] * n
     where = [-1] * n
+    preempts = []                # (t, req_id, inst): A14 recompute preemptions
     # per instance
     phase = [0] * n_inst
     tsw = [0] * n_inst
@@ -52,21 +53,35 @@ def tick_simulate(reqs, n_inst: int, total_blocks: int, cfg, cost, token_budget:
             fin_unrep[i] = []
             macro.update_status(i, phase[i], tsw[i], rs)
 
+    def blocks(tokens):          # 64-token KV blocks holding `tokens` tokens
+        return -(-tokens // 64)
+
     def kick(t):
         for i in range(n_inst):
             if end[i] >= 0:
                 continue
-            if queue[i]:
+            # blocks held: prompt + fed tokens of every prefilled request on the instance
+            held = 0
+            for k in waiting[i] + running[i]:
+                held += blocks(S[k] + ngen[k] - 1)
+            # a prefill processes the prompt, plus the generated tokens after a preemption
+            if queue[i] and blocks(S[queue[i][0]] + ngen[queue[i][0]]) + held <= total_blocks:
                 if phase[i] != 1:
                     phase[i], tsw[i] = 1, t
                 batch, tok = [], 0
-                while queue[i] and (not batch or tok + S[queue[i][0]] <= token_budget):
-                    k = queue[i].pop(0)
+                while queue[i]:
+                    k = queue[i][0]
+                    if batch and tok + S[k] + ngen[k] > token_budget:
+                        break
+                    if held + blocks(S[k] + ngen[k]) > total_blocks:
+                        break
+                    queue[i].pop(0)
                     batch.append(k)
-                    tok += S[k]
+                    tok += S[k] + ngen[k]
+                    held += blocks(S[k] + ngen[k])
                 d = 0
                 for k in batch:
-                    d += cost.prefill_ns(S[k])
+                    d += cost.prefill_ns(S[k] + ngen[k])
                 if d % tick:
                     raise ValueError("prefill duration is not a multiple of the tick")
                 end[i], opkind[i], opids[i] = t + d, "prefill", batch
@@ -74,11 +89,27 @@ def tick_simulate(reqs, n_inst: int, total_blocks: int, cfg, cost, token_budget:
                 if phase[i] != 2:
                     phase[i], tsw[i] = 2, t
                     for k in waiting[i]:
-                        dbeg[k] = t
+                        if dbeg[k] == -1:
+                            dbeg[k] = t
                     running[i] = running[i] + waiting[i]
                     waiting[i] = []
                 batch = running[i]
                 running[i] = []
+                # every member grows to S + ngen tokens in this step; drop latest arrivals
+                # to the queue front until that fits (A14)
+                while batch:
+                    after = 0
+                    for k in batch:
+                        after += blocks(S[k] + ngen[k])
+                    if after <= total_blocks:
+                        break
+                    late = batch[0]
+                    for k in batch:
+                        if (arr[k], ids[k]) > (arr[late], ids[late]):
+                            late = k
+                    batch.remove(late)
+                    queue[i].insert(0, late)
+                    preempts.append((t, ids[late], i))
                 d = cost.decode_ns(len(batch), sum(S[k] + ngen[k] for k in batch))
                 if d % tick:
                     raise ValueError("decode duration is not a multiple of the tick")
@@ -89,13 +120,13 @@ def tick_simulate(reqs, n_inst: int, total_blocks: int, cfg, cost, token_budget:
         for i in range(n_inst):
             if end[i] == t:
                 for k in opids[i]:
-                    if opkind[i] == "prefill":
+                    if opkind[i] == "prefill" and first[k] == -1:
                         first[k], ngen[k] = t, 1
                     else:
                         ngen[k] += 1
                     if ngen[k] >= G[k]:
                         done[k] = t
-                        if opkind[i] == "prefill":
+                        if opkind[i] == "prefill" and dbeg[k] == -1:
                             dbeg[k] = t
                         fin_unrep[i].append(k)
                     elif opkind[i] == "prefill":
@@ -133,4 +164,4 @@ def tick_simulate(reqs, n_inst: int, total_blocks: int, cfg, cost, token_budget:
         t += tick
     recs = {ids[k]: dict(inst=where[k], t_first_ns=first[k], t_decode_begin_ns=dbeg[k],
                          t_done_ns=done[k], n_gen=ngen[k]) for k in range(n)}
-    return recs, log
+    return recs, log, preempts

@@ -155,7 +155,7 @@ SIGNATURES = {
     "ecoserve_handler_serialize": (I32, [C.POINTER(InstanceHandler), C.POINTER(C.c_uint8), I32]),
     "ecoserve_handler_deserialize": (C.c_int, [C.POINTER(C.c_uint8), I32, C.POINTER(InstanceHandler)]),
     "ecoserve_des_run": (C.c_int, [C.POINTER(MacroConfig), C.POINTER(DesConfig), PI64, PI32, PI32, I32, PI32,
-                                   PI64, PI64, PI64, PI64, I32, PI32]),
+                                   PI64, PI64, PI64, PI64, I32, PI32, PI32]),
     "ecoserve_op_gemm": (C.c_int, [P, P, I32, I32, I32, I32, P, I32, P]),
     "ecoserve_op_gemm_swap": (C.c_int, [P, P, I32, I32, I32, I32, P, P, I32, P]),
     "ecoserve_op_gemm_swap_bf16": (C.c_int, [P, P, I32, I32, I32, I32, P, P, P, I32, P]),

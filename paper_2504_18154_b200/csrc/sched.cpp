@@ -16,6 +16,11 @@
 //    DES: prefill windows drain the routed queue FIFO in <= token_budget
 //    batches; decode steps are non-preemptive (A15); new decodes join at
 //    window end (A16); completions before arrivals at equal time.
+//    KV pressure (A14, only when R is below true outputs): a decode step preempts
+//    the latest-arrived batch members until every member can hold
+//    ceil((S + n_gen)/64) blocks after the step; they go to the front of the queue
+//    and are recomputed by a prefill of prompt + generated tokens; a
+//    prefill batch is the FIFO prefix that fits the budget and the free blocks.
 #include <stdint.h>
 #include <string.h>
 
@@ -349,7 +354,8 @@ ecoserve_status ecoserve_handler_deserialize(const uint8_t* in, int32_t n, ecose
 ecoserve_status ecoserve_des_run(const ecoserve_macro_config* mcfg, const ecoserve_des_config* dcfg,
                                  const int64_t* arrival_ns, const int32_t* prompt_len, const int32_t* output_len,
                                  int32_t n_req, int32_t* out_inst, int64_t* out_first, int64_t* out_dbeg,
-                                 int64_t* out_done, int64_t* route_log, int32_t route_log_cap, int32_t* n_route_log) {
+                                 int64_t* out_done, int64_t* route_log, int32_t route_log_cap, int32_t* n_route_log,
+                                 int32_t* out_n_preempt) {
   if (!mcfg || !dcfg || n_req < 0 || (n_req > 0 && (!arrival_ns || !prompt_len || !output_len || !out_inst ||
                                                      !out_first || !out_dbeg || !out_done)))
     return ECOSERVE_ERR_INVALID_ARG;
@@ -359,7 +365,7 @@ ecoserve_status ecoserve_des_run(const ecoserve_macro_config* mcfg, const ecoser
   const int N = m->n;
   struct R {
     int64_t arr;
-    int32_t S, G, inst = -1, n_gen = 0;
+    int32_t S, G, inst = -1, n_gen = 0, n_pre = 0;
     int64_t first = -1, dbeg = -1, done = -1;
   };
   std::vector<R> rq(n_req);
@@ -407,20 +413,31 @@ ecoserve_status ecoserve_des_run(const ecoserve_macro_config* mcfg, const ecoser
   typedef std::tuple<int64_t, int, int> Ev;
   std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> ev;
   for (int k = 0; k < n_req; ++k) ev.push(Ev(rq[k].arr, 1, k));
+  const int64_t BT = m->block;
+  // tokens a prefill of k processes: the prompt, plus the generated tokens of a recompute (A14)
+  auto plen = [&](int k) -> int64_t { return (int64_t)rq[k].S + rq[k].n_gen; };
+  bool pool_error = false;
   auto start = [&](int i, int64_t t) {
     I& x = in[i];
     if (x.busy) return;
-    if (!x.queue.empty()) {
+    const int64_t total = m->inst[i].total_blocks;
+    int64_t held = 0;  // prompt + fed tokens of the prefilled requests
+    for (int k : x.waiting) held += cdiv((int64_t)rq[k].S + rq[k].n_gen - 1, BT);
+    for (int k : x.running) held += cdiv((int64_t)rq[k].S + rq[k].n_gen - 1, BT);
+    int64_t free_b = total - held;
+    if (!x.queue.empty() && cdiv(plen(x.queue.front()), BT) <= free_b) {
       if (x.phase != 1) { x.phase = 1; x.t_switch = t; }
       x.op.clear();
       int64_t tok = 0, dur = 0;
       while (!x.queue.empty()) {
         const int k = x.queue.front();
-        if (!x.op.empty() && tok + rq[k].S > dcfg->token_budget) break;
+        if (!x.op.empty() && tok + plen(k) > dcfg->token_budget) break;
+        if (cdiv(plen(k), BT) > free_b) break;
         x.queue.pop_front();
         x.op.push_back(k);
-        tok += rq[k].S;
-        dur += m->pred(rq[k].S);
+        tok += plen(k);
+        free_b -= cdiv(plen(k), BT);
+        dur += m->pred(plen(k));
       }
       x.busy = true;
       x.op_prefill = true;
@@ -429,18 +446,37 @@ ecoserve_status ecoserve_des_run(const ecoserve_macro_config* mcfg, const ecoser
       if (x.phase != 2) {
         x.phase = 2;
         x.t_switch = t;
-        for (int k : x.waiting) rq[k].dbeg = t;
+        for (int k : x.waiting)
+          if (rq[k].dbeg < 0) rq[k].dbeg = t;
         x.running.insert(x.running.end(), x.waiting.begin(), x.waiting.end());
         x.waiting.clear();
       }
       x.op = x.running;
       x.running.clear();
+      for (;;) {  // A14: preempt latest arrivals until the grown batch fits the pool
+        int64_t after = 0;
+        for (int k : x.op) after += cdiv((int64_t)rq[k].S + rq[k].n_gen, BT);
+        if (x.op.empty() || after <= total) break;
+        size_t v = 0;
+        for (size_t j = 1; j < x.op.size(); ++j)
+          if (std::make_pair(rq[x.op[j]].arr, x.op[j]) > std::make_pair(rq[x.op[v]].arr, x.op[v])) v = j;
+        const int k = x.op[v];
+        x.op.erase(x.op.begin() + v);
+        x.queue.push_front(k);
+        ++rq[k].n_pre;
+      }
+      if (x.op.empty()) {
+        pool_error = true;  // one request outgrew the whole pool
+        return;
+      }
       int64_t sum_ctx = 0;
       for (int k : x.op) sum_ctx += rq[k].S + rq[k].n_gen;
       const int64_t dur = dcfg->cost_d_ns + dcfg->cost_e_ns * (int64_t)x.op.size() + (dcfg->cost_f_ps * sum_ctx) / 1000;
       x.busy = true;
       x.op_prefill = false;
       ev.push(Ev(t + dur, 0, i));
+    } else if (!x.queue.empty()) {
+      pool_error = true;  // the queue head needs more blocks than the empty pool holds
     }
   };
   while (!ev.empty()) {
@@ -451,15 +487,15 @@ ecoserve_status ecoserve_des_run(const ecoserve_macro_config* mcfg, const ecoser
     if (std::get<1>(e) == 0) {
       I& x = in[idx];
       for (int k : x.op) {
-        if (x.op_prefill) {
+        if (x.op_prefill && rq[k].n_gen == 0) {
           rq[k].first = t;
           rq[k].n_gen = 1;
-        } else {
+        } else {  // decode step, or a recompute prefill (A14): the next token
           rq[k].n_gen += 1;
         }
         if (rq[k].n_gen >= rq[k].G) {
           rq[k].done = t;
-          if (x.op_prefill) rq[k].dbeg = t;
+          if (x.op_prefill && rq[k].dbeg < 0) rq[k].dbeg = t;
           x.fin.push_back(k);
         } else if (x.op_prefill) {
           x.waiting.push_back(k);
@@ -492,16 +528,18 @@ ecoserve_status ecoserve_des_run(const ecoserve_macro_config* mcfg, const ecoser
       }
     }
     for (int i = 0; i < N; ++i) start(i, t);
+    if (pool_error) break;
   }
   for (int k = 0; k < n_req; ++k) {
     out_inst[k] = rq[k].inst;
     out_first[k] = rq[k].first;
     out_dbeg[k] = rq[k].dbeg;
     out_done[k] = rq[k].done;
+    if (out_n_preempt) out_n_preempt[k] = rq[k].n_pre;
   }
   if (n_route_log) *n_route_log = nlog;
   ecoserve_macro_destroy(m);
-  return ECOSERVE_OK;
+  return pool_error ? ECOSERVE_ERR_KV_EXHAUSTED : ECOSERVE_OK;
 }
 
 }  // extern "C"

@@ -134,7 +134,7 @@ def handler_from_bytes(b: bytes) -> dict:
 def des_run(cfg: SchedConfig, arrival_ns, prompt_len, output_len, cost_d_ns=COST_DEFAULT["d"],
             cost_e_ns=COST_DEFAULT["e"], cost_f_ps=COST_DEFAULT["f"], token_budget: int = 16384):
     """Virtual-clock DES of the macro instance (C++). Returns dict of per-request
-    arrays (inst, t_first, t_decode_begin, t_done) and the route log [(t, req, inst)]."""
+    arrays (inst, t_first, t_decode_begin, t_done, n_preempt) and the route log [(t, req, inst)]."""
     lib = L.load()
     c, keep = cfg.to_c()
     n = len(arrival_ns)
@@ -142,6 +142,7 @@ def des_run(cfg: SchedConfig, arrival_ns, prompt_len, output_len, cost_d_ns=COST
     s = np.ascontiguousarray(prompt_len, dtype=np.int32)
     g = np.ascontiguousarray(output_len, dtype=np.int32)
     inst = np.zeros(n, np.int32)
+    npre = np.zeros(n, np.int32)
     tf, tb, td = np.zeros(n, np.int64), np.zeros(n, np.int64), np.zeros(n, np.int64)
     cap = 8 * n + 16
     log = np.zeros((cap, 3), np.int64)
@@ -150,6 +151,6 @@ def des_run(cfg: SchedConfig, arrival_ns, prompt_len, output_len, cost_d_ns=COST
     L.check(lib.ecoserve_des_run(C.byref(c), C.byref(d), a.ctypes.data_as(L.PI64), s.ctypes.data_as(L.PI32),
                                  g.ctypes.data_as(L.PI32), n, inst.ctypes.data_as(L.PI32), tf.ctypes.data_as(L.PI64),
                                  tb.ctypes.data_as(L.PI64), td.ctypes.data_as(L.PI64), log.ctypes.data_as(L.PI64),
-                                 cap, C.byref(nlog)))
-    return dict(inst=inst, t_first=tf, t_decode_begin=tb, t_done=td,
+                                 cap, C.byref(nlog), npre.ctypes.data_as(L.PI32)))
+    return dict(inst=inst, t_first=tf, t_decode_begin=tb, t_done=td, n_preempt=npre,
                 route_log=[tuple(int(v) for v in row) for row in log[:min(cap, nlog.value)]])

@@ -163,12 +163,69 @@ def test_des_equals_tick_simulator(seed):
     blocks = rng.choice([12, 40])
     budget = rng.choice([256, 1024])
     sim = des.simulate(reqs, n_inst, blocks, cfg, cost, budget)
-    recs, log = tick_sim.tick_simulate(reqs, n_inst, blocks, cfg, cost, budget, tick, horizon=10 ** 13)
+    recs, log, pre = tick_sim.tick_simulate(reqs, n_inst, blocks, cfg, cost, budget, tick, horizon=10 ** 13)
+    assert pre == sim.preempt_log
     for rid, r in sim.reqs.items():
         t = recs[rid]
         assert (r.inst, r.t_first_ns, r.t_decode_begin_ns, r.t_done_ns, r.n_gen) == \
             (t["inst"], t["t_first_ns"], t["t_decode_begin_ns"], t["t_done_ns"], t["n_gen"])
     assert sim.route_log == log
+
+
+def _pressure_case(seed):
+    """A tiny trace whose outputs outgrow the reservation (R = 0): C3 admits more
+    than the pool can hold once the requests grow, so A14 preemption must fire."""
+    rng = random.Random(1000 + seed)
+    tick = 500_000
+    # one tick per prompt token, so recompute prefills (prompt + generated) stay on the tick grid
+    cost = S.CostModel(a=rng.choice([1, 2]) * tick, b=tick * 1000, c=0, d=rng.choice([3, 5]) * tick, e=0, f=0)
+    n_inst = rng.randint(1, 2)
+    reqs = [Request(i, rng.randint(0, 30) * tick, rng.randint(20, 150), rng.randint(30, 160))
+            for i in range(rng.randint(3, 8))]
+    cfg = S.MacroConfig(slo_ttft_ns=10 ** 12, slo_tpot_ns=10 ** 12, reserve_tokens=0)
+    blocks = rng.choice([6, 8, 10])
+    return reqs, n_inst, blocks, cfg, cost, tick
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_des_preemption_equals_tick_simulator(seed):
+    """Reading A14 (recompute preemption, TD-Pipe P:1112) in the DES == the naive
+    tick simulator, bit-exact: timestamps, routing and the preemption log."""
+    reqs, n_inst, blocks, cfg, cost, tick = _pressure_case(seed)
+    sim = des.simulate(reqs, n_inst, blocks, cfg, cost, 256)
+    recs, log, pre = tick_sim.tick_simulate(reqs, n_inst, blocks, cfg, cost, 256, tick, horizon=10 ** 13)
+    assert pre == sim.preempt_log
+    assert sim.route_log == log
+    for rid, r in sim.reqs.items():
+        t = recs[rid]
+        assert (r.inst, r.t_first_ns, r.t_decode_begin_ns, r.t_done_ns, r.n_gen) == \
+            (t["inst"], t["t_first_ns"], t["t_decode_begin_ns"], t["t_done_ns"], t["n_gen"])
+        assert r.n_gen == r.G and r.t_done_ns >= 0                     # nothing lost, exact lengths
+        assert r.arrival_ns <= r.t_first_ns <= r.t_decode_begin_ns <= r.t_done_ns
+    assert max(sim.max_blocks_used) <= blocks                          # KV conservation
+
+
+def test_preemption_fires_and_recomputes():
+    """The pressure cases really exercise A14: requests are preempted, re-prefilled
+    with prompt + generated tokens, and still finish with exactly G tokens."""
+    fired = 0
+    for seed in range(16):
+        reqs, n_inst, blocks, cfg, cost, _ = _pressure_case(seed)
+        sim = des.simulate(reqs, n_inst, blocks, cfg, cost, 256)
+        fired += len(sim.preempt_log)
+        for (t, rid, i) in sim.preempt_log:
+            r = sim.reqs[rid]
+            assert r.n_preempt >= 1 and r.t_first_ns <= t < r.t_done_ns and r.inst == i
+    assert fired >= 10
+
+
+def test_no_preemption_when_reservation_covers_outputs():
+    """With R >= every output length, C3 keeps the pool from ever running out: the
+    A14 path never fires (the parity runs rely on this)."""
+    reqs = make_trace("sharegpt", 300, seed=2, rate_per_s=150.0)
+    R = max(r.output_len for r in reqs)
+    sim = des.simulate(reqs, 2, 3000, S.MacroConfig(5 * SEC, SEC // 10, reserve_tokens=R), S.CostModel(), 16384)
+    assert sim.preempt_log == [] and all(r.t_done_ns >= 0 for r in sim.reqs.values())
 
 
 def test_des_invariants_on_sharegpt_trace():

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from oracle import des, scheduler as S
-from synthetic.traces import make_trace
+from synthetic.traces import Request, make_trace
 
 SEC = 1_000_000_000
 
@@ -92,3 +92,25 @@ def test_deferred_fifo_drain(M):
     assert cm.drain_deferred(1) == []
     cm.update_status(1, 1, 0, 1000, [(2, 0, 10, 5, 1, True)])   # request 2 finished
     assert cm.drain_deferred(2) == [(3, 1)]    # 3 fits, 4 is still deferred (FIFO head stops)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_des_preemption_bitexact_vs_oracle(M, seed):
+    """Reading A14 under KV pressure (R = 0 on a small pool): the C++ DES preempts and
+    recomputes exactly as the oracle does (timestamps, routing, preemption counts)."""
+    rng = random.Random(7000 + seed)
+    n = rng.randint(6, 40)
+    arr = sorted(rng.randint(0, 2 * SEC) for _ in range(n))
+    reqs = [Request(i, arr[i], rng.randint(16, 600), rng.randint(20, 400)) for i in range(n)]
+    n_inst, blocks = rng.randint(1, 3), rng.choice([18, 24, 40])
+    ocfg = S.MacroConfig(50 * SEC, SEC, 0)
+    sim = des.simulate(reqs, n_inst, blocks, ocfg, S.CostModel(), 2048)
+    assert sim.preempt_log, "the case must exercise A14"
+    cfg = M.SchedConfig(n_inst, 50 * SEC, SEC, 0, [blocks] * n_inst)
+    got = M.des_run(cfg, [r.arrival_ns for r in reqs], [r.prompt_len for r in reqs], [r.output_len for r in reqs],
+                    token_budget=2048)
+    for k, r in enumerate(reqs):
+        o = sim.reqs[r.req_id]
+        assert (got["inst"][k], got["t_first"][k], got["t_decode_begin"][k], got["t_done"][k],
+                got["n_preempt"][k]) == (o.inst, o.t_first_ns, o.t_decode_begin_ns, o.t_done_ns, o.n_preempt), k
+    assert got["route_log"] == [tuple(x) for x in sim.route_log]
