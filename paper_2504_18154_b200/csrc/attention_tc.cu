@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(AttnCfg<HP>::THREADS, 1)
   }
   if (warp == 1) tmem_alloc(tmem_ptr, C::TMEM_COLS);
   tc_fence_before();
+  __syncwarp();  // lanes of the role warps reconverge: bar.sync counts whole warps
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_ptr;
@@ -358,6 +359,7 @@ __global__ void __launch_bounds__(AttnCfg<HP>::THREADS, 1)
     }
   }
   tc_fence_before();
+  __syncwarp();  // lanes of the role warps reconverge: bar.sync counts whole warps
   __syncthreads();
   tc_fence_after();
   if (warp == 1) {

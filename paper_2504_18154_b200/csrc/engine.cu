@@ -16,6 +16,8 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <memory>
 #include <string>
 #include <unordered_map>
@@ -201,6 +203,20 @@ struct ecoserve_instance {
   float* chain_ws = nullptr;                 // split-tile sums [1024 tiles][128][128] (zeroed)
   int* chain_cnt = nullptr;                  // [4][1024] tile arrival counters
   double chain_bytes_layer = 0;              // weight bytes streamed per chain launch (O + GU + down + QKV)
+  // decode flow (decode_flow.cu): O -> gate/up -> down of a layer as one dataflow kernel
+  bool flow = false;
+  bool registered = false;                   // counted in device_instances
+  float* flow_slots = nullptr;               // [3][num_sms][2][128 * 128] partial tiles
+  int* flow_flags = nullptr;                 // [H/128] O flags, then [2F/128] gate/up flags
+  int* flow_cnt = nullptr;                   // [6][flow_cnt_ld] arrival + done counters, + [1] down tiles done
+  int flow_cnt_ld = 0;
+  float* flow_ss = nullptr;                  // [2][H/128][128] sums of squares (after O, after down)
+  float* flow_rvec = nullptr;                // [128]
+  int* flow_err = nullptr;
+  int* h_flow_err = nullptr;                 // pinned copy, read after every decode step
+  int flow_epoch = 0;
+  unsigned long long* flow_trace = nullptr;  // ECOSERVE_FLOW_TRACE (debug)
+  CUtensorMap flow_xmap, flow_actmap;         // x (f32, TMA reduce-add target), act (bf16, TMA store)
 
   bool fail(const char* what, cudaError_t e) {
     err = std::string(what) + ": " + cudaGetErrorString(e);
@@ -253,6 +269,37 @@ static ecoserve_model_shape local_shape(const ecoserve_model_shape* s) {
   l.ffn_dim = s->ffn_dim / tp;
   return l;
 }
+
+// Live instances per device. The decode flow kernel's CTAs wait on each other, so they
+// must all be resident at once: it only runs while its instance is alone on the GPU
+// (another instance's kernels on a concurrent stream could hold SMs indefinitely).
+static int device_instances(int device, int delta) {
+  static std::mutex mu;
+  static std::map<int, int> n;
+  std::lock_guard<std::mutex> lock(mu);
+  return n[device] += delta;
+}
+
+// ECOSERVE_FLOW=1 enables the decode flow kernel (decode_flow.cu). Off by default: it is
+// parity-green but measured slower than the per-kernel decode path (8B, B = 128, ctx 1.3k:
+// 9.09 vs 7.7 ms per decode step).
+static bool flow_env_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_FLOW");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// debug: ECOSERVE_FLOW_TRACE=path appends per-CTA phase marks of one flow launch per step
+static const char* flow_trace_path() {
+  static const char* p = getenv("ECOSERVE_FLOW_TRACE");
+  return p;
+}
+
+// gate/up flags start on a 128-byte boundary after the O flags (pollers read 16-B vectors)
+static int flow_gu_flag_off(int H) { return (H / 128 + 31) / 32 * 32; }
 
 static bool shape_ok(const ecoserve_model_shape* s) {
   if (!s) return false;
@@ -388,6 +435,11 @@ void ecoserve_instance_destroy(ecoserve_instance* inst) {
   if (inst->h_tokens) cudaFreeHost(inst->h_tokens);
   if (inst->h_chain_err) cudaFreeHost(inst->h_chain_err);
   if (inst->h_tp_err) cudaFreeHost(inst->h_tp_err);
+  if (inst->h_flow_err) cudaFreeHost(inst->h_flow_err);
+  for (void* p : {(void*)inst->flow_slots, (void*)inst->flow_flags, (void*)inst->flow_cnt, (void*)inst->flow_ss,
+                  (void*)inst->flow_rvec, (void*)inst->flow_err, (void*)inst->flow_trace})
+    if (p) cudaFree(p);
+  if (inst->registered) device_instances(inst->device, -1);
   if (inst->tp_err) cudaFree(inst->tp_err);
   for (cudaEvent_t e : inst->prof.pool) cudaEventDestroy(e);
   if (inst->peer_ipc) {
@@ -614,6 +666,34 @@ ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, cons
     const ecoserve_status es = build_chain(inst);
     if (es != ECOSERVE_OK) return es;
   }
+  if (inst->tp == 1 && !inst->chain && flow_env_enabled() && H % 128 == 0 && F % 64 == 0 && (M * D) % 64 == 0 &&
+      2 * F / 128 <= 256 && H / 128 <= 128) {
+    const int nt_o = H / 128, nt_gu = 2 * F / 128;
+    inst->flow_cnt_ld = std::max(nt_o, nt_gu);
+    CK(cudaMalloc(&inst->flow_slots, sizeof(float) * decode_flow_slot_floats(inst->num_sms)));
+    CK(cudaMalloc(&inst->flow_flags, sizeof(int) * (flow_gu_flag_off(H) + nt_gu)));  // (128-B aligned groups)
+    CK(cudaMemset(inst->flow_flags, 0, sizeof(int) * (flow_gu_flag_off(H) + nt_gu)));
+    CK(cudaMalloc(&inst->flow_cnt, sizeof(int) * (6 * inst->flow_cnt_ld + 1)));
+    CK(cudaMemset(inst->flow_cnt, 0, sizeof(int) * (6 * inst->flow_cnt_ld + 1)));
+    CK(cudaMalloc(&inst->flow_ss, sizeof(float) * 2 * nt_o * 128));
+    CK(cudaMalloc(&inst->flow_rvec, sizeof(float) * 128));
+    if (flow_trace_path()) {
+      CK(cudaMalloc(&inst->flow_trace, sizeof(unsigned long long) * inst->num_sms * 16));
+      CK(cudaMemset(inst->flow_trace, 0, sizeof(unsigned long long) * inst->num_sms * 16));
+    }
+    if (make_tmap_2d_plain(&inst->flow_xmap, inst->x, 1, inst->T_max, H, 128, 32) ||
+        make_tmap_2d_plain(&inst->flow_actmap, inst->act, 0, inst->T_max, F, 64, 32)) {
+      inst->err = "decode flow: tensor map creation failed";
+      return ECOSERVE_ERR_CUDA;
+    }
+    CK(cudaMalloc(&inst->flow_err, sizeof(int)));
+    CK(cudaMemset(inst->flow_err, 0, sizeof(int)));
+    CK(cudaMallocHost(&inst->h_flow_err, sizeof(int)));
+    *inst->h_flow_err = 0;
+    inst->flow = true;
+  }
+  device_instances(device, +1);  // (a failed create is not counted)
+  inst->registered = true;
   *out = holder.release();
   return ECOSERVE_OK;
 }
@@ -802,6 +882,19 @@ int decode_variant() {  // 1: one A+B ring (default); 3: lean (co-resident); 4: 
 // (bench r01: decode 11.7k vs 13.8k tok/s) -- clusters need whole free GPC slices, so
 // they cannot start while the previous kernel's CTAs drain under PDL.
 // ECOSERVE_CLUSTER_SPLITK=1 enables it.
+// Timing experiments only (tools/decode_ablate.py): ECOSERVE_ABLATE=<bitmask> drops
+// kernels from the decode step so their in-step cost can be measured by difference:
+// 1 = decode attention, 2 = O / gate-up / down GEMMs and their reductions, 4 = the QKV
+// GEMM. The tokens are then meaningless; never set in the product path.
+int ablate_mask() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_ABLATE");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 bool host_timing_enabled() {  // ECOSERVE_HOST_TIMING=1: per decode step host-enqueue vs wall time (stderr)
   static int v = -1;
   if (v < 0) {
@@ -1065,6 +1158,12 @@ cudaError_t tp_allreduce(ecoserve_instance* inst, int ep, int rows, const bf16* 
 
 }  // namespace
 
+// The decode flow kernel runs when the instance set it up (TP=1, ECOSERVE_FLOW=1),
+// the batch fits one 128-token tile and the instance is alone on its GPU (device_instances).
+static bool use_flow(ecoserve_instance* inst, int B) {
+  return inst->flow && B >= 1 && B <= 128 && device_instances(inst->device, 0) == 1;
+}
+
 // Context splits of the decode attention: split only as much as needed for
 // B x Mkv x splits to fill the SMs about twice (uniform 512-token chunks were measured
 // slower: more CTAs, partials, combine). ECOSERVE_ATTN_SPLITS=n forces n (sweeps).
@@ -1305,6 +1404,101 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     }
     return ECOSERVE_OK;
   }
+  if (use_flow(inst, B)) {
+    // per layer: QKV GEMM (+ split reduction with RoPE / KV write, scaled by the 1/rms the
+    // previous flow kernel left in flow_rvec) -> attention -> one flow kernel (O, gate/up,
+    // down; decode_flow.cu) that leaves x, h = bf16(x * next gamma) and flow_rvec
+    LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, inst->lw[0].attn_norm, inst->h, B, H, eps, st));
+    const int bn = B <= 64 ? 64 : 128;
+    const int bi = bn_index(bn);
+    const double flow_bytes = 2.0 * ((double)H * M * D + 2.0 * F * H + (double)H * F);
+    const int nt_o = H / 128;
+    for (int l = 0; l < L; ++l) {
+      LayerW& w = inst->lw[l];
+      GemmEpi e = epi_base(inst);
+      e.pos = d_pos;
+      e.slot = d_slot;
+      e.k_cache = k_layer(inst, l);
+      e.v_cache = v_layer(inst, l);
+      if (l > 0) e.rvec = inst->flow_rvec;
+      int nk = 0;
+      LAUNCH(P_GEMM_DECODE, 2.0 * inst->QKV * H, nk,
+             decode_gemm(inst, w.qkv_a, inst->m_h, inst->QKV, H, B, EPI_SWAP_QKV, e, &nk, nullptr, nullptr, nullptr,
+                         &w.qkv_b));
+      DecodeAttnArgs a;
+      a.q = inst->q;
+      a.k_cache = k_layer(inst, l);
+      a.v_cache = v_layer(inst, l);
+      a.blk_stride = inst->blk_stride;
+      a.ctx_lens = d_ctx;
+      a.block_tables = d_bt;
+      a.bt_ld = bt_ld;
+      a.B = B;
+      a.n_heads = M;
+      a.n_kv = inst->Mkv;
+      a.n_splits = n_splits;
+      a.blocks_per_split = bps;
+      a.part_o = inst->attn_ws;
+      a.part_ml = inst->attn_ws + (int64_t)B * M * n_splits * D;
+      a.out = inst->ao;
+      a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
+      a.order = d_order;
+      a.kvmap = inst->attn_tc ? &inst->attn_kvmap : nullptr;
+      a.layer = l;
+      a.n_layers = L;
+      LAUNCH(P_ATTN_DECODE, kv_bytes, n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
+      const bool last = l + 1 == L;
+      FlowArgs fa;
+      fa.B = B;
+      fa.H = H;
+      fa.F = F;
+      fa.MD = M * D;
+      fa.epoch = ++inst->flow_epoch;
+      fa.eps = eps;
+      fa.inv_h = 1.f / (float)H;
+      fa.x = inst->x;
+      fa.h = inst->h;
+      fa.h_out = last ? inst->hl : inst->h;
+      fa.act = inst->act;
+      fa.gamma_o = w.ffn_norm;
+      fa.gamma_d = last ? inst->final_norm : inst->lw[l + 1].attn_norm;
+      fa.ss_o = inst->flow_ss;
+      fa.ss_d = inst->flow_ss + nt_o * 128;
+      fa.rvec = inst->flow_rvec;
+      fa.flags_o = inst->flow_flags;
+      fa.flags_gu = inst->flow_flags + flow_gu_flag_off(H);
+      fa.cnt = inst->flow_cnt;
+      fa.cnt_ld = inst->flow_cnt_ld;
+      fa.done_d = inst->flow_cnt + 6 * inst->flow_cnt_ld;
+      fa.slots = inst->flow_slots;
+      fa.err = inst->flow_err;
+      fa.trace = (flow_trace_path() && l == std::min(5, L - 1)) ? inst->flow_trace : nullptr;
+      LAUNCH(P_GEMM_DECODE, flow_bytes, 1,
+             decode_flow_launch(&w.o_a, &w.gu_a, &w.d_a, &inst->m_ao.b[bi], &inst->m_h.b[bi], &inst->m_act.b[bi],
+                                &inst->flow_xmap, &inst->flow_actmap, fa, bn, inst->num_sms, st));
+      if (inst->debug)
+        CK(cudaMemcpyAsync(inst->dbg + (int64_t)(l + 1) * inst->T_max * H, inst->x, sizeof(float) * (int64_t)B * H,
+                           cudaMemcpyDeviceToDevice, st));
+    }
+    *final_normed = true;  // hl = bf16(x * final_norm): the LM-head argmax is invariant to 1/rms > 0
+    if (flow_trace_path()) {  // debug: append "cta mark t_ns" of layer 5's flow kernel
+      std::vector<unsigned long long> t((size_t)inst->num_sms * 16);
+      CK(cudaMemcpyAsync(t.data(), inst->flow_trace, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      unsigned long long t0 = ~0ull;
+      for (int c = 0; c < inst->num_sms; ++c) if (t[c * 16]) t0 = std::min(t0, t[c * 16]);
+      FILE* f = fopen(flow_trace_path(), "a");
+      if (f) {
+        fprintf(f, "# B=%d\n", B);
+        for (int c = 0; c < inst->num_sms; ++c)
+          for (int k = 0; k < 16; ++k)
+            if (t[c * 16 + k] >= t0) fprintf(f, "%d %d %llu\n", c, k, t[c * 16 + k] - t0);
+        fclose(f);
+      }
+      CK(cudaMemsetAsync(inst->flow_trace, 0, sizeof(unsigned long long) * t.size(), st));
+    }
+    return ECOSERVE_OK;
+  }
   bool h_ready = false, fused = false;
   *final_normed = false;
   for (int l = 0; l < L; ++l) {
@@ -1317,9 +1511,11 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     e.k_cache = k_layer(inst, l);
     e.v_cache = v_layer(inst, l);
     int nk = 0;
-    LAUNCH(P_GEMM_DECODE, 2.0 * inst->QKV * H, nk,
-           decode_gemm(inst, w.qkv_a, inst->m_h, inst->QKV, H, B, EPI_SWAP_QKV, e, &nk, nullptr, nullptr, nullptr,
-                       &w.qkv_b));
+    const int abl = ablate_mask();
+    if (!(abl & 4))
+      LAUNCH(P_GEMM_DECODE, 2.0 * inst->QKV * H, nk,
+             decode_gemm(inst, w.qkv_a, inst->m_h, inst->QKV, H, B, EPI_SWAP_QKV, e, &nk, nullptr, nullptr, nullptr,
+                         &w.qkv_b));
     DecodeAttnArgs a;
     a.q = inst->q;
     a.k_cache = k_layer(inst, l);
@@ -1341,7 +1537,11 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     a.kvmap = inst->attn_tc ? &inst->attn_kvmap : nullptr;  // TMA staging of K / V (head_dim 128)
     a.layer = l;
     a.n_layers = L;
-    LAUNCH(P_ATTN_DECODE, kv_bytes, n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
+    if (!(abl & 1)) LAUNCH(P_ATTN_DECODE, kv_bytes, n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
+    if (abl & 2) {
+      h_ready = true;
+      continue;
+    }
     if (inst->tp_fused) {  // partials -> fused push + all-reduce + residual + RMSNorm over NVLink (N2)
       const int ep = ++inst->tp_epoch;
       int sp = 1;
@@ -1897,9 +2097,15 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
     inst->prof.end(pm, B, st);
     CK(cudaMemcpyAsync(inst->h_tokens, inst->d_tokens, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
     if (inst->chain) CK(cudaMemcpyAsync(inst->h_chain_err, inst->chain_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (inst->flow) CK(cudaMemcpyAsync(inst->h_flow_err, inst->flow_err, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(copy_step_flags(inst));
     const auto t_enq1 = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(st));
+    if (inst->flow && *inst->h_flow_err) {
+      inst->err = "decode flow: a dependency wait timed out (CTAs not co-resident; ECOSERVE_FLOW=0 disables it)";
+      inst->dead = true;
+      return ECOSERVE_ERR_CUDA;
+    }
     if (inst->chain && *inst->h_chain_err) {
       inst->err = "decode chain: grid barrier timed out (CTAs not co-resident; set ECOSERVE_CHAIN=0 when several "
                   "instances share a GPU)";

@@ -206,8 +206,15 @@ __device__ __forceinline__ void epi_rows(const GemmEpi& e, int m, int n0, int n_
 // in f[]. Pair-interleaved rows (RoPE, SiLU) sit in adjacent lanes: exchange by shuffle,
 // so every lane executes the shuffles before any bounds check.
 __device__ __forceinline__ void epi_swap(const GemmEpi& e, int m, int m_rows, int n0, int n_rows, int lane,
-                                         const float (&f)[32]) {
+                                         const float (&f_in)[32]) {
   const bool mv = m < m_rows;
+  float f[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) f[i] = f_in[i];
+  if (e.rvec && e.mode == EPI_SWAP_QKV) {  // deferred RMSNorm (decode flow path)
+#pragma unroll
+    for (int i = 0; i < 32; ++i) f[i] *= (n0 + i < n_rows) ? e.rvec[n0 + i] : 0.f;
+  }
   const int ncols = min(32, n_rows - n0);
   switch (e.mode) {
     case EPI_SWAP_BF16: {
@@ -332,6 +339,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
   if (warp == 1) tmem_alloc(tmem_base_ptr, C::TMEM_COLS);
   tc_fence_before();
+  __syncwarp();  // lanes of the role warps reconverge: bar.sync counts whole warps
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_ptr;
@@ -806,6 +814,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (epi.out2) __threadfence_system();  // TP push complete before the grid ends
   }
   tc_fence_before();
+  __syncwarp();  // lanes of the role warps reconverge: bar.sync counts whole warps
   __syncthreads();
   tc_fence_after();
   if (warp == 1) {
@@ -876,6 +885,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
   if (warp == 1) tmem_alloc(tmem_base_ptr, C::TMEM_COLS);
   tc_fence_before();
+  __syncwarp();  // lanes of the role warps reconverge: bar.sync counts whole warps
   __syncthreads();
   cluster_sync();  // every CTA's barriers are initialised before any remote arrive
   tc_fence_after();
@@ -1006,6 +1016,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (threadIdx.x == 64) trace_mark(epi, 4);
   }
   tc_fence_before();
+  __syncwarp();  // lanes of the role warps reconverge: bar.sync counts whole warps
   __syncthreads();
   tc_fence_after();
   if (warp == 1) {
@@ -1294,6 +1305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     if (push) __threadfence_system();  // TP push complete before the grid ends
   }
   tc_fence_before();
+  __syncwarp();  // lanes of the role warps reconverge: bar.sync counts whole warps
   __syncthreads();
   cluster_sync();
   tc_fence_after();
@@ -1346,6 +1358,21 @@ int make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)r;
+}
+
+int make_tmap_2d_plain(CUtensorMap* map, const void* ptr, int f32, int64_t rows, int64_t cols, int box_cols,
+                       int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return -1;
+  const int esz = f32 ? 4 : 2;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * esz};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : (int)r;
 }
 
@@ -1601,6 +1628,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
   if (warp == 1) tmem_alloc(tmem_base_ptr, C::TMEM_COLS);
   tc_fence_before();
+  __syncwarp();  // lanes of the role warps reconverge: bar.sync counts whole warps
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_ptr;
@@ -1880,6 +1908,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   }
   tc_fence_before();
+  __syncwarp();  // lanes of the role warps reconverge: bar.sync counts whole warps
   __syncthreads();
   tc_fence_after();
   if (warp == 1) {

@@ -72,6 +72,9 @@ struct GemmEpi {
   // output element here -- the peer GPU's receive plane over NVLink, same layout as
   // out / resid -- and the epilogue threads end with fence.sys
   float* out2;
+  // deferred RMSNorm (decode flow path): the GEMM input was bf16(x * gamma), so the QKV
+  // epilogues (EPI_SWAP_QKV, RED_QKV) multiply token n's outputs by rvec[n] = 1/rms(x_n)
+  const float* rvec;
 };
 
 // Split count for a decode GEMM: minimises waves x K-blocks per CTA (+ a per-split reduction cost).
@@ -84,6 +87,10 @@ int gemm_decode_splits(int m_rows, int K, int num_sms);
 
 // Creates a 2D bf16 tensor map (rows x cols, row-major, 128B swizzle, box 64 x box_rows).
 int make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int box_rows);
+// Plain (unswizzled) 2D map for TMA stores / reductions from row-major smem tiles:
+// f32 (f32 != 0) or bf16 [rows][cols], box box_cols x box_rows.
+int make_tmap_2d_plain(CUtensorMap* map, const void* ptr, int f32, int64_t rows, int64_t cols, int box_cols,
+                       int box_rows);
 // General bf16 tensor map, 128B swizzle: dims[0] innermost; strides_bytes[i] of dim i+1.
 int make_tmap_bf16_nd(CUtensorMap* map, const void* ptr, int rank, const int64_t* dims, const int64_t* strides_bytes,
                       const int* box);
@@ -245,6 +252,48 @@ struct TpRowsArgs {
   unsigned long long timeout_ns;
 };
 cudaError_t tp_push_rows_launch(const TpRowsArgs& a, int num_sms, cudaStream_t s);
+
+// ------------------------------------------------------------------ decode flow
+// One persistent kernel per decoder layer runs the O projection, gate/up (+SiLU) and
+// down projection of a decode step (rows a9-a11 / a15) as a dataflow: every GEMM's
+// K blocks are spread evenly over all CTAs (split tiles summed by their last arriving
+// contributor in fixed order), and each CTA's activation loads wait on per-tile
+// readiness flags of the producing GEMM instead of a kernel boundary, while its weight
+// loads run ahead. RMSNorm is deferred: the O / down reducers write x (f32), h =
+// bf16(x * gamma_next) and per-tile sums of squares; the consumer (gate/up epilogue,
+// next QKV reduction) multiplies by 1/rms. See decode_flow.cu.
+struct FlowArgs {
+  int B;                   // tokens (<= BN)
+  int H, F, MD;            // hidden, FFN width, heads * head_dim
+  int epoch;               // flags of this launch read as ready when >= epoch
+  float eps, inv_h;
+  float* x;                // [>=B][H] f32 residual, updated in place
+  bf16* h;                 // [>=B][H] gate/up input: bf16(x * gamma_o) after O
+  bf16* h_out;             // [>=B][H] bf16(x * gamma_d) after down (next QKV / LM head input)
+  bf16* act;               // [>=B][F] silu(g) * u
+  const bf16* gamma_o;     // ffn_norm of this layer
+  const bf16* gamma_d;     // next layer's attn_norm, or the final norm
+  float* ss_o;             // [H/128][128] per-tile sums of x^2 after O
+  float* ss_d;             // [H/128][128] after down
+  float* rvec;             // [128] 1/rms(x) after down (read by the next QKV epilogue)
+  int* flags_o;            // [H/128]
+  int* flags_gu;           // [2F/128]
+  int* cnt;                // [6][cnt_ld] per-tile arrival (g) and reduced (3 + g) counters, zero at rest
+  int cnt_ld;
+  int* done_d;             // completed down tiles, zero at rest
+  float* slots;            // [3][grid][2][BN * 128] f32 partial tiles
+  int* err;                // set on a dependency-wait timeout (CTAs not co-resident)
+  unsigned long long* trace;  // debug: [grid][16] %globaltimer marks, or null
+};
+// BN (64 or 128) >= B. maps: weights (128-row boxes) of O, gate/up, down; activations
+// ao / h / act as B operands with BN-row boxes.
+// x_map: f32 x [rows][H], box 128 x 32 (TMA reduce-add of split partials); act_map: bf16
+// act [rows][F], box 64 x 32 (TMA store of the gate/up output). Both unswizzled.
+cudaError_t decode_flow_launch(const CUtensorMap* w_o, const CUtensorMap* w_gu, const CUtensorMap* w_d,
+                               const CUtensorMap* b_o, const CUtensorMap* b_gu, const CUtensorMap* b_d,
+                               const CUtensorMap* x_map, const CUtensorMap* act_map, const FlowArgs& a, int bn,
+                               int num_sms, cudaStream_t s);
+int64_t decode_flow_slot_floats(int num_sms);  // size of FlowArgs::slots
 
 // ------------------------------------------------------------------ small kernels
 // x[t] = E[clamp(ids[t], 0, V-1)] (fp32)

@@ -459,6 +459,11 @@ __global__ void splitk_reduce_kernel(int mode, const float* __restrict__ part, i
       reinterpret_cast<bf16*>(e.out)[(int64_t)row * e.ldo + c / 2] = __float2bfloat16_rn(silu_r(a) * b);
       break;
     case RED_QKV: {
+      if (e.rvec) {  // deferred RMSNorm: the input was bf16(x * gamma)
+        const float r = e.rvec[row];
+        a *= r;
+        b *= r;
+      }
       const int D = e.head_dim, half = D / 2;
       const int qd = e.n_heads * D, kd = e.n_kv * D;
       if (c < qd + kd) {

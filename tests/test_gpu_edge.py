@@ -72,11 +72,12 @@ def test_decode_batch_sizes(setup, B):
     assert inst.status()[0]["blocks_used"] == 0
 
 
-@pytest.mark.parametrize("env", ["ECOSERVE_CHAIN=1", "ECOSERVE_DEC_VARIANT=4", "ECOSERVE_PAIR_TILES=1", "ECOSERVE_DEC_R2=1",
+@pytest.mark.parametrize("env", ["ECOSERVE_FLOW=1", "ECOSERVE_CHAIN=1", "ECOSERVE_DEC_VARIANT=4", "ECOSERVE_PAIR_TILES=1", "ECOSERVE_DEC_R2=1",
                                  "ECOSERVE_ATTN_STAGES=2", "ECOSERVE_PDL=0"])
 @pytest.mark.parametrize("shape", ["tiny", "tiny-d128"])
 def test_opt_in_decode_variants_match_oracle(env, shape):
-    """The opt-in decode variants keep the per-layer A19 bar:
+    """The opt-in decode variants (ECOSERVE_FLOW=1 is the decode
+    dataflow kernel O -> gate/up -> down) keep the per-layer A19 bar:
     decode hidden states, teacher-forced on the GPU's own tokens, within 1e-2 of the
     oracle over 3 decode steps (fresh process: the switches are read once)."""
     import os

@@ -66,6 +66,36 @@ def test_fullwidth_single_gpu(name):
     assert checked >= len(prompts) * G // 2
 
 
+@pytest.mark.parametrize("B", [100, 128])
+def test_fullwidth_decode_batch_sampled(B):
+    """The decode step at bench-like batch sizes (B > 64: the 128-token tile of the decode
+    flow kernel, split tiles reduced by their last contributor) at the 8B width, 2 layers:
+    B requests decode together; a sample of them is recomputed by the oracle."""
+    from paper_2504_18154_b200.instance import Instance, device_weights_from_host
+    shape = get_shape("8b-L2")
+    w = make_weights(shape, seed=0)
+    inst = Instance(shape, device_weights_from_host(w, "cuda:0"), 512, 0, token_budget=8192, max_batch=256,
+                    max_positions=1024, debug_hidden=True)
+    lens = [int(x) for x in np.random.default_rng(B).integers(8, 90, B)]
+    prompts = random_prompts(9 + B, lens, shape.vocab)
+    first = inst.prefill([(i, p, G) for i, p in enumerate(prompts)])
+    toks, _ = inst.decode(list(range(B)), G - 1)
+    sample = [0, 1, B // 2, B - 1]
+    hd = {i: [inst.hidden(i, l, 1) for l in range(shape.n_layers + 1)] for i in sample}
+    inst.close()
+    model = T.Model(shape, w.as_f64())
+    for i in sample:
+        otoks, outs = model.generate(list(prompts[i]), G)
+        seq = [first[i]] + list(toks[i])
+        ok = all(seq[k] == otoks[k] for k in range(G))
+        if ok:  # teacher-forced equality holds: the last decode step's hidden states match
+            for l in range(shape.n_layers + 1):
+                assert rel(hd[i][l], outs[G - 1].hidden[l][-1:]) <= 1e-2, (i, l)
+        else:
+            k = next(k for k in range(G) if seq[k] != otoks[k])
+            assert T.top2_margin(outs[k].logits) <= 5e-2, (i, k)
+
+
 def _tp_worker(rank, nccl_id, q):
     import os
     import sys
@@ -113,3 +143,20 @@ def test_fullwidth_70b_tp2():
     prompts = random_prompts(5, LENS, shape.vocab)
     checked = check_against_oracle(shape, w, res[0][0], res[0][1], res[0][2], None, prompts)
     assert checked >= len(prompts) * G // 2
+
+
+def test_fullwidth_decode_flow_kernel():
+    """The opt-in decode dataflow kernel (ECOSERVE_FLOW=1: O -> gate/up -> down in one
+    persistent kernel, split tiles reduce-added into x by TMA, deferred RMSNorm) at full
+    8B / 34B widths and bench-like batches, against the same oracle bars (fresh process:
+    the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if os.environ.get("ECOSERVE_FLOW") == "1":
+        pytest.skip("already running with ECOSERVE_FLOW=1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.abspath(__file__), "-k",
+                        "single_gpu or sampled"], env={**os.environ, "ECOSERVE_FLOW": "1"}, cwd=root,
+                       capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
