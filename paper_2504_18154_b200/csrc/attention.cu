@@ -234,6 +234,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a, cons
   bf16* sQ = sV + DEC_STAGES * 64 * D;                     // [16][D]
   uint64_t* full = reinterpret_cast<uint64_t*>(sQ + 16 * D);  // [STAGES] (TMA)
   uint64_t* empty = full + DEC_STAGES;                         // [STAGES]: the 4 warps consumed the stage
+  int* s_bt = reinterpret_cast<int*>(empty + DEC_STAGES);      // (TMA) [256] this CTA's block-table range
   float* red = reinterpret_cast<float*>(sm);               // reused after the main loop
   if (TMA && threadIdx.x == 0) {
     for (int s = 0; s < DEC_STAGES; ++s) {
@@ -259,6 +260,14 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a, cons
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int g = lane >> 2, t4 = lane & 3;
 
+  // (TMA) the CTA's block-table range staged in smem by all threads at once: the issuing
+  // thread otherwise reads bt[] from global right before every refill (an L2 round trip
+  // on the critical path of each 64-token block)
+  const bool sbt = TMA && blk1 - blk0 <= 256;
+  if (sbt) {
+    for (int i = tid; i < blk1 - blk0; i += 128) s_bt[i] = bt[blk0 + i];
+    __syncthreads();
+  }
   // q rows: head kvh*G + r for r < G, zero rows above
   for (int i = tid; i < 16 * (D / 8); i += 128) {
     const int r = i / (D / 8), c = i % (D / 8);
@@ -270,7 +279,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a, cons
     if constexpr (TMA) {
       if (tid == 0) {
         // pool rows: ((block * L + layer) * 2 + kv) * Mkv * 64 + kvh * 64 + token
-        const int64_t base = ((int64_t)bt[blk] * a.n_layers + a.layer) * 2;
+        const int64_t base = ((int64_t)(sbt ? s_bt[blk - blk0] : bt[blk]) * a.n_layers + a.layer) * 2;
         const int krow = (int)((base * a.n_kv + kvh) * 64);
         const int vrow = (int)(((base + 1) * a.n_kv + kvh) * 64);
         mbar_arrive_expect_tx(&full[st], 2 * 64 * D * 2);
@@ -336,11 +345,16 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a, cons
       mma_bf16_16816(s[0], qf[kk], b0, b1);
       mma_bf16_16816(s[1], qf[kk], b2, b3);
     }
+    // Rows 8..15 of the MMA (accumulator elements 2, 3) hold heads 8..15 of the group:
+    // with G <= 8 (every shape here) they are padding, so their max / exp / rescale work
+    // is skipped and their P is zero (the decode step is issue-bound at power-capped clocks)
+    const bool hi_rows = G > 8;  // block-uniform
     float mnew[2] = {mrow[0], mrow[1]};
 #pragma unroll
     for (int n = 0; n < 2; ++n)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
+        if (e >= 2 && !hi_rows) continue;
         const int kpos = blk * 64 + warp * 16 + n * 8 + 2 * t4 + (e & 1);
         float v = (kpos < ctx) ? s[n][e] * a.scale_log2 : -INFINITY;
         s[n][e] = v;
@@ -348,19 +362,26 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a, cons
       }
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
+      if (r == 1 && !hi_rows) continue;
       mnew[r] = fmaxf(mnew[r], __shfl_xor_sync(0xffffffffu, mnew[r], 1));
       mnew[r] = fmaxf(mnew[r], __shfl_xor_sync(0xffffffffu, mnew[r], 2));
     }
-    float corr[2], rs[2] = {0.f, 0.f};
+    float corr[2] = {1.f, 1.f}, rs[2] = {0.f, 0.f};
 #pragma unroll
-    for (int r = 0; r < 2; ++r) corr[r] = (mrow[r] == -INFINITY) ? 0.f : exp2f(mrow[r] - mnew[r]);
+    for (int r = 0; r < 2; ++r) {
+      if (r == 1 && !hi_rows) continue;
+      corr[r] = (mrow[r] == -INFINITY) ? 0.f : exp2f(mrow[r] - mnew[r]);
+    }
     uint32_t af[4];
 #pragma unroll
     for (int n = 0; n < 2; ++n) {
       float p0 = (mnew[0] == -INFINITY) ? 0.f : exp2f(s[n][0] - mnew[0]);
       float p1 = (mnew[0] == -INFINITY) ? 0.f : exp2f(s[n][1] - mnew[0]);
-      float p2 = (mnew[1] == -INFINITY) ? 0.f : exp2f(s[n][2] - mnew[1]);
-      float p3 = (mnew[1] == -INFINITY) ? 0.f : exp2f(s[n][3] - mnew[1]);
+      float p2 = 0.f, p3 = 0.f;
+      if (hi_rows) {
+        p2 = (mnew[1] == -INFINITY) ? 0.f : exp2f(s[n][2] - mnew[1]);
+        p3 = (mnew[1] == -INFINITY) ? 0.f : exp2f(s[n][3] - mnew[1]);
+      }
       rs[0] += p0 + p1;
       rs[1] += p2 + p3;
       af[n * 2 + 0] = pack_bf16x2(p0, p1);
@@ -371,10 +392,13 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a, cons
       lrow[r] = lrow[r] * corr[r] + rs[r];
       mrow[r] = mnew[r];
     }
+    // rescale O only when some row of the warp raised its max (rare after the first blocks)
+    if (__any_sync(0xffffffffu, corr[0] != 1.f || corr[1] != 1.f)) {
 #pragma unroll
-    for (int i = 0; i < ND; ++i) {
-      o[i][0] *= corr[0]; o[i][1] *= corr[0];
-      o[i][2] *= corr[1]; o[i][3] *= corr[1];
+      for (int i = 0; i < ND; ++i) {
+        o[i][0] *= corr[0]; o[i][1] *= corr[0];
+        o[i][2] *= corr[1]; o[i][3] *= corr[1];
+      }
     }
 #pragma unroll
     for (int dn = 0; dn < ND; dn += 2) {
@@ -486,7 +510,7 @@ static cudaError_t decode_st(const DecodeAttnArgs& a, cudaStream_t s) {
   int smem = (2 * ST * 64 * D + 16 * D) * 2;
   const int red_bytes = 4 * 16 * (D + 2) * 4;
   if (smem < red_bytes) smem = red_bytes;
-  if (tma) smem += 1024 + 64;  // 1 KB alignment slack + stage barriers
+  if (tma) smem += 1024 + 64 + 256 * 4;  // 1 KB alignment slack + stage barriers + block-table range
   cudaError_t e = tma ? ensure_smem(attn_decode_kernel<D, true, ST>, smem)
                       : ensure_smem(attn_decode_kernel<D, false, ST>, smem);
   if (e != cudaSuccess) return e;

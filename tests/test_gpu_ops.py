@@ -240,7 +240,9 @@ def test_attention_prefill_chunked(ops, tc, M, Mkv):
 @pytest.mark.parametrize("D,M,Mkv,splits,bps,tma", [(128, 32, 8, 1, 64, False), (128, 32, 8, 4, 5, False),
                                                      (32, 8, 2, 3, 7, False), (128, 64, 8, 2, 9, False),
                                                      (64, 4, 4, 1, 64, False), (128, 32, 8, 1, 64, True),
-                                                     (128, 32, 8, 4, 5, True), (128, 64, 8, 2, 9, True)])
+                                                     (128, 32, 8, 4, 5, True), (128, 64, 8, 2, 9, True),
+                                                     # G = 16 q heads per kv head: MMA rows 8..15 are real heads
+                                                     (128, 32, 2, 1, 64, True), (64, 16, 1, 2, 9, False)])
 def test_attention_decode(ops, D, M, Mkv, splits, bps, tma):
     rng = np.random.default_rng(D * 3 + splits)
     ctx = [1, 64, 65, 300, 1000][: 5]
