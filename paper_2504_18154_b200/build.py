@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libecoserve.so")
-SOURCES = ["gemm_sm100.cu", "attention.cu", "attention_tc.cu", "small_kernels.cu", "decode_flow.cu", "engine.cu", "ops.cu",
+SOURCES = ["gemm_sm100.cu", "attention.cu", "attention_tc.cu", "small_kernels.cu", "decode_flow.cu", "decode_gu.cu", "engine.cu", "ops.cu",
            "sched.cpp"]
 HEADERS = ["common.cuh", "kernels.h", "launch.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

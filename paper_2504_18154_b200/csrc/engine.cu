@@ -216,6 +216,16 @@ struct ecoserve_instance {
   int* h_flow_err = nullptr;                 // pinned copy, read after every decode step
   int flow_epoch = 0;
   unsigned long long* flow_trace = nullptr;  // ECOSERVE_FLOW_TRACE (debug)
+  // decode gate/up, stream-K (decode_gu.cu)
+  bool gu_sk = false;
+  float* gu_part = nullptr;                  // [2F][128] f32 tail partials
+  int* gu_flags = nullptr;                   // [2F/128]
+  int gu_epoch = 0;
+  int* gu_err = nullptr;
+  int* h_gu_err = nullptr;                   // pinned copy, read after every decode step
+  CUtensorMap gu_actmap, gu_partmap;
+  unsigned long long* gu_trace = nullptr;    // ECOSERVE_GU_TRACE (debug)
+  int gu_trace_layer = -1;                   // layer being enqueued (trace: layer 5)
   CUtensorMap flow_xmap, flow_actmap;         // x (f32, TMA reduce-add target), act (bf16, TMA store)
 
   bool fail(const char* what, cudaError_t e) {
@@ -296,6 +306,27 @@ static bool flow_env_enabled() {
 static const char* flow_trace_path() {
   static const char* p = getenv("ECOSERVE_FLOW_TRACE");
   return p;
+}
+
+// debug: ECOSERVE_GU_TRACE=path appends per-CTA marks of the gate/up stream-K kernel
+// (the launch of layer 5 of each decode step; see tools/flow_trace.py --gu)
+static const char* gu_trace_path() {
+  static const char* p = getenv("ECOSERVE_GU_TRACE");
+  return p;
+}
+
+// ECOSERVE_GU_SK=1 enables the stream-K decode gate/up kernel (decode_gu.cu). Off by
+// default: parity-green, its mainloop streams at 6.3 TB/s (8B), but the step measured
+// slower (8B B = 128: 7.76 vs 7.47 ms; 70B rank shard: 22.5 vs 21.8 ms) -- every CTA now
+// ends together, while in the 1.5-wave GEMM the CTAs done after one tile already run
+// the down projection's prologue and weight prefetch under PDL.
+static bool gu_sk_env_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_GU_SK");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
 }
 
 // gate/up flags start on a 128-byte boundary after the O flags (pollers read 16-B vectors)
@@ -436,6 +467,9 @@ void ecoserve_instance_destroy(ecoserve_instance* inst) {
   if (inst->h_chain_err) cudaFreeHost(inst->h_chain_err);
   if (inst->h_tp_err) cudaFreeHost(inst->h_tp_err);
   if (inst->h_flow_err) cudaFreeHost(inst->h_flow_err);
+  if (inst->h_gu_err) cudaFreeHost(inst->h_gu_err);
+  for (void* p : {(void*)inst->gu_part, (void*)inst->gu_flags, (void*)inst->gu_err, (void*)inst->gu_trace})
+    if (p) cudaFree(p);
   for (void* p : {(void*)inst->flow_slots, (void*)inst->flow_flags, (void*)inst->flow_cnt, (void*)inst->flow_ss,
                   (void*)inst->flow_rvec, (void*)inst->flow_err, (void*)inst->flow_trace})
     if (p) cudaFree(p);
@@ -691,6 +725,21 @@ ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, cons
     CK(cudaMallocHost(&inst->h_flow_err, sizeof(int)));
     *inst->h_flow_err = 0;
     inst->flow = true;
+  }
+  if (gu_sk_env_enabled() && F % 64 == 0 && H % 64 == 0) {
+    CK(cudaMalloc(&inst->gu_part, sizeof(float) * 2LL * F * 128));
+    CK(cudaMalloc(&inst->gu_flags, sizeof(int) * (2 * F / 128 + 1)));
+    CK(cudaMemset(inst->gu_flags, 0, sizeof(int) * (2 * F / 128 + 1)));
+    CK(cudaMalloc(&inst->gu_err, sizeof(int)));
+    CK(cudaMemset(inst->gu_err, 0, sizeof(int)));
+    CK(cudaMallocHost(&inst->h_gu_err, sizeof(int)));
+    *inst->h_gu_err = 0;
+    if (make_tmap_2d_plain(&inst->gu_actmap, inst->act, 0, inst->T_max, F, 64, 32) ||
+        make_tmap_2d_plain(&inst->gu_partmap, inst->gu_part, 1, 2LL * F, 128, 128, 32)) {
+      inst->err = "gate/up stream-K: tensor map creation failed";
+      return ECOSERVE_ERR_CUDA;
+    }
+    inst->gu_sk = true;
   }
   device_instances(device, +1);  // (a failed create is not counted)
   inst->registered = true;
@@ -987,6 +1036,15 @@ int decode_splits_r2(int n_out, int K, int num_sms) {
   return best;
 }
 
+unsigned long long* gu_trace_buf(ecoserve_instance* inst) {
+  if (!gu_trace_path() || inst->gu_trace_layer != 5) return nullptr;
+  if (!inst->gu_trace) {
+    if (cudaMalloc(&inst->gu_trace, sizeof(unsigned long long) * inst->num_sms * 16) != cudaSuccess) return nullptr;
+    cudaMemset(inst->gu_trace, 0, sizeof(unsigned long long) * inst->num_sms * 16);
+  }
+  return inst->gu_trace;
+}
+
 cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const ActMaps& xm, int n_out, int K, int B,
                         int mode, GemmEpi e, int* nk, const bf16* norm_gamma = nullptr, bf16* norm_out = nullptr,
                         bool* fused = nullptr, const CUtensorMap* wmap256 = nullptr) {
@@ -1003,6 +1061,22 @@ cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const 
     e.mode = mode;
     *nk = 1;
     return gemm_launch_r(wm, &xm.b[bn_index(bn)], n_out, B, K, bn, 2, 1, e, inst->num_sms, inst->stream);
+  }
+  if (splits == 1 && mode == EPI_SWAP_SILU && inst->gu_sk && gu_sk_applicable(n_out, K, B, inst->num_sms) &&
+      device_instances(inst->device, 0) == 1) {
+    // more weight tiles than SMs: balanced stream-K with deterministic two-way tile sums
+    // (decode_gu.cu); its CTAs wait on each other, so only while alone on the GPU
+    GuSkArgs ga;
+    ga.m_rows = n_out;
+    ga.K = K;
+    ga.B = B;
+    ga.epoch = ++inst->gu_epoch;
+    ga.flags = inst->gu_flags;
+    ga.err = inst->gu_err;
+    ga.trace = gu_trace_buf(inst);
+    *nk = 1;
+    return gu_sk_launch(&wmap, &xm.b[bn_index(bn)], &inst->gu_actmap, &inst->gu_partmap, ga, bn, inst->num_sms,
+                        inst->stream);
   }
   if (splits == 1) {  // epilogue in the GEMM
     e.mode = mode;
@@ -1566,6 +1640,7 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     eg.out = inst->act;
     eg.ldo = F;
     set_prefetch(inst, eg, 4 * l + 3, H, F, B);  // down next
+    inst->gu_trace_layer = l;
     LAUNCH(P_GEMM_DECODE, 2.0 * 2 * F * H, nk,
            decode_gemm(inst, w.gu_a, inst->m_h, 2 * F, H, B, EPI_SWAP_SILU, eg, &nk, nullptr, nullptr, nullptr, &w.gu_b));
     // the down projection's reduction also applies the next RMSNorm: the next layer's
@@ -2098,9 +2173,31 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
     CK(cudaMemcpyAsync(inst->h_tokens, inst->d_tokens, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
     if (inst->chain) CK(cudaMemcpyAsync(inst->h_chain_err, inst->chain_err, sizeof(int), cudaMemcpyDeviceToHost, st));
     if (inst->flow) CK(cudaMemcpyAsync(inst->h_flow_err, inst->flow_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (inst->gu_sk) CK(cudaMemcpyAsync(inst->h_gu_err, inst->gu_err, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(copy_step_flags(inst));
     const auto t_enq1 = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(st));
+    if (inst->gu_trace && gu_trace_path()) {  // debug: "cta mark t_ns" of layer 5's gate/up launch
+      std::vector<unsigned long long> tr((size_t)inst->num_sms * 16);
+      CK(cudaMemcpy(tr.data(), inst->gu_trace, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost));
+      unsigned long long t0 = ~0ull;
+      for (int c = 0; c < inst->num_sms; ++c) if (tr[c * 16]) t0 = std::min(t0, tr[c * 16]);
+      FILE* f = fopen(gu_trace_path(), "a");
+      if (f) {
+        fprintf(f, "# B=%d\n", B);
+        for (int c = 0; c < inst->num_sms; ++c)
+          for (int k = 0; k < 8; ++k)
+            if (tr[c * 16 + k] >= t0) fprintf(f, "%d %d %llu\n", c, k, tr[c * 16 + k] - t0);
+        fclose(f);
+      }
+      CK(cudaMemset(inst->gu_trace, 0, sizeof(unsigned long long) * tr.size()));
+    }
+    if (inst->gu_sk && *inst->h_gu_err) {
+      inst->err = "decode gate/up stream-K: a partial-tile wait timed out (CTAs not co-resident; ECOSERVE_GU_SK=0 "
+                  "disables it)";
+      inst->dead = true;
+      return ECOSERVE_ERR_CUDA;
+    }
     if (inst->flow && *inst->h_flow_err) {
       inst->err = "decode flow: a dependency wait timed out (CTAs not co-resident; ECOSERVE_FLOW=0 disables it)";
       inst->dead = true;

@@ -295,6 +295,23 @@ cudaError_t decode_flow_launch(const CUtensorMap* w_o, const CUtensorMap* w_gu, 
                                int num_sms, cudaStream_t s);
 int64_t decode_flow_slot_floats(int num_sms);  // size of FlowArgs::slots
 
+// ------------------------------------------------------------------ decode gate/up, stream-K
+// (decode_gu.cu) act = silu(gate) * up of W_gu [m_rows = 2F][K = H] x h [B][H], every
+// CTA streaming the same number of weight K blocks; a tile split between two CTAs is
+// finished by the head's owner from the tail's partial (flags[t] >= epoch) -- a
+// two-term sum, bitwise deterministic.
+struct GuSkArgs {
+  int m_rows, K, B, epoch;
+  int* flags;              // [m_rows / 128], epoch of the tail partial's store
+  int* err;                // set on a flag-wait timeout (CTAs not co-resident)
+  unsigned long long* trace;  // debug: [grid][16] %globaltimer marks, or null
+};
+bool gu_sk_applicable(int m_rows, int K, int B, int num_sms);
+// w_map: W_gu (128-row boxes, SW128), x_map: h as B operand (bn-row box), act_map: bf16
+// act [rows][F] box 64 x 32 (plain), part_map: f32 partials [m_rows][128] box 128 x 32.
+cudaError_t gu_sk_launch(const CUtensorMap* w_map, const CUtensorMap* x_map, const CUtensorMap* act_map,
+                         const CUtensorMap* part_map, const GuSkArgs& a, int bn, int num_sms, cudaStream_t s);
+
 // ------------------------------------------------------------------ small kernels
 // x[t] = E[clamp(ids[t], 0, V-1)] (fp32)
 cudaError_t embed_launch(const int* ids, const bf16* E, float* x, int n, int H, int V, cudaStream_t s);

@@ -145,6 +145,22 @@ def test_fullwidth_70b_tp2():
     assert checked >= len(prompts) * G // 2
 
 
+def test_fullwidth_decode_gu_stream_k():
+    """The opt-in stream-K gate/up kernel (ECOSERVE_GU_SK=1: 224 / 344 tiles balanced over
+    the SMs, tiles split between two CTAs summed deterministically) at the 8B and 34B
+    widths, same oracle bars (fresh process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if os.environ.get("ECOSERVE_GU_SK") == "1":
+        pytest.skip("already running with ECOSERVE_GU_SK=1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.abspath(__file__), "-k",
+                        "single_gpu or sampled"], env={**os.environ, "ECOSERVE_GU_SK": "1"}, cwd=root,
+                       capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 def test_fullwidth_decode_flow_kernel():
     """The opt-in decode dataflow kernel (ECOSERVE_FLOW=1: O -> gate/up -> down in one
     persistent kernel, split tiles reduce-added into x by TMA, deferred RMSNorm) at full

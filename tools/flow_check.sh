@@ -1,5 +1,4 @@
-timeout 600 python -m pytest -q -x tests/test_gpu_ops.py -k "attention_decode" 2>&1 | tail -2
 for i in 1 2; do
-timeout 300 python tools/decode_ablate.py --one
-ECOSERVE_ABLATE=1 timeout 300 python tools/decode_ablate.py --one
+timeout 900 python tools/tp_bench.py --tp1 --reps 2
+ECOSERVE_GU_SK=0 timeout 900 python tools/tp_bench.py --tp1 --reps 2
 done

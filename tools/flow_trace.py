@@ -11,7 +11,12 @@ NAMES = ["start", "first weights", "O mma done", "GU mma done", "down mma done",
          "O reducer chunk0 loads", "O reducer chunk0 stores", "O reducer all chunks", "O reducer chunk0 slots"]
 
 
+GU_NAMES = ["start", "first stage", "last MMA", "tail published", "head flag seen", "head partial landed",
+            "epilogue done", "end"]
+
+
 def main(path):
+    names = GU_NAMES if "--gu" in sys.argv else NAMES
     runs, cur = [], None
     for line in open(path):
         if line.startswith("#"):
@@ -22,11 +27,11 @@ def main(path):
         cur[int(k)].append(int(t) / 1e3)
     r = runs[-1]
     print(f"{len(runs)} traced launches; the last one:")
-    for k, n in enumerate(NAMES):
+    for k, n in enumerate(names):
         v = np.array(r.get(k, []))
         if len(v):
             print(f"  {k:2d} {n:22s} min {v.min():8.2f}  med {np.median(v):8.2f}  max {v.max():8.2f} us  ({len(v)} CTAs)")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main([a for a in sys.argv[1:] if not a.startswith("--")][0])
