@@ -175,6 +175,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     """Load the CUDA library (no fallback: raises if it is missing)."""
     global _lib
     if _lib is None:
+        path = os.environ.get("ECOSERVE_LIB_AB", path)  # A/B timing of two builds only (tools/)
         if not os.path.exists(path):
             raise ImportError(f"{path} is missing: run `python -m paper_2504_18154_b200.build` "
                               "(the hot path has no CPU fallback)")

@@ -263,23 +263,17 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a, cons
   // (TMA) the CTA's block-table range staged in smem by all threads at once: the issuing
   // thread otherwise reads bt[] from global right before every refill (an L2 round trip
   // on the critical path of each 64-token block)
+  // (the first refill reads it after the prologue barrier; the prologue loads below read
+  // bt[] directly, so the first K/V loads go out before any other global round trip)
   const bool sbt = TMA && blk1 - blk0 <= 256;
-  if (sbt) {
+  if (sbt)
     for (int i = tid; i < blk1 - blk0; i += 128) s_bt[i] = bt[blk0 + i];
-    __syncthreads();
-  }
-  // q rows: head kvh*G + r for r < G, zero rows above
-  for (int i = tid; i < 16 * (D / 8); i += 128) {
-    const int r = i / (D / 8), c = i % (D / 8);
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < G) v = *reinterpret_cast<const uint4*>(a.q + ((int64_t)b * a.n_heads + kvh * G + r) * D + c * 8);
-    *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sQ) + swz<D>(r, c) * 16) = v;
-  }
   auto issue = [&](int blk, int st) {
     if constexpr (TMA) {
       if (tid == 0) {
         // pool rows: ((block * L + layer) * 2 + kv) * Mkv * 64 + kvh * 64 + token
-        const int64_t base = ((int64_t)(sbt ? s_bt[blk - blk0] : bt[blk]) * a.n_layers + a.layer) * 2;
+        const int64_t base =
+            ((int64_t)((sbt && blk >= blk0 + DEC_STAGES - 1) ? s_bt[blk - blk0] : bt[blk]) * a.n_layers + a.layer) * 2;
         const int krow = (int)((base * a.n_kv + kvh) * 64);
         const int vrow = (int)(((base + 1) * a.n_kv + kvh) * 64);
         mbar_arrive_expect_tx(&full[st], 2 * 64 * D * 2);
@@ -299,11 +293,18 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a, cons
     if constexpr (TMA) return tma_swz(r, c);
     else return (uint32_t)swz<D>(r, c) * 16;
   };
-  // prologue
+  // prologue: the first K/V blocks, then the q rows (their loads overlap)
 #pragma unroll
   for (int s = 0; s < DEC_STAGES - 1; ++s) {
     if (blk0 + s < blk1) issue(blk0 + s, s);
     if (!TMA) cp_async_commit();
+  }
+  // q rows: head kvh*G + r for r < G, zero rows above
+  for (int i = tid; i < 16 * (D / 8); i += 128) {
+    const int r = i / (D / 8), c = i % (D / 8);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < G) v = *reinterpret_cast<const uint4*>(a.q + ((int64_t)b * a.n_heads + kvh * G + r) * D + c * 8);
+    *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sQ) + swz<D>(r, c) * 16) = v;
   }
   __syncthreads();
   uint32_t qf[NK][4];
