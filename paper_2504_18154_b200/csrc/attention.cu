@@ -293,20 +293,71 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a, cons
     if constexpr (TMA) return tma_swz(r, c);
     else return (uint32_t)swz<D>(r, c) * 16;
   };
+  const bool fused_qkv = TMA && a.qkv_part != nullptr;  // (kernel-uniform)
+  // the current token's K / V are written by this CTA (fused QKV) into the last block:
+  // that block's TMA load must follow the writes
+  const bool writes_kv = fused_qkv && blk1 == n_blocks;
+  const int late = writes_kv ? n_blocks - 1 : -1;  // block whose load waits for the K / V write
   // prologue: the first K/V blocks, then the q rows (their loads overlap)
 #pragma unroll
   for (int s = 0; s < DEC_STAGES - 1; ++s) {
-    if (blk0 + s < blk1) issue(blk0 + s, s);
+    if (blk0 + s < blk1 && blk0 + s != late) issue(blk0 + s, s);
     if (!TMA) cp_async_commit();
   }
-  // q rows: head kvh*G + r for r < G, zero rows above
-  for (int i = tid; i < 16 * (D / 8); i += 128) {
-    const int r = i / (D / 8), c = i % (D / 8);
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < G) v = *reinterpret_cast<const uint4*>(a.q + ((int64_t)b * a.n_heads + kvh * G + r) * D + c * 8);
-    *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sQ) + swz<D>(r, c) * 16) = v;
+  if (fused_qkv) {
+    // q = RoPE(sum of the splits) for the G heads, and the new k (RoPE) / v row
+    const int half = D / 2, qd = a.n_heads * D, kd = a.n_kv * D;
+    const int p = a.pos[b];
+    const int64_t plane = (int64_t)a.B * a.qkv_ld;
+    const float* src = a.qkv_part + (int64_t)b * a.qkv_ld;
+    if (tid < 16 * (D / 8) - G * (D / 8))  // zero q rows G..15
+      for (int i = G * (D / 8) + tid; i < 16 * (D / 8); i += 128) {
+        const int r = i / (D / 8), c = i % (D / 8);
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sQ) + swz<D>(r, c) * 16) = make_uint4(0, 0, 0, 0);
+      }
+    for (int i = tid; i < (G + 2) * half; i += 128) {
+      const int r = i / half, j = i % half;  // r < G: q head; G: k; G + 1: v (pair j = columns 2j, 2j + 1)
+      const int col = r < G ? (kvh * G + r) * D + 2 * j : r == G ? qd + kvh * D + 2 * j : qd + kd + kvh * D + 2 * j;
+      float x0 = 0.f, x1 = 0.f;
+      for (int sp = 0; sp < a.qkv_splits; ++sp) {  // split order, as the reduction kernel
+        const float2 v = *reinterpret_cast<const float2*>(src + sp * plane + col);
+        x0 += v.x;
+        x1 += v.y;
+      }
+      if (r <= G) {
+        const float cs = a.rope_cos[(int64_t)p * half + j], sn = a.rope_sin[(int64_t)p * half + j];
+        const float y0 = x0 * cs - x1 * sn, y1 = x1 * cs + x0 * sn;  // dims j and j + D/2
+        if (r < G) {
+          uint8_t* q8 = reinterpret_cast<uint8_t*>(sQ);
+          *reinterpret_cast<bf16*>(q8 + swz<D>(r, j / 8) * 16 + (j % 8) * 2) = __float2bfloat16_rn(y0);
+          *reinterpret_cast<bf16*>(q8 + swz<D>(r, (j + half) / 8) * 16 + ((j + half) % 8) * 2) = __float2bfloat16_rn(y1);
+        } else if (writes_kv) {
+          const int sl = a.slot[b];
+          bf16* dst = const_cast<bf16*>(a.k_cache) + (int64_t)(sl >> 6) * a.blk_stride + ((int64_t)kvh * 64 + (sl & 63)) * D;
+          dst[j] = __float2bfloat16_rn(y0);
+          dst[j + half] = __float2bfloat16_rn(y1);
+        }
+      } else if (writes_kv) {
+        const int sl = a.slot[b];
+        bf16* dst = const_cast<bf16*>(a.v_cache) + (int64_t)(sl >> 6) * a.blk_stride + ((int64_t)kvh * 64 + (sl & 63)) * D;
+        *reinterpret_cast<uint32_t*>(dst + 2 * j) = pack_bf16x2(x0, x1);
+      }
+    }
+    if (writes_kv) asm volatile("fence.proxy.async.global;" ::: "memory");  // generic K/V writes -> TMA reads
+  } else {
+    // q rows: head kvh*G + r for r < G, zero rows above
+    for (int i = tid; i < 16 * (D / 8); i += 128) {
+      const int r = i / (D / 8), c = i % (D / 8);
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (r < G) v = *reinterpret_cast<const uint4*>(a.q + ((int64_t)b * a.n_heads + kvh * G + r) * D + c * 8);
+      *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sQ) + swz<D>(r, c) * 16) = v;
+    }
   }
   __syncthreads();
+  if (late >= blk0 && late < blk0 + DEC_STAGES - 1) {  // the last block was held back: load it now
+    if (tid == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+    issue(late, late - blk0);
+  }
   uint32_t qf[NK][4];
   {
     const uint32_t qb = smem_u32(sQ);

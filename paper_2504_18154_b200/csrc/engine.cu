@@ -290,6 +290,20 @@ static int device_instances(int device, int delta) {
   return n[device] += delta;
 }
 
+// ECOSERVE_QKV_FUSE=1: the decode QKV split reduction (RoPE, K/V append) inside the
+// attention kernel's prologue instead of its own kernel. Off by default: parity-green but
+// measured slower (8B B = 128: 7.93-8.02 vs 7.73-7.80 ms per step) -- the pos -> RoPE
+// table round trips delay every attention CTA's first MMA by more than the reduction
+// kernel costs.
+static bool qkv_fuse_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_QKV_FUSE");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 // ECOSERVE_FLOW=1 enables the decode flow kernel (decode_flow.cu). Off by default: it is
 // parity-green but measured slower than the per-kernel decode path (8B, B = 128, ctx 1.3k:
 // 9.09 vs 7.7 ms per decode step).
@@ -1586,11 +1600,28 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     e.v_cache = v_layer(inst, l);
     int nk = 0;
     const int abl = ablate_mask();
-    if (!(abl & 4))
-      LAUNCH(P_GEMM_DECODE, 2.0 * inst->QKV * H, nk,
-             decode_gemm(inst, w.qkv_a, inst->m_h, inst->QKV, H, B, EPI_SWAP_QKV, e, &nk, nullptr, nullptr, nullptr,
-                         &w.qkv_b));
+    // QKV split partials reduced (+ RoPE, K/V append) inside the attention kernel (TMA path)
+    const bool fuse_qkv = qkv_fuse_enabled() && inst->attn_tc && D == 128;
+    int qkv_sp = 0;
+    if (!(abl & 4)) {
+      if (fuse_qkv)
+        LAUNCH(P_GEMM_DECODE, 2.0 * inst->QKV * H, 1,
+               decode_partials(inst, w.qkv_a, inst->m_h, inst->QKV, H, B, &qkv_sp));
+      else
+        LAUNCH(P_GEMM_DECODE, 2.0 * inst->QKV * H, nk,
+               decode_gemm(inst, w.qkv_a, inst->m_h, inst->QKV, H, B, EPI_SWAP_QKV, e, &nk, nullptr, nullptr, nullptr,
+                           &w.qkv_b));
+    }
     DecodeAttnArgs a;
+    if (fuse_qkv && qkv_sp > 0) {
+      a.qkv_part = inst->part;
+      a.qkv_splits = qkv_sp;
+      a.qkv_ld = inst->QKV;
+      a.pos = d_pos;
+      a.slot = d_slot;
+      a.rope_cos = inst->rope_cos;
+      a.rope_sin = inst->rope_sin;
+    }
     a.q = inst->q;
     a.k_cache = k_layer(inst, l);
     a.v_cache = v_layer(inst, l);

@@ -215,6 +215,17 @@ struct DecodeAttnArgs {
   // locate the layer in the block-major pool
   const CUtensorMap* kvmap;
   int layer, n_layers;
+  // optional (TMA path): the QKV projection's split-K f32 partials [qkv_splits][B][qkv_ld]
+  // instead of q -- each CTA sums its q heads and its kv head's new k / v row in split
+  // order, applies RoPE (pair-interleaved prepared rows, tables rope_cos / rope_sin at
+  // pos[b]) and writes the new K / V into the pool at slot[b] itself (the split that owns
+  // the last block), replacing the separate reduction kernel (a13)
+  const float* qkv_part = nullptr;
+  int qkv_splits = 0, qkv_ld = 0;
+  const int* pos = nullptr;
+  const int* slot = nullptr;
+  const float* rope_cos = nullptr;
+  const float* rope_sin = nullptr;
 };
 cudaError_t attn_decode_launch(const DecodeAttnArgs& a, int head_dim, cudaStream_t s);
 
