@@ -83,8 +83,15 @@ class Clock:
 class Worker(threading.Thread):
     def __init__(self, idx: int, inst, clock: Clock, status_q: "queue.Queue", token_budget: int,
                  decode_steps_per_poll: int = 1, max_batch: int = 256, hybrid_budget: int = 0,
-                 role: str = "both", handoff=None):
+                 role: str = "both", handoff=None, admission: str = "reserve"):
         super().__init__(daemon=True)
+        # "reserve": FCFS reservation of prompt + output blocks (no preemption ever needed);
+        # "preempt": reading A14 -- admit on the prompt's blocks, and before a decode step that
+        # would outgrow the pool preempt the latest arrivals for recompute (as oracle/des.py)
+        if admission not in ("reserve", "preempt"):
+            raise ValueError(f"unknown admission {admission!r}")
+        self.admission = admission
+        self.n_preempted = 0
         self.hybrid_budget = hybrid_budget   # > 0: Sarathi-style hybrid iterations
         self.role = role                     # "both" | "prefill" | "decode" (FuDG)
         self.handoff = handoff               # FuDG prefill role: () -> the decode Worker for the next request
@@ -111,9 +118,28 @@ class Worker(threading.Thread):
         self.committed: Dict[int, int] = {}
         self.commit_sum = 0
 
-    def _fits(self, r: LiveReq) -> bool:
+    def _fits(self, r: LiveReq, extra: int = 0) -> bool:
+        if self.admission == "preempt":  # the prompt (plus regenerated tokens) must fit now
+            return self._held() + extra + (r.S + r.n_gen + 63) // 64 <= self.total_blocks
         return r.req_id in self.committed or \
             self.commit_sum + (r.S + r.G + 63) // 64 <= self.total_blocks
+
+    def _held(self) -> int:
+        """Blocks the engine holds for prefilled requests: prompt + fed tokens (A14)."""
+        return sum((r.S + r.n_gen - 1 + 63) // 64 for r in self.waiting + self.running)
+
+    def _preempt_for(self, steps: int) -> None:
+        """Reading A14 in live mode: while the running batch would need more blocks than the
+        pool after `steps` decode steps, release the latest-arrived request and put it at the
+        front of the queue; its recompute prefill feeds prompt + every generated token."""
+        def need():
+            return sum((r.S + min(r.n_gen + steps, r.G) - 1 + 63) // 64 for r in self.running)
+        while len(self.running) > 1 and need() > self.total_blocks:
+            v = max(self.running, key=lambda r: (r.arrival_ns, r.req_id))
+            self.running.remove(v)
+            self.inst.release([v.req_id])
+            self.pending.appendleft(v)
+            self.n_preempted += 1
 
     def _commit(self, r: LiveReq) -> None:
         if r.req_id not in self.committed:
@@ -214,23 +240,31 @@ class Worker(threading.Thread):
             if self.pending and self._fits(self.pending[0]):
                 if self.phase != PREFILL:
                     self.phase, self.t_switch = PREFILL, self.clock.now()
-                batch, tok = [], 0
+                batch, tok, extra = [], 0, 0
                 while self.pending and len(batch) < self.max_batch and \
-                        (not batch or tok + self.pending[0].S <= self.budget) and self._fits(self.pending[0]):
+                        (not batch or tok + self.pending[0].S + self.pending[0].n_gen <= self.budget) and \
+                        self._fits(self.pending[0], extra):
                     r = self.pending.popleft()
                     self._commit(r)
                     batch.append(r)
-                    tok += r.S
+                    tok += r.S + r.n_gen
+                    extra += (r.S + r.n_gen + 63) // 64  # (preempt admission: blocks of this batch)
                 t0 = self.clock.now()
-                first = self.inst.prefill([(r.req_id, r.prompt, r.G) for r in batch])
+                # a recompute (A14) prefills the prompt and every generated token; the engine
+                # request then owes the remaining G - n_gen tokens
+                first = self.inst.prefill([(r.req_id, self._prefill_ids(r), r.G - r.n_gen) for r in batch])
                 t = self.clock.now()
                 self.timeline.append((t0, t, "prefill", len(batch)))
                 fin = []
                 for r, f in zip(batch, first):
-                    r.t_first_ns, r.n_gen = t, 1
+                    if r.n_gen == 0:
+                        r.t_first_ns = t
+                    r.n_gen += 1
                     r.tokens.append(int(f))
-                    if r.G <= 1:
-                        r.t_decode_begin_ns = r.t_done_ns = t
+                    if r.n_gen >= r.G:
+                        if r.t_decode_begin_ns < 0:
+                            r.t_decode_begin_ns = t
+                        r.t_done_ns = t
                         fin.append(r)
                     elif self.role == "prefill":  # FuDG: the KV moves to a decode instance
                         dst = self.handoff()
@@ -245,9 +279,12 @@ class Worker(threading.Thread):
                 if self.phase != DECODE:
                     self.phase, self.t_switch = DECODE, self.clock.now()
                     for r in self.waiting:
-                        r.t_decode_begin_ns = self.t_switch
+                        if r.t_decode_begin_ns < 0:
+                            r.t_decode_begin_ns = self.t_switch
                     self.running += self.waiting
                     self.waiting = []
+                if self.admission == "preempt":
+                    self._preempt_for(self.k)
                 t0 = self.clock.now()
                 ids = [r.req_id for r in self.running]
                 # decode phases of <= max_batch requests (the instance's batch limit)
@@ -314,6 +351,12 @@ class Worker(threading.Thread):
             self._finish(fin)
             self.push_status(fin)
 
+    @staticmethod
+    def _prefill_ids(r: LiveReq) -> np.ndarray:
+        if r.n_gen == 0:
+            return r.prompt
+        return np.concatenate([r.prompt, np.asarray(r.tokens, dtype=np.int32)])
+
     def _finish(self, fin):
         if fin:
             self.inst.release([r.req_id for r in fin])
@@ -348,7 +391,7 @@ class PaDGServer:
     def __init__(self, instances: Sequence, slo_ttft_ns: int, slo_tpot_ns: int, reserve_tokens: int,
                  predictor_table=None, token_budget: int = 16384, decode_steps_per_poll: int = 1,
                  probe_printed: bool = False, policy: str = "padg", chunk_budget: int = 1024,
-                 fudg_prefill: int = 0):
+                 fudg_prefill: int = 0, admission: str = "reserve"):
         if policy not in ("padg", "nodg", "sarathi", "fudg"):
             raise ValueError(f"unknown policy {policy!r}")
         self.policy = policy
@@ -374,8 +417,10 @@ class PaDGServer:
                 self._rr_dec += 1
             return w
 
+        if admission == "preempt" and policy not in ("padg", "nodg"):
+            raise ValueError("preempt admission is implemented for the separate-batching loops (padg, nodg)")
         self.workers = [Worker(i, inst, self.clock, self.status_q, token_budget, decode_steps_per_poll,
-                               hybrid_budget=hb, role=roles[i], handoff=handoff)
+                               hybrid_budget=hb, role=roles[i], handoff=handoff, admission=admission)
                         for i, inst in enumerate(instances)]
         if policy == "fudg":
             def decode_full():

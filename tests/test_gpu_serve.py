@@ -73,3 +73,37 @@ def test_fudg_on_gpu_same_tokens_as_padg():
     assert got["padg"] == got["fudg"]
     for i in insts:
         i.close()
+
+
+def test_preempt_admission_on_gpu_matches_oracle():
+    """Reading A14 live on the GPU: a pool too small for the outputs (reservation R = 0),
+    so the worker preempts and re-prefills requests with prompt + generated tokens. Every
+    request finishes with G tokens equal to the oracle's greedy continuation wherever its
+    top-2 margin is decisive (a recompute runs the prefill kernels on the generated tokens,
+    so a near tie may break differently than the decode path would)."""
+    from paper_2504_18154_b200.instance import Instance, device_weights_from_host
+    from paper_2504_18154_b200.serve import PaDGServer
+    shape = get_shape("tiny-gqa")
+    w = make_weights(shape, seed=0)
+    dw = device_weights_from_host(w, "cuda:0")
+    inst = Instance(shape, dw, 14, 0, token_budget=2048, max_batch=64, max_positions=2048)
+    trace = make_trace("tiny", 10, seed=13, rate_per_s=2000.0, vocab=shape.vocab)
+    for r in trace:
+        r.output_len = 80 + (r.req_id * 29) % 60
+    srv = PaDGServer([inst], slo_ttft_ns=10 ** 11, slo_tpot_ns=10 ** 10, reserve_tokens=0, token_budget=2048,
+                     admission="preempt")
+    out = srv.run(trace, timeout_s=300)
+    assert all(r.t_done_ns >= 0 and len(r.tokens) == r.G for r in out.values())
+    assert srv.workers[0].n_preempted >= 1
+    assert not inst.status()[1], "every request released"
+    model = T.Model(shape, w.as_f64())
+    checked = 0
+    for r in out.values():
+        toks, outs = model.generate(list(r.prompt), r.G)
+        for k in range(r.G):
+            if r.tokens[k] != toks[k]:
+                assert T.top2_margin(outs[k].logits) <= 5e-2, (r.req_id, k)
+                break
+            checked += 1
+    assert checked >= 0.5 * sum(r.G for r in out.values())
+    inst.close()

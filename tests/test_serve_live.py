@@ -218,3 +218,64 @@ def test_fudg_prefill_and_decode_roles(S):
     assert sum(sum(1 for c in d.calls if c[0] == "import") for d in insts[1:]) == n_multi
     for r in out.values():
         assert r.t_first_ns <= r.t_decode_begin_ns <= r.t_done_ns
+
+
+class FakeBlockInstance(FakeInstance):
+    """+ the engine's 64-token KV block accounting: a prefill holds ceil(S/64) blocks, a
+    decode step that writes position p needs ceil((p+1)/64); exceeding the pool raises
+    like ECOSERVE_ERR_KV_EXHAUSTED. The prefill's prompt length is what the worker sends
+    (prompt + generated tokens for a recompute)."""
+
+    def __init__(self, num_blocks, **kw):
+        super().__init__(num_blocks=num_blocks, **kw)
+        self.kv = {}   # rid -> tokens with KV (prompt + fed tokens)
+        self.prefills = []
+
+    def used(self):
+        return sum((n + 63) // 64 for n in self.kv.values())
+
+    def prefill(self, reqs):
+        for rid, p, g in reqs:
+            assert g >= 1
+            self.kv[rid] = len(p)
+            self.prefills.append((rid, len(p), g))
+        assert self.used() <= self.num_blocks, "KV pool exhausted at prefill"
+        return super().prefill(reqs)
+
+    def decode(self, ids, steps):
+        toks, nf = super().decode(ids, steps)
+        for i, rid in enumerate(ids):
+            self.kv[rid] += int((toks[i] >= 0).sum())
+        assert self.used() <= self.num_blocks, "KV pool exhausted at decode"
+        return toks, nf
+
+    def release(self, ids):
+        super().release(ids)
+        for rid in ids:
+            self.kv.pop(rid, None)
+
+
+def test_preempt_admission_recomputes_under_kv_pressure(S):
+    """Reading A14 in live mode: with the reservation R = 0 the macro admits more than the
+    pool holds once outputs grow; the worker preempts the latest arrivals before a decode
+    step would outgrow the pool and re-prefills them with prompt + generated tokens. Every
+    request still finishes with exactly G tokens and the pool never overflows."""
+    trace = make_trace("tiny", 12, seed=6, rate_per_s=2000.0, vocab=1000)
+    for r in trace:
+        r.output_len = 60 + (r.req_id * 37) % 90
+    inst = FakeBlockInstance(num_blocks=9, scale=1.0)
+    srv = S.PaDGServer([inst], slo_ttft_ns=100 * SEC, slo_tpot_ns=100 * SEC, reserve_tokens=0, token_budget=4096,
+                       admission="preempt")
+    out = srv.run(trace, timeout_s=60)
+    assert all(r.t_done_ns >= 0 and len(r.tokens) == r.G and r.n_gen == r.G for r in out.values())
+    w = srv.workers[0]
+    assert w.n_preempted >= 1
+    recomputes = [(rid, n, g) for rid, n, g in inst.prefills if n > out[rid].S]
+    assert len(recomputes) == w.n_preempted
+    for rid, n, g in recomputes:          # prompt + every generated token, the rest still owed
+        r = out[rid]
+        assert n - r.S + g == r.G
+    for r in out.values():
+        assert r.arrival_ns <= r.t_first_ns <= r.t_decode_begin_ns <= r.t_done_ns
+    with pytest.raises(ValueError):
+        S.PaDGServer([inst], 1, 1, 0, policy="sarathi", admission="preempt")
