@@ -85,6 +85,19 @@ ecoserve_status ecoserve_op_attention_decode(const void* q, const void* pool, in
                                              int32_t blocks_per_split, float* workspace, void* out, void* stream,
                                              int32_t use_tma);
 
+/* The persistent stream-K decode attention (head_dim 128, n_heads / n_kv <= 4; the
+ * engine uses it with ECOSERVE_ATTN_SK=1 when the work is large enough): sequences in longest-first order,
+ * their (kv head, 64-token block) units split evenly over 2 CTAs per SM, items cut
+ * between CTAs combined by their last contributor. ctx_host: host int32 [B];
+ * block_tables: device int32 [B][bt_ld] into a single-layer pool; workspace: device f32
+ * >= B * n_heads * 64 * (head_dim + 2); counters: device int32 [B * n_kv], zero (left
+ * zero); meta: device int32 scratch >= 2B + 1. Synchronous. ECOSERVE_ERR_UNSUPPORTED
+ * when the work is too small or the group too wide for this kernel. */
+ecoserve_status ecoserve_op_attention_decode_sk(const void* q, const void* pool, int32_t n_heads, int32_t n_kv,
+                                                int32_t head_dim, const int32_t* ctx_host, int32_t B,
+                                                const int32_t* block_tables, int32_t bt_ld, float* workspace,
+                                                int32_t* counters, int32_t* meta, void* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

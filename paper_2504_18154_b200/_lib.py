@@ -166,6 +166,7 @@ SIGNATURES = {
     "ecoserve_op_attention_prefill": (C.c_int, [P, P, I64, I32, I32, I32, PI32, I32, P, I32, P, P, PI32]),
     "ecoserve_op_attention_prefill_tc": (C.c_int, [P, P, I64, I32, I32, PI32, I32, P, I32, P, P, PI32]),
     "ecoserve_op_attention_decode": (C.c_int, [P, P, I32, I32, I32, P, I32, P, I32, I32, I32, P, P, P, I32]),
+    "ecoserve_op_attention_decode_sk": (C.c_int, [P, P, I32, I32, I32, PI32, I32, P, I32, P, P, P, P, P]),
 }
 
 _lib = None

@@ -517,6 +517,306 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a, cons
   }
 }
 
+// ------------------------------------------------------------------ decode, stream-K
+// Persistent variant of the TMA decode kernel (head_dim 128, G <= 4 q heads per kv head).
+// tools/attn_decode_probe.py: at B = 128 the per-item kernel pays ~37 us per launch on
+// top of streaming (ctx 1300: 129.5 us; ctx 2600: 222.3 us, i.e. 7.4 TB/s marginal) --
+// each CTA's start-up round trips and the last partial wave (1024 CTAs = 3.46 waves of
+// 296). Here sk_grid CTAs (2 per SM) stream equal shares of the (rank, kv head, block)
+// units in LPT order, one start-up each; the K / V ring runs across item boundaries.
+// An item cut between CTAs leaves each part's (m, l, o) in the workspace; its last
+// contributor (per-item counter) combines the parts in order and writes the output.
+constexpr int SK_MAXPARTS = 32;  // parts (items) per CTA
+constexpr int SK_UNITS = 256;    // units per CTA (pool row table in smem)
+
+template <int DEC_STAGES>
+__global__ void __launch_bounds__(128) attn_decode_sk_kernel(DecodeAttnArgs a, const __grid_constant__ CUtensorMap kvmap) {
+  constexpr int D = 128, NK = D / 16, ND = D / 8, GMAX = 4, RS = D + 2;
+  extern __shared__ __align__(128) uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  bf16* sK = reinterpret_cast<bf16*>(sm);                      // [STAGES][64][D]
+  bf16* sV = sK + DEC_STAGES * 64 * D;
+  bf16* sQ = sV + DEC_STAGES * 64 * D;                         // [16][D]
+  float* red = reinterpret_cast<float*>(sQ + 16 * D);          // [4 warps][GMAX rows][D + 2]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + 4 * GMAX * RS);
+  uint64_t* empty = full + DEC_STAGES;
+  int* s_row = reinterpret_cast<int*>(empty + DEC_STAGES);     // [SK_UNITS] K pool row of each unit
+  int* s_part = s_row + SK_UNITS;                              // [SK_MAXPARTS][8] part descriptors
+  int* s_np = s_part + SK_MAXPARTS * 8;                        // [0] parts, [1] last-arriver flag
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int G = a.n_heads / a.n_kv;
+  if (tid == 0) {
+    for (int s = 0; s < DEC_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
+    fence_barrier_init();
+    tma_prefetch(&kvmap);
+  }
+  pdl_trigger();
+  pdl_wait();
+  const int NR = a.B;                 // LPT ranks
+  const int Ctot = gridDim.x, c = blockIdx.x;
+  const int U = a.sk_prefix[NR] * a.n_kv;
+  const int u0 = (int)((long long)c * U / Ctot), u1 = (int)((long long)(c + 1) * U / Ctot);
+  // ---- this CTA's parts: descriptor = {rank, kvh, blk0, blk1, nb, seq, ctx, first unit}
+  if (tid == 0) {
+    int lo = 0, hi = NR;  // the rank r with prefix[r] * n_kv <= u0 < prefix[r + 1] * n_kv
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) / 2;
+      if (a.sk_prefix[mid] * a.n_kv <= u0) lo = mid;
+      else hi = mid;
+    }
+    int np = 0, u = u0, r = lo;
+    while (u < u1 && np < SK_MAXPARTS) {
+      const int p0 = a.sk_prefix[r], nb = a.sk_prefix[r + 1] - p0;
+      if (nb == 0 || u >= (p0 + nb) * a.n_kv) {
+        ++r;
+        continue;
+      }
+      const int off = u - p0 * a.n_kv, kvh = off / nb, blk0 = off % nb;
+      const int blk1 = min(nb, blk0 + (u1 - u));
+      const int seq = a.order ? a.order[r] : r;
+      int* d = s_part + np * 8;
+      d[0] = r; d[1] = kvh; d[2] = blk0; d[3] = blk1; d[4] = nb; d[5] = seq; d[6] = a.ctx_lens[seq]; d[7] = u - u0;
+      ++np;
+      u += blk1 - blk0;
+    }
+    s_np[0] = (u < u1) ? -1 : np;  // -1: more parts than SK_MAXPARTS (the host sizes the grid so this never happens)
+  }
+  __syncthreads();
+  const int np = s_np[0];
+  const int n_units = min(u1 - u0, SK_UNITS);
+  if (np < 0 || u1 - u0 > SK_UNITS) {  // (cannot happen for grids from attn_decode_sk_grid)
+    if (tid == 0) __trap();
+    return;
+  }
+  // ---- K pool row of every unit (one round trip for all, before the stream starts)
+  for (int j = tid; j < n_units; j += 128) {
+    int k = 0;
+    while (k + 1 < np && s_part[(k + 1) * 8 + 7] <= j) ++k;
+    const int* d = s_part + k * 8;
+    const int blk = d[2] + (j - d[7]);
+    const int64_t base = ((int64_t)a.block_tables[(int64_t)d[5] * a.bt_ld + blk] * a.n_layers + a.layer) * 2;
+    s_row[j] = (int)((base * a.n_kv + d[1]) * 64);
+  }
+  __syncthreads();
+  auto issue = [&](int j) {  // unit j into stage j % S (tid 0)
+    const int st = j % DEC_STAGES;
+    const int krow = s_row[j], vrow = krow + a.n_kv * 64;
+    mbar_arrive_expect_tx(&full[st], 2 * 64 * D * 2);
+    for (int pn = 0; pn < 2; ++pn) {
+      tma_load_2d(reinterpret_cast<uint8_t*>(sK + st * 64 * D) + pn * 8192, &kvmap, &full[st], pn * 64, krow);
+      tma_load_2d(reinterpret_cast<uint8_t*>(sV + st * 64 * D) + pn * 8192, &kvmap, &full[st], pn * 64, vrow);
+    }
+  };
+  if (tid == 0)
+    for (int j = 0; j < DEC_STAGES - 1 && j < n_units; ++j) issue(j);
+
+  const float* part_o = a.part_o;   // [item][maxp][G][D]
+  float* part_w = a.part_o;
+  float* part_ml = a.part_o + (int64_t)NR * a.n_kv * a.sk_maxp * G * D;  // [item][maxp][G][2]
+  // q rows of part k (head kvh * G + row; rows >= G zero): each thread's 2 x 16 B of the
+  // [16][D] tile, loaded into registers one part ahead (the loads of part k + 1 fly while
+  // part k streams) and stored to sQ at the part boundary
+  static_assert(16 * (D / 8) == 2 * 128, "two 16-byte q chunks per thread");
+  auto fetch_q = [&](int k, uint4 (&qv)[2]) {
+    const int* d = s_part + k * 8;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = tid + h * 128, row = i / (D / 8), cc = i % (D / 8);
+      qv[h] = row < G ? *reinterpret_cast<const uint4*>(a.q + ((int64_t)d[5] * a.n_heads + d[1] * G + row) * D + cc * 8)
+                      : make_uint4(0, 0, 0, 0);
+    }
+  };
+  uint4 qnext[2];
+  if (np > 0) fetch_q(0, qnext);
+  for (int k = 0; k < np; ++k) {
+    const int* d = s_part + k * 8;
+    const int r = d[0], kvh = d[1], blk0 = d[2], blk1 = d[3], nb = d[4], seq = d[5], ctx = d[6], j0 = d[7];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = tid + h * 128, row = i / (D / 8), cc = i % (D / 8);
+      *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sQ) + swz<D>(row, cc) * 16) = qnext[h];
+    }
+    __syncthreads();
+    if (k + 1 < np) fetch_q(k + 1, qnext);
+    uint32_t qf[NK][4];
+    {
+      const uint32_t qb = smem_u32(sQ);
+#pragma unroll
+      for (int kk = 0; kk < NK; ++kk)
+        ldmatrix_x4(qb + swz<D>(lane & 15, kk * 2 + (lane >> 4)) * 16, qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3]);
+    }
+    float o[ND][4];
+#pragma unroll
+    for (int i = 0; i < ND; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float mrow = -INFINITY, lrow = 0.f;  // row g (rows g + 8 are padding: G <= 4)
+    for (int blk = blk0; blk < blk1; ++blk) {
+      const int j = j0 + (blk - blk0);
+      if (tid == 0 && j + DEC_STAGES - 1 < n_units) {
+        if (j >= 1) mbar_wait(&empty[(j - 1) % DEC_STAGES], ((j - 1) / DEC_STAGES) & 1);
+        issue(j + DEC_STAGES - 1);
+      }
+      const int st = j % DEC_STAGES;
+      mbar_wait(&full[st], (j / DEC_STAGES) & 1);
+      const uint32_t kb = smem_u32(sK + st * 64 * D), vb = smem_u32(sV + st * 64 * D);
+      float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+      for (int kk = 0; kk < NK; ++kk) {
+        uint32_t b0, b1, b2, b3;
+        const int rr = warp * 16 + (lane & 7) + ((lane >> 4) << 3);
+        ldmatrix_x4(kb + tma_swz(rr, kk * 2 + ((lane >> 3) & 1)), b0, b1, b2, b3);
+        mma_bf16_16816(s[0], qf[kk], b0, b1);
+        mma_bf16_16816(s[1], qf[kk], b2, b3);
+      }
+      float mnew = mrow;
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int kpos = blk * 64 + warp * 16 + n * 8 + 2 * t4 + e;
+          const float v = (kpos < ctx) ? s[n][e] * a.scale_log2 : -INFINITY;
+          s[n][e] = v;
+          mnew = fmaxf(mnew, v);
+        }
+      mnew = fmaxf(mnew, __shfl_xor_sync(0xffffffffu, mnew, 1));
+      mnew = fmaxf(mnew, __shfl_xor_sync(0xffffffffu, mnew, 2));
+      const float corr = (mrow == -INFINITY) ? 0.f : exp2f(mrow - mnew);
+      float rs = 0.f;
+      uint32_t af[4];
+#pragma unroll
+      for (int n = 0; n < 2; ++n) {
+        const float p0 = (mnew == -INFINITY) ? 0.f : exp2f(s[n][0] - mnew);
+        const float p1 = (mnew == -INFINITY) ? 0.f : exp2f(s[n][1] - mnew);
+        rs += p0 + p1;
+        af[n * 2 + 0] = pack_bf16x2(p0, p1);
+        af[n * 2 + 1] = 0u;  // rows 8..15: padding
+      }
+      lrow = lrow * corr + rs;
+      mrow = mnew;
+      if (__any_sync(0xffffffffu, corr != 1.f)) {
+#pragma unroll
+        for (int i = 0; i < ND; ++i) {
+          o[i][0] *= corr;
+          o[i][1] *= corr;
+        }
+      }
+#pragma unroll
+      for (int dn = 0; dn < ND; dn += 2) {
+        uint32_t b0, b1, b2, b3;
+        const int rr = warp * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+        ldmatrix_x4_trans(vb + tma_swz(rr, dn + (lane >> 4)), b0, b1, b2, b3);
+        mma_bf16_16816(o[dn], af, b0, b1);
+        mma_bf16_16816(o[dn + 1], af, b2, b3);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    // ---- the part's (m, l, o) over its blocks: warps combined in fixed order
+    lrow += __shfl_xor_sync(0xffffffffu, lrow, 1);
+    lrow += __shfl_xor_sync(0xffffffffu, lrow, 2);
+    float* myred = red + warp * GMAX * RS;
+    if (g < G) {
+#pragma unroll
+      for (int i = 0; i < ND; ++i) {
+        myred[g * RS + i * 8 + 2 * t4] = o[i][0];
+        myred[g * RS + i * 8 + 2 * t4 + 1] = o[i][1];
+      }
+      if (t4 == 0) {
+        myred[g * RS + D] = mrow;
+        myred[g * RS + D + 1] = lrow;
+      }
+    }
+    __syncthreads();
+    const bool whole = blk0 == 0 && blk1 == nb;
+    const int item = r * a.n_kv + kvh;
+    // part index within the item: CTAs from the owner of the item's first unit
+    const int iu0 = (a.sk_prefix[r] * a.n_kv) + kvh * nb;
+    const int c_lo = (int)(((long long)(iu0 + 1) * Ctot - 1) / U);
+    const int c_hi = (int)(((long long)(iu0 + nb) * Ctot - 1) / U);
+    const int pidx = c - c_lo, nparts = c_hi - c_lo + 1;
+    for (int i = tid; i < G * D; i += 128) {
+      const int row = i / D, dd = i % D;
+      float M = -INFINITY;
+      for (int w = 0; w < 4; ++w) M = fmaxf(M, red[(w * GMAX + row) * RS + D]);
+      float acc = 0.f, l = 0.f;
+      for (int w = 0; w < 4; ++w) {
+        const float mw = red[(w * GMAX + row) * RS + D];
+        const float f = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
+        acc += f * red[(w * GMAX + row) * RS + dd];
+        l += f * red[(w * GMAX + row) * RS + D + 1];
+      }
+      if (whole) {
+        a.out[(int64_t)seq * a.n_heads * D + (kvh * G + row) * D + dd] = __float2bfloat16_rn(acc / l);
+      } else {
+        const int64_t pi = (int64_t)item * a.sk_maxp + pidx;
+        part_w[(pi * G + row) * D + dd] = acc;
+        if (dd == 0) {
+          part_ml[(pi * G + row) * 2] = M;
+          part_ml[(pi * G + row) * 2 + 1] = l;
+        }
+      }
+    }
+    if (!whole) {
+      // the last of the item's parts to finish combines them all in part order
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        const int old = atomicAdd(&a.sk_cnt[item], 1);
+        s_np[1] = old == nparts - 1;
+        if (old == nparts - 1) a.sk_cnt[item] = 0;
+      }
+      __syncthreads();
+      if (s_np[1]) {
+        __threadfence();
+        for (int i = tid; i < G * D; i += 128) {
+          const int row = i / D, dd = i % D;
+          const int64_t pb = (int64_t)item * a.sk_maxp;
+          float M = -INFINITY;
+          for (int pp = 0; pp < nparts; ++pp) M = fmaxf(M, __ldcg(part_ml + ((pb + pp) * G + row) * 2));
+          float acc = 0.f, l = 0.f;
+          for (int pp = 0; pp < nparts; ++pp) {
+            const float mp = __ldcg(part_ml + ((pb + pp) * G + row) * 2);
+            const float f = (mp == -INFINITY) ? 0.f : exp2f(mp - M);
+            acc += f * __ldcg(part_o + ((pb + pp) * G + row) * D + dd);
+            l += f * __ldcg(part_ml + ((pb + pp) * G + row) * 2 + 1);
+          }
+          a.out[(int64_t)seq * a.n_heads * D + (kvh * G + row) * D + dd] = __float2bfloat16_rn(acc / l);
+        }
+      }
+    }
+    __syncthreads();  // red / sQ free for the next part
+  }
+}
+
+int attn_decode_sk_grid(int total_units, int max_item_blocks, int min_item_blocks, int n_heads, int n_kv,
+                        int head_dim, int num_sms, int* maxp, bool force) {
+  // ECOSERVE_ATTN_SK=1 enables the stream-K kernel. Off by default: standalone it removes the
+  // per-item kernel's start-up / last-wave cost, but inside the decode step it measured
+  // slower (8B B = 128: 8.08-8.16 vs 7.79-7.83 ms per step): every CTA ends together, while
+  // the per-item kernel's LPT tail lets the O projection's CTAs start and prefetch weights
+  // under PDL on the SMs it frees.
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("ECOSERVE_ATTN_SK");
+    mode = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (!(mode || force) || head_dim != 128 || n_heads / n_kv > 4) return 0;
+  const int grid = 2 * num_sms;
+  if (total_units < 4 * grid) return 0;  // (short work: the per-item kernel)
+  const int per = total_units / grid;    // units per CTA (floor)
+  if (per + 1 > SK_UNITS) return 0;
+  // parts per item: ceil(len / per) + 1; parts per CTA: <= units per CTA (every part >= 1 unit)
+  const int mp = (max_item_blocks + per - 1) / per + 1;
+  if (mp > 64) return 0;
+  *maxp = mp;
+  // parts per CTA: a range of <= per + 1 units over items of >= min_item_blocks each
+  if ((per + 1 + min_item_blocks - 1) / max(1, min_item_blocks) + 1 > SK_MAXPARTS) return 0;
+  return grid;
+}
+
 template <int D>
 __global__ void attn_combine_kernel(DecodeAttnArgs a) {
   pdl_trigger();
@@ -556,8 +856,21 @@ cudaError_t attn_prefill_launch(const PrefillAttnArgs& a, int head_dim, cudaStre
   }
 }
 
+static size_t sk_smem(int stages) {
+  return (size_t)stages * 2 * 64 * 128 * 2 + 16 * 128 * 2 + 4 * 4 * (128 + 2) * 4 + 2 * stages * 8 + SK_UNITS * 4 +
+         SK_MAXPARTS * 8 * 4 + 16 + 1024;
+}
+
 template <int D, int ST>
 static cudaError_t decode_st(const DecodeAttnArgs& a, cudaStream_t s) {
+  if constexpr (D == 128) {
+    if (a.sk_grid > 0 && a.kvmap) {
+      const int smem = (int)sk_smem(ST);
+      cudaError_t e = ensure_smem(attn_decode_sk_kernel<ST>, smem);
+      if (e != cudaSuccess) return e;
+      return launch_k(attn_decode_sk_kernel<ST>, dim3(a.sk_grid), dim3(128), smem, s, a, *a.kvmap);
+    }
+  }
   const bool tma = D == 128 && a.kvmap != nullptr;
   int smem = (2 * ST * 64 * D + 16 * D) * 2;
   const int red_bytes = 4 * 16 * (D + 2) * 4;

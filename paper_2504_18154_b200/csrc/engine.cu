@@ -179,6 +179,7 @@ struct ecoserve_instance {
   int* am_idx = nullptr;
   int am_ld = 0;
   int* d_tokens = nullptr;
+  int* sk_cnt = nullptr;         // [B_max * Mkv] stream-K decode attention item counters (zero at rest)
   float *rope_cos = nullptr, *rope_sin = nullptr;
   int* d_meta = nullptr;
   int* h_meta = nullptr;         // pinned
@@ -473,7 +474,7 @@ void ecoserve_instance_destroy(ecoserve_instance* inst) {
   if (inst->stream) cudaStreamSynchronize(inst->stream);
   void* dev[] = {inst->x, inst->h, inst->q, inst->ao, inst->act, inst->hl, inst->part, inst->counters, inst->attn_ws,
                  inst->am_val,
-                 inst->am_idx, inst->d_tokens, inst->rope_cos, inst->rope_sin, inst->d_meta, inst->dbg};
+                 inst->am_idx, inst->d_tokens, inst->sk_cnt, inst->rope_cos, inst->rope_sin, inst->d_meta, inst->dbg};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (inst->h_meta) cudaFreeHost(inst->h_meta);
@@ -662,6 +663,8 @@ ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, cons
   const int max_blocks_seq = (inst->P_max + BLOCK - 1) / BLOCK;
   inst->attn_ws_elems = (int64_t)inst->B_max * M * 64 * (D + 2);
   CK(cudaMalloc(&inst->attn_ws, sizeof(float) * inst->attn_ws_elems));
+  CK(cudaMalloc(&inst->sk_cnt, sizeof(int) * (int64_t)inst->B_max * Mkv));
+  CK(cudaMemset(inst->sk_cnt, 0, sizeof(int) * (int64_t)inst->B_max * Mkv));
   inst->am_ld = (V + 127) / 128;
   CK(cudaMalloc(&inst->am_val, sizeof(float) * (int64_t)inst->B_max * inst->am_ld));
   CK(cudaMalloc(&inst->am_idx, sizeof(int) * (int64_t)inst->B_max * inst->am_ld));
@@ -1395,10 +1398,25 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
   return ECOSERVE_OK;
 }
 
+// d_skp / sk_grid / sk_maxp: the stream-K decode attention (attention.cu) when sk_grid > 0
+struct SkAttn {
+  const int* d_skp = nullptr;  // [B + 1] block prefix over the LPT ranks
+  int grid = 0, maxp = 0;
+};
+
+static void set_sk(ecoserve_instance* inst, DecodeAttnArgs& a, const SkAttn& sk) {
+  if (sk.grid <= 0) return;
+  a.sk_prefix = sk.d_skp;
+  a.sk_cnt = inst->sk_cnt;
+  a.sk_grid = sk.grid;
+  a.sk_maxp = sk.maxp;
+  a.n_splits = 1;
+}
+
 static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const int* d_ids, const int* d_pos,
                                          const int* d_slot, const int* d_ctx, const int* d_bt, int bt_ld,
                                          int max_blocks, double kv_bytes, bool* final_normed,
-                                         const int* d_order = nullptr) {
+                                         const int* d_order = nullptr, SkAttn sk = SkAttn()) {
   cudaStream_t st = inst->stream;
   const int L = inst->L, H = inst->H, M = inst->M, D = inst->D, F = inst->F;
   const float eps = inst->shape.rms_eps;
@@ -1458,7 +1476,8 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
       a.kvmap = inst->attn_tc ? &inst->attn_kvmap : nullptr;
       a.layer = l;
       a.n_layers = L;
-      LAUNCH(P_ATTN_DECODE, kv_bytes, n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
+      set_sk(inst, a, sk);
+      LAUNCH(P_ATTN_DECODE, kv_bytes, a.n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
       cc.bar_base = inst->chain_base;
       cc.trace = (trace_path && l == std::min(1, L - 1)) ? inst->chain_trace : nullptr;
       const int n = inst->chain_n[l];
@@ -1534,7 +1553,8 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
       a.kvmap = inst->attn_tc ? &inst->attn_kvmap : nullptr;
       a.layer = l;
       a.n_layers = L;
-      LAUNCH(P_ATTN_DECODE, kv_bytes, n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
+      set_sk(inst, a, sk);
+      LAUNCH(P_ATTN_DECODE, kv_bytes, a.n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
       const bool last = l + 1 == L;
       FlowArgs fa;
       fa.B = B;
@@ -1642,7 +1662,8 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     a.kvmap = inst->attn_tc ? &inst->attn_kvmap : nullptr;  // TMA staging of K / V (head_dim 128)
     a.layer = l;
     a.n_layers = L;
-    if (!(abl & 1)) LAUNCH(P_ATTN_DECODE, kv_bytes, n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
+    set_sk(inst, a, sk);
+    if (!(abl & 1)) LAUNCH(P_ATTN_DECODE, kv_bytes, a.n_splits > 1 ? 2 : 1, attn_decode_launch(a, D, st));
     if (abl & 2) {
       h_ready = true;
       continue;
@@ -2170,7 +2191,8 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
     int* rows = ctx + B;
     int* bt = rows + B;
     int* ord = bt + (int64_t)B * bt_ld;  // decode attention: longest context first
-    const int64_t used = (ord - hm) + B;
+    int* skp = ord + B;                  // [B + 1] stream-K attention: block prefix over LPT ranks
+    const int64_t used = (skp - hm) + B + 1;
     if (used > inst->meta_cap) return ECOSERVE_ERR_INVALID_ARG;
     if (inst->debug) inst->dbg_rows.clear();
     for (int k = 0; k < B; ++k) {
@@ -2186,9 +2208,24 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
     }
     for (int k = 0; k < B; ++k) ord[k] = k;
     std::stable_sort(ord, ord + B, [ctx](int x, int y) { return ctx[x] > ctx[y]; });
+    SkAttn sk;
+    {
+      int max_nb = 0, min_nb = 1 << 30;
+      skp[0] = 0;
+      for (int r = 0; r < B; ++r) {
+        const int nb = (ctx[ord[r]] + 63) / 64;
+        skp[r + 1] = skp[r] + nb;
+        max_nb = std::max(max_nb, nb);
+        min_nb = std::min(min_nb, nb);
+      }
+      if (inst->attn_tc && inst->tp == 1)
+        sk.grid = attn_decode_sk_grid(skp[B] * inst->Mkv, max_nb, min_nb, inst->M, inst->Mkv, inst->D, inst->num_sms,
+                                      &sk.maxp);
+    }
     cudaStream_t st = inst->stream;
     CK(cudaMemcpyAsync(inst->d_meta, hm, sizeof(int) * used, cudaMemcpyHostToDevice, st));
     int* d = inst->d_meta;
+    sk.d_skp = d + (skp - hm);
     double kv_tokens = 0;
     for (int k = 0; k < B; ++k) kv_tokens += ctx[k];
     const double kv_bytes = kv_tokens * 2.0 * inst->Mkv * inst->D * 2.0;  // K and V, one layer
@@ -2196,7 +2233,7 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
     const auto t_enq0 = std::chrono::steady_clock::now();
     bool final_normed = false;
     ecoserve_status es = run_layers_decode(inst, B, d, d + (pos - hm), d + (slot - hm), d + (ctx - hm), d + (bt - hm),
-                                           bt_ld, max_blocks, kv_bytes, &final_normed, d + (ord - hm));
+                                           bt_ld, max_blocks, kv_bytes, &final_normed, d + (ord - hm), sk);
     if (es != ECOSERVE_OK) return es;
     es = lm_head_argmax(inst, d + (rows - hm), B, P_GEMM_DECODE, final_normed);
     if (es != ECOSERVE_OK) return es;

@@ -226,8 +226,18 @@ struct DecodeAttnArgs {
   const int* slot = nullptr;
   const float* rope_cos = nullptr;
   const float* rope_sin = nullptr;
+  // optional (TMA path, head_dim 128, G <= 4): persistent stream-K decode attention. The
+  // (rank, kv head, 64-token block) units in LPT rank order are split evenly over
+  // sk_grid CTAs; items cut between CTAs are combined by their last contributor.
+  const int* sk_prefix = nullptr;  // [B + 1] blocks before each LPT rank (rank r = sequence order[r])
+  int* sk_cnt = nullptr;           // [B * n_kv] arrival counters, zero at rest
+  int sk_grid = 0, sk_maxp = 0;    // CTAs; parts per item bound (workspace stride)
 };
 cudaError_t attn_decode_launch(const DecodeAttnArgs& a, int head_dim, cudaStream_t s);
+// the stream-K kernel applies (and is enabled: ECOSERVE_ATTN_SK=1, or force for the op-level
+// entry point): returns its grid (0 = use the per-item kernel)
+int attn_decode_sk_grid(int total_units, int max_item_blocks, int min_item_blocks, int n_heads, int n_kv,
+                        int head_dim, int num_sms, int* maxp, bool force = false);
 
 // ------------------------------------------------------------------ TP=2 fused all-reduce (N2)
 struct TpAllreduceArgs {

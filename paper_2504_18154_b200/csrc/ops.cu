@@ -7,6 +7,9 @@
 #include "../../include/ecoserve_ops.h"
 #include "kernels.h"
 
+#include <algorithm>
+#include <vector>
+
 using namespace eco;
 
 static int g_num_sms = 0;
@@ -278,6 +281,78 @@ ecoserve_status ecoserve_op_attention_decode(const void* q, const void* pool, in
     a.kvmap = &kvm;
   }
   OPCK(attn_decode_launch(a, head_dim, (cudaStream_t)stream));
+  return ECOSERVE_OK;
+}
+
+ecoserve_status ecoserve_op_attention_decode_sk(const void* q, const void* pool, int32_t n_heads, int32_t n_kv,
+                                                int32_t head_dim, const int32_t* ctx_host, int32_t B,
+                                                const int32_t* block_tables, int32_t bt_ld, float* workspace,
+                                                int32_t* counters, int32_t* meta, void* out, void* stream) {
+  if (!q || !pool || !ctx_host || !block_tables || !out || !workspace || !counters || !meta || B < 1 ||
+      n_heads % n_kv || head_dim != 128)
+    return ECOSERVE_ERR_INVALID_ARG;
+  // LPT order and the block prefix over it, as the engine builds them
+  std::vector<int32_t> h((size_t)2 * B + 1);
+  int32_t* ord = h.data();
+  int32_t* skp = ord + B;
+  for (int k = 0; k < B; ++k) ord[k] = k;
+  std::stable_sort(ord, ord + B, [ctx_host](int x, int y) { return ctx_host[x] > ctx_host[y]; });
+  int max_nb = 0, min_nb = 1 << 30;
+  skp[0] = 0;
+  for (int r = 0; r < B; ++r) {
+    const int nb = (ctx_host[ord[r]] + 63) / 64;
+    skp[r + 1] = skp[r] + nb;
+    max_nb = std::max(max_nb, nb);
+    min_nb = std::min(min_nb, nb);
+  }
+  int dev = 0, sms = 148, maxp = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = attn_decode_sk_grid(skp[B] * n_kv, max_nb, min_nb, n_heads, n_kv, head_dim, sms, &maxp, true);
+  if (grid <= 0) return ECOSERVE_ERR_UNSUPPORTED;
+  OPCK(cudaMemcpyAsync(meta, h.data(), sizeof(int32_t) * h.size(), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  OPCK(cudaStreamSynchronize((cudaStream_t)stream));  // (h is a local)
+  // ctx_lens on the device: the caller's block tables are, the lengths are only on the host
+  int32_t* d_ctx = nullptr;
+  OPCK(cudaMalloc(&d_ctx, sizeof(int32_t) * B));
+  OPCK(cudaMemcpy(d_ctx, ctx_host, sizeof(int32_t) * B, cudaMemcpyHostToDevice));
+  DecodeAttnArgs a;
+  a.q = (const bf16*)q;
+  a.k_cache = (const bf16*)pool;
+  a.v_cache = (const bf16*)pool + (int64_t)n_kv * 64 * head_dim;
+  a.blk_stride = 2LL * n_kv * 64 * head_dim;
+  a.ctx_lens = d_ctx;
+  a.block_tables = block_tables;
+  a.bt_ld = bt_ld;
+  a.B = B;
+  a.n_heads = n_heads;
+  a.n_kv = n_kv;
+  a.n_splits = 1;
+  a.blocks_per_split = max_nb;
+  a.part_o = workspace;
+  a.part_ml = nullptr;
+  a.out = (bf16*)out;
+  a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)head_dim));
+  a.order = meta;
+  a.layer = 0;
+  a.n_layers = 1;
+  a.sk_prefix = meta + B;
+  a.sk_cnt = counters;
+  a.sk_grid = grid;
+  a.sk_maxp = maxp;
+  CUtensorMap kvm;
+  const int64_t dims[2] = {128, (int64_t)1 << 30};
+  const int64_t strides[1] = {256};
+  const int box[2] = {64, 64};
+  if (make_tmap_bf16_nd(&kvm, pool, 2, dims, strides, box)) {
+    cudaFree(d_ctx);
+    return ECOSERVE_ERR_CUDA;
+  }
+  a.kvmap = &kvm;
+  const cudaError_t e = attn_decode_launch(a, head_dim, (cudaStream_t)stream);
+  cudaStreamSynchronize((cudaStream_t)stream);
+  cudaFree(d_ctx);
+  OPCK(e);
   return ECOSERVE_OK;
 }
 

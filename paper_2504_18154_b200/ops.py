@@ -130,3 +130,20 @@ def attention_decode(q, pool, n_heads, n_kv, head_dim, ctx_lens, block_tables, n
                                                   block_tables.shape[1], n_splits, blocks_per_split, ws.data_ptr(),
                                                   out.data_ptr(), _s(), 1 if use_tma else 0))
     return out
+
+
+def attention_decode_sk(q, pool, n_heads, n_kv, head_dim, ctx_lens, block_tables):
+    """Persistent stream-K decode attention (head_dim 128); ctx_lens: host int sequence."""
+    import numpy as np
+    B = q.shape[0]
+    out = torch.empty(B, n_heads * head_dim, dtype=torch.bfloat16, device=q.device)
+    ws = torch.empty(B * n_heads * 64 * (head_dim + 2), dtype=torch.float32, device=q.device)
+    cnt = torch.zeros(B * n_kv, dtype=torch.int32, device=q.device)
+    meta = torch.empty(2 * B + 1, dtype=torch.int32, device=q.device)
+    ctx = np.ascontiguousarray(ctx_lens, dtype=np.int32)
+    L.check(L.load().ecoserve_op_attention_decode_sk(q.data_ptr(), pool.data_ptr(), n_heads, n_kv, head_dim,
+                                                     ctx.ctypes.data_as(L.PI32), B, block_tables.data_ptr(),
+                                                     block_tables.shape[1], ws.data_ptr(), cnt.data_ptr(),
+                                                     meta.data_ptr(), out.data_ptr(), _s()))
+    assert int(cnt.abs().sum()) == 0, "item counters must be left at zero"
+    return out

@@ -265,3 +265,36 @@ def test_attention_decode(ops, D, M, Mkv, splits, bps, tma):
         vs = np.stack([pool_h[bt[i, t // 64], 1, :, t % 64, :] for t in range(c)])
         ref = T.attention(q_h[i:i + 1], ks, vs, np.array([c - 1]), np.arange(c)).reshape(M * D)
         assert rel_err(got[i], ref) < 1e-2, (i, c)
+
+
+@pytest.mark.parametrize("M,Mkv,ctx_kind", [(32, 8, "mixed"), (32, 8, "one_long"), (16, 8, "mixed"), (8, 8, "uniform")])
+def test_attention_decode_stream_k(ops, M, Mkv, ctx_kind):
+    """Persistent stream-K decode attention (the engine's default for large decode steps):
+    items cut between CTAs -- including one 8k-token sequence spread over several CTAs --
+    combined by their last contributor; every output row against the fp64 definition."""
+    D = 128
+    rng = np.random.default_rng(M + Mkv + len(ctx_kind))
+    if ctx_kind == "mixed":
+        ctx = [int(x) for x in rng.integers(200, 3000, 64)]
+    elif ctx_kind == "one_long":
+        ctx = [8000] + [int(x) for x in rng.integers(200, 900, 47)]
+    else:
+        ctx = [1300] * 160
+    nb = [(c + 63) // 64 for c in ctx]
+    n_blocks = sum(nb) + 2
+    pool_h, pool_d = make_pool(rng, n_blocks, Mkv, D)
+    perm = rng.permutation(n_blocks)
+    bt = np.zeros((len(ctx), max(nb)), dtype=np.int32)
+    k = 0
+    for i, b in enumerate(nb):
+        bt[i, :b] = perm[k:k + b]
+        k += b
+    q_h, q_d = bf16_rand(rng, (len(ctx), M, D))
+    got = ops.attention_decode_sk(q_d, pool_d, M, Mkv, D, ctx, torch.from_numpy(bt).cuda()).float().cpu().numpy()
+    check = range(len(ctx)) if len(ctx) <= 64 else range(0, len(ctx), 7)
+    for i in check:
+        c = ctx[i]
+        ks = np.stack([pool_h[bt[i, t // 64], 0, :, t % 64, :] for t in range(c)])
+        vs = np.stack([pool_h[bt[i, t // 64], 1, :, t % 64, :] for t in range(c)])
+        ref = T.attention(q_h[i:i + 1], ks, vs, np.array([c - 1]), np.arange(c)).reshape(M * D)
+        assert rel_err(got[i], ref) < 1e-2, (i, c)
