@@ -57,6 +57,9 @@ struct LayerW {
   const bf16 *attn_norm, *ffn_norm, *wo, *wd;
   bf16 *wqkv, *wgu;
   CUtensorMap qkv_a, qkv_b, o_a, o_b, gu_a, gu_b, d_a, d_b;  // _a: box 128 (decode A), _b: box 256 (prefill B)
+  // decode gate/up in two waves (gu2_a: the tiles past the first wave) and the down
+  // projection split at that K boundary (d1_a: K blocks [0, W1), d2_a: [W1, F/64))
+  CUtensorMap gu2_a, d1_a, d2_a;
 };
 
 int bn_index(int bn) { return bn == 64 ? 0 : bn == 128 ? 1 : 2; }
@@ -180,6 +183,12 @@ struct ecoserve_instance {
   int am_ld = 0;
   int* d_tokens = nullptr;
   int* sk_cnt = nullptr;         // [B_max * Mkv] stream-K decode attention item counters (zero at rest)
+  // decode gate/up second wave beside the down projection's first K part (gu_waves)
+  int gw_w1 = 0;                 // gate/up tiles of the first wave (= K blocks of the down's first part)
+  ActMaps act_k1, act_k2;        // act columns [0, 64 * W1) and [64 * W1, F) as B operands
+  int* gw_flag = nullptr;        // gate/up wave 1 passed its PDL wait (epoch)
+  unsigned long long* gw_trace = nullptr;  // ECOSERVE_GW_TRACE (debug)
+  int gw_epoch = 0;
   float *rope_cos = nullptr, *rope_sin = nullptr;
   int* d_meta = nullptr;
   int* h_meta = nullptr;         // pinned
@@ -289,6 +298,31 @@ static int device_instances(int device, int delta) {
   static std::map<int, int> n;
   std::lock_guard<std::mutex> lock(mu);
   return n[device] += delta;
+}
+
+// ECOSERVE_GU_WAVES=1 enables the two-wave decode gate/up with the concurrent first part of
+// the down projection (run_layers_decode). Off by default: parity-green and the concurrent
+// phase streams at 6.1 TB/s (ECOSERVE_GW_TRACE, tools/gw_trace.py), but the two extra
+// kernel boundaries (~3 us TMA ramp after each CTA start + ~3-4 us epilogue tail each) eat
+// the gain: 8B B = 128 step 7.91 vs 7.83 ms.
+static bool gu_waves_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_GU_WAVES");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// ECOSERVE_L2_OWN=n: each decode GEMM CTA prefetches up to n of its weight K blocks
+// (16 KB each) beyond its smem ring into L2 before its PDL wait (A/B measurement).
+static int l2_own_prefetch_kb() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_L2_OWN");
+    v = e ? std::max(0, atoi(e)) : 0;
+  }
+  return v;
 }
 
 // ECOSERVE_QKV_FUSE=1: the decode QKV split reduction (RoPE, K/V append) inside the
@@ -474,7 +508,7 @@ void ecoserve_instance_destroy(ecoserve_instance* inst) {
   if (inst->stream) cudaStreamSynchronize(inst->stream);
   void* dev[] = {inst->x, inst->h, inst->q, inst->ao, inst->act, inst->hl, inst->part, inst->counters, inst->attn_ws,
                  inst->am_val,
-                 inst->am_idx, inst->d_tokens, inst->sk_cnt, inst->rope_cos, inst->rope_sin, inst->d_meta, inst->dbg};
+                 inst->am_idx, inst->d_tokens, inst->sk_cnt, inst->gw_flag, inst->rope_cos, inst->rope_sin, inst->d_meta, inst->dbg};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (inst->h_meta) cudaFreeHost(inst->h_meta);
@@ -663,6 +697,37 @@ ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, cons
   const int max_blocks_seq = (inst->P_max + BLOCK - 1) / BLOCK;
   inst->attn_ws_elems = (int64_t)inst->B_max * M * 64 * (D + 2);
   CK(cudaMalloc(&inst->attn_ws, sizeof(float) * inst->attn_ws_elems));
+  if (gu_waves_enabled() && inst->tp == 1 && F % 64 == 0 && H % 128 == 0 && 2 * F / 128 > inst->num_sms &&
+      2 * F / 128 - inst->num_sms <= inst->num_sms - H / 128) {
+    // gate/up has more tiles than SMs: W1 = num_sms tiles first, the rest (W2) beside the
+    // down projection's K blocks [0, W1) -- those read only first-wave output columns
+    const int W1 = inst->num_sms;
+    inst->gw_w1 = W1;
+    bool bad = false;
+    for (int l = 0; l < L && !bad; ++l) {
+      LayerW& w = inst->lw[l];
+      const int64_t dg[2] = {H, 2LL * F - 128LL * W1}, sg[1] = {2LL * H};
+      const int64_t d1[2] = {64LL * W1, H}, d2[2] = {(int64_t)F - 64LL * W1, H}, sd[1] = {2LL * F};
+      const int box[2] = {64, 128};
+      bad = make_tmap_bf16_nd(&w.gu2_a, w.wgu + 128LL * W1 * H, 2, dg, sg, box) ||
+            make_tmap_bf16_nd(&w.d1_a, w.wd, 2, d1, sd, box) ||
+            make_tmap_bf16_nd(&w.d2_a, w.wd + 64LL * W1, 2, d2, sd, box);
+    }
+    for (int i = 0; i < 3 && !bad; ++i) {
+      const int boxes[3] = {64, 128, 256};
+      const int64_t sa[1] = {2LL * F};
+      const int64_t a1[2] = {64LL * W1, T}, a2[2] = {(int64_t)F - 64LL * W1, T};
+      const int bx[2] = {64, boxes[i]};
+      bad = make_tmap_bf16_nd(&inst->act_k1.b[i], inst->act, 2, a1, sa, bx) ||
+            make_tmap_bf16_nd(&inst->act_k2.b[i], inst->act + 64LL * W1, 2, a2, sa, bx);
+    }
+    if (bad) {
+      inst->err = "cuTensorMapEncodeTiled failed (gate/up waves)";
+      return ECOSERVE_ERR_CUDA;
+    }
+    CK(cudaMalloc(&inst->gw_flag, sizeof(int)));
+    CK(cudaMemset(inst->gw_flag, 0, sizeof(int)));
+  }
   CK(cudaMalloc(&inst->sk_cnt, sizeof(int) * (int64_t)inst->B_max * Mkv));
   CK(cudaMemset(inst->sk_cnt, 0, sizeof(int) * (int64_t)inst->B_max * Mkv));
   inst->am_ld = (V + 127) / 128;
@@ -1073,6 +1138,7 @@ cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const 
   const int var = rr;
   if (fused) *fused = false;
   e.indep = 1;  // weights (A) prefetch before the PDL wait
+  e.l2_pf_kb = l2_own_prefetch_kb();
   if (r2) e.pf_map = nullptr;  // (the L2 prefetch assumes 128-row units)
   if (splits == 1 && r2) {
     e.mode = mode;
@@ -1693,11 +1759,92 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
     eg.ldo = F;
     set_prefetch(inst, eg, 4 * l + 3, H, F, B);  // down next
     inst->gu_trace_layer = l;
-    LAUNCH(P_GEMM_DECODE, 2.0 * 2 * F * H, nk,
-           decode_gemm(inst, w.gu_a, inst->m_h, 2 * F, H, B, EPI_SWAP_SILU, eg, &nk, nullptr, nullptr, nullptr, &w.gu_b));
     // the down projection's reduction also applies the next RMSNorm: the next layer's
     // attention norm, or after the last layer the final norm (into the LM-head input)
     const bool last = l + 1 == L;
+    if (inst->gw_w1 > 0 && B <= 128 && !inst->tp_fused && inst->tp == 1 && decode_variant() == 1) {
+      // gate/up in two waves. Its 2F/128 tiles exceed the SMs: in one kernel the second
+      // wave leaves the SMs done after one tile waiting (the down GEMM behind it can only
+      // prefetch weights). Here wave 1 (W1 = num_sms tiles) runs alone; then the down
+      // projection's K blocks [0, W1) -- which read only wave-1 output -- run beside wave 2
+      // on the other SMs (wave 2 waits on a flag instead of the kernel before it, see
+      // GemmEpi::flag_wait); then the down K blocks [W1, F/64); one reduction sums all
+      // split planes in order and applies the next RMSNorm.
+      const int W1 = inst->gw_w1, W2 = 2 * F / 128 - W1, dt = H / 128;
+      const int bn = B <= 64 ? 64 : 128, bi = bn_index(bn);
+      const int s1 = gemm_effective_splits(64 * W1, std::max(1, std::min(4, (inst->num_sms - W2) / dt)));
+      const int s2 = gemm_effective_splits(F - 64 * W1, std::max(1, std::min(4, inst->num_sms / dt)));
+      const int ep = ++inst->gw_epoch;
+      static const char* gw_trace = getenv("ECOSERVE_GW_TRACE");  // debug: per-CTA marks of layer 5
+      unsigned long long* tr = nullptr;
+      if (gw_trace && l == 5) {
+        if (!inst->gw_trace) {
+          CK(cudaMalloc(&inst->gw_trace, sizeof(unsigned long long) * 4 * inst->num_sms * 16));
+        }
+        CK(cudaMemsetAsync(inst->gw_trace, 0, sizeof(unsigned long long) * 4 * inst->num_sms * 16, st));
+        tr = inst->gw_trace;
+      }
+      GemmEpi g1 = eg;
+      g1.trace = tr;
+      g1.mode = EPI_SWAP_SILU;
+      g1.indep = 1;
+      g1.pf_map = nullptr;
+      g1.flag_set = inst->gw_flag;
+      g1.flag_epoch = ep;
+      LAUNCH(P_GEMM_DECODE, 2.0 * 128 * W1 * H, 1,
+             gemm_launch_r(&w.gu_a, &inst->m_h.b[bi], 128 * W1, B, H, bn, 1, 1, g1, inst->num_sms, st));
+      GemmEpi d1 = epi_base(inst);
+      d1.mode = EPI_SWAP_F32;
+      d1.out = inst->part;
+      d1.ldo = H;
+      d1.indep = 1;
+      d1.trace = tr ? tr + 1 * inst->num_sms * 16 : nullptr;
+      LAUNCH(P_GEMM_DECODE, 2.0 * H * 64 * W1, 1,
+             gemm_launch_r(&w.d1_a, &inst->act_k1.b[bi], H, B, 64 * W1, bn, 1, s1, d1, inst->num_sms, st));
+      GemmEpi g2 = g1;
+      g2.out = inst->act + 64LL * W1;
+      g2.flag_set = nullptr;
+      g2.flag_wait = inst->gw_flag;
+      g2.trace = tr ? tr + 2 * inst->num_sms * 16 : nullptr;
+      LAUNCH(P_GEMM_DECODE, 2.0 * 128 * W2 * H, 1,
+             gemm_launch_r(&w.gu2_a, &inst->m_h.b[bi], 128 * W2, B, H, bn, 1, 1, g2, inst->num_sms, st));
+      GemmEpi d2 = d1;
+      d2.out = inst->part + (int64_t)s1 * B * H;
+      d2.trace = tr ? tr + 3 * inst->num_sms * 16 : nullptr;
+      LAUNCH(P_GEMM_DECODE, 2.0 * H * (F - 64.0 * W1), 1,
+             gemm_launch_r(&w.d2_a, &inst->act_k2.b[bi], H, B, F - 64 * W1, bn, 1, s2, d2, inst->num_sms, st));
+      LAUNCH(P_OTHER, 0, 1,
+             splitk_resid_rmsnorm_launch(inst->part, s1 + s2, B, inst->x, last ? inst->final_norm : inst->lw[l + 1].attn_norm,
+                                         last ? inst->hl : inst->h, H, eps, st));
+      if (tr) {  // append "kernel cta mark t_ns" (relative to the earliest mark)
+        std::vector<unsigned long long> t((size_t)4 * inst->num_sms * 16);
+        CK(cudaMemcpyAsync(t.data(), tr, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        unsigned long long t0 = ~0ull;
+        for (auto v : t)
+          if (v) t0 = std::min(t0, v);
+        FILE* f = fopen(gw_trace, "a");
+        if (f) {
+          fprintf(f, "#\n");
+          for (int kk = 0; kk < 4; ++kk)
+            for (int c = 0; c < inst->num_sms; ++c)
+              for (int m = 0; m < 8; ++m) {
+                const unsigned long long v = t[((size_t)kk * inst->num_sms + c) * 16 + m];
+                if (v) fprintf(f, "%d %d %d %llu\n", kk, c, m, v - t0);
+              }
+          fclose(f);
+        }
+      }
+      fused = true;
+      h_ready = !last;
+      if (last) *final_normed = true;
+      if (inst->debug)
+        CK(cudaMemcpyAsync(inst->dbg + (int64_t)(l + 1) * inst->T_max * H, inst->x, sizeof(float) * (int64_t)B * H,
+                           cudaMemcpyDeviceToDevice, st));
+      continue;
+    }
+    LAUNCH(P_GEMM_DECODE, 2.0 * 2 * F * H, nk,
+           decode_gemm(inst, w.gu_a, inst->m_h, 2 * F, H, B, EPI_SWAP_SILU, eg, &nk, nullptr, nullptr, nullptr, &w.gu_b));
     if (inst->tp_fused) {
       const int ep = ++inst->tp_epoch;
       int sp = 1;

@@ -85,6 +85,29 @@ __device__ __forceinline__ void trace_put(const GemmEpi& e, int i, long long v) 
   if (e.trace) e.trace[blockIdx.x * 16 + i] = (unsigned long long)v;
 }
 
+// The producer's wait before its first dependent load. Normally the PDL wait for the
+// previous kernel on the stream. With epi.flag_wait the GEMM instead waits until the flag
+// reaches flag_epoch -- raised by an earlier kernel once its own inputs were complete
+// (epi.flag_set) -- so it can run beside the kernel just before it (GemmEpi::flag_wait).
+// With epi.flag_set, CTA 0 raises the flag once its PDL wait returned.
+__device__ __forceinline__ void gemm_dep_wait(const GemmEpi& epi) {
+  if (epi.flag_wait) {
+    for (;;) {
+      int v;
+      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(epi.flag_wait) : "memory");
+      if (v >= epi.flag_epoch) break;
+      __nanosleep(64);
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // the TMA loads that follow
+  } else {
+    pdl_wait();
+  }
+  if (epi.flag_set && blockIdx.x == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(epi.flag_set), "r"(epi.flag_epoch) : "memory");
+  }
+}
+
 __device__ __forceinline__ float silu_f(float z) { return __fdividef(z, 1.f + __expf(-z)); }
 
 // ---------------------------------------------------------------- epilogues
@@ -375,7 +398,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_arrive_expect_tx(&full_bar[na], C::A_BYTES);
         tma_load_2d(smem + na * C::A_BYTES, &mapA, &full_bar[na], ca.kb * BK, ca.mt * BM);
       }
-      pdl_wait();
+      gemm_dep_wait(epi);
       for (; nb < C::SB && (b_more = next(cb)); ++nb) {
         mbar_arrive_expect_tx(&full_b[nb], C::B_BYTES);
         tma_load_2d(ring_b + nb * C::B_BYTES, &mapB, &full_b[nb], cb.kb * BK, cb.nt * BN);
@@ -456,8 +479,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           ++npre;
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
+        // 1b) decode: the weight K blocks beyond the smem ring into L2 (up to l2_pf_kb), so
+        //     the previous kernel's tail (attention / reduction, SMs freeing up under PDL)
+        //     also streams this GEMM's weights; the loads after the wait then hit L2
+        if (indep == 1 && epi.l2_pf_kb > 0) {
+          const int sw = w, skb = kb, skb1 = kb1, smt = mt, snt = nt;
+          for (int n = 0; n < epi.l2_pf_kb && next(); ++n)
+            asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                             reinterpret_cast<uint64_t>(&mapA)),
+                         "r"(kb * BK), "r"(mt * BM * R)
+                         : "memory");
+          w = sw; kb = skb; kb1 = skb1; mt = smt; nt = snt;  // rewind the cursor
+        }
       }
-      pdl_wait();
+      gemm_dep_wait(epi);
       // 2) their dependent operand
       for (int i = 0; i < npre; ++i) {
         uint8_t* sa = smem + i * C::STAGE_BYTES;
@@ -533,7 +568,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    pdl_wait();              // the epilogue reads/writes buffers of the previous kernels
+    if (!epi.flag_wait) pdl_wait();  // the epilogue reads/writes buffers of the previous kernels
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int ep_tid = (warp - 2) * 32 + lane;
     int acc = 0;
@@ -821,6 +856,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     __syncwarp();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
+  // a flag-gated GEMM did not wait for the kernel before it on the stream: it completes only
+  // after that kernel does, so the kernels after it still see both (see GemmEpi::flag_wait)
+  if (epi.flag_wait && threadIdx.x == 0) pdl_wait();
 }
 
 // ---------------------------------------------------------------- cluster split-K decode GEMM

@@ -72,6 +72,19 @@ struct GemmEpi {
   // output element here -- the peer GPU's receive plane over NVLink, same layout as
   // out / resid -- and the epilogue threads end with fence.sys
   float* out2;
+  // Concurrent decode GEMMs (the gate/up second wave beside the down projection's first K
+  // part): flag_set -- CTA 0 stores flag_epoch there once its PDL wait returned (its inputs,
+  // and so the inputs of later kernels that read the same buffers, are complete);
+  // flag_wait -- the GEMM does not wait for the previous kernel: its producer waits until
+  // *flag_wait >= flag_epoch instead, the epilogue writes without waiting, and thread 0
+  // of every CTA waits for the previous kernel at the very end (so kernels launched after
+  // this one still wait, through it, for the one before it).
+  int* flag_set;
+  const int* flag_wait;
+  int flag_epoch;
+  // decode (indep == 1): after the first smem stages, prefetch up to this many more of the
+  // CTA's weight K blocks into L2 before the PDL wait (0 = none)
+  int l2_pf_kb;
   // deferred RMSNorm (decode flow path): the GEMM input was bf16(x * gamma), so the QKV
   // epilogues (EPI_SWAP_QKV, RED_QKV) multiply token n's outputs by rvec[n] = 1/rms(x_n)
   const float* rvec;

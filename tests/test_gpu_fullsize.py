@@ -145,34 +145,23 @@ def test_fullwidth_70b_tp2():
     assert checked >= len(prompts) * G // 2
 
 
-def test_fullwidth_decode_gu_stream_k():
-    """The opt-in stream-K gate/up kernel (ECOSERVE_GU_SK=1: 224 / 344 tiles balanced over
-    the SMs, tiles split between two CTAs summed deterministically) at the 8B and 34B
-    widths, same oracle bars (fresh process)."""
+@pytest.mark.parametrize("env", ["ECOSERVE_GU_SK=1", "ECOSERVE_FLOW=1", "ECOSERVE_ATTN_SK=1", "ECOSERVE_GU_WAVES=1",
+                                 "ECOSERVE_QKV_FUSE=1"])
+def test_fullwidth_decode_variants(env):
+    """Every decode variant switch at full 8B / 34B widths and bench-like batches, against
+    the same oracle bars (fresh process: the switches are read once). GU_SK: stream-K
+    gate/up (224 / 344 tiles balanced, two-way tile sums); FLOW: the O -> gate/up -> down
+    dataflow kernel; ATTN_SK: persistent stream-K decode attention; GU_WAVES: gate/up
+    in two waves, the second beside the down GEMM's first K part; QKV_FUSE:
+    the QKV reduction in the attention prologue."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    if os.environ.get("ECOSERVE_GU_SK") == "1":
-        pytest.skip("already running with ECOSERVE_GU_SK=1")
+    k, v = env.split("=")
+    if os.environ.get(k) == v:
+        pytest.skip(f"already running with {env}")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.abspath(__file__), "-k",
-                        "single_gpu or sampled"], env={**os.environ, "ECOSERVE_GU_SK": "1"}, cwd=root,
-                       capture_output=True, text=True, timeout=1200)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-
-
-def test_fullwidth_decode_flow_kernel():
-    """The opt-in decode dataflow kernel (ECOSERVE_FLOW=1: O -> gate/up -> down in one
-    persistent kernel, split tiles reduce-added into x by TMA, deferred RMSNorm) at full
-    8B / 34B widths and bench-like batches, against the same oracle bars (fresh process:
-    the switch is read once)."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    if os.environ.get("ECOSERVE_FLOW") == "1":
-        pytest.skip("already running with ECOSERVE_FLOW=1")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.abspath(__file__), "-k",
-                        "single_gpu or sampled"], env={**os.environ, "ECOSERVE_FLOW": "1"}, cwd=root,
+                        "single_gpu or sampled"], env={**os.environ, k: v}, cwd=root,
                        capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

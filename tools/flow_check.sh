@@ -1,5 +1,2 @@
-timeout 600 python -m pytest -q -x tests/test_gpu_ops.py -k "stream_k" 2>&1 | tail -2
-for i in 1 2 3; do
-timeout 300 python tools/decode_ablate.py --one
-ECOSERVE_ATTN_SK=0 timeout 300 python tools/decode_ablate.py --one
-done
+ECOSERVE_GW_TRACE=gpurun_out/gw_trace.txt timeout 300 python tools/decode_ablate.py --one
+python tools/gw_trace.py gpurun_out/gw_trace.txt
