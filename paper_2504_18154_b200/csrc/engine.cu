@@ -183,6 +183,7 @@ struct ecoserve_instance {
   int am_ld = 0;
   int* d_tokens = nullptr;
   int* sk_cnt = nullptr;         // [B_max * Mkv] stream-K decode attention item counters (zero at rest)
+  float* nrm_ss = nullptr;       // [ceil(H/256)][T_max] prefill deferred RMSNorm: per-tile sums of x^2
   // decode gate/up second wave beside the down projection's first K part (gu_waves)
   int gw_w1 = 0;                 // gate/up tiles of the first wave (= K blocks of the down's first part)
   ActMaps act_k1, act_k2;        // act columns [0, 64 * W1) and [64 * W1, F) as B operands
@@ -310,6 +311,18 @@ static bool gu_waves_enabled() {
   if (v < 0) {
     const char* e = getenv("ECOSERVE_GU_WAVES");
     v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// ECOSERVE_PREFILL_DNORM=0: prefill RMSNorms as their own kernels instead of folded into
+// the O / down epilogues (h = bf16(x * gamma), per-tile sums of squares) and the QKV /
+// gate-up epilogues (x 1/rms) -- A/B measurement.
+static bool prefill_dnorm_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_PREFILL_DNORM");
+    v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
 }
@@ -508,7 +521,7 @@ void ecoserve_instance_destroy(ecoserve_instance* inst) {
   if (inst->stream) cudaStreamSynchronize(inst->stream);
   void* dev[] = {inst->x, inst->h, inst->q, inst->ao, inst->act, inst->hl, inst->part, inst->counters, inst->attn_ws,
                  inst->am_val,
-                 inst->am_idx, inst->d_tokens, inst->sk_cnt, inst->gw_flag, inst->rope_cos, inst->rope_sin, inst->d_meta, inst->dbg};
+                 inst->am_idx, inst->d_tokens, inst->sk_cnt, inst->gw_flag, inst->nrm_ss, inst->rope_cos, inst->rope_sin, inst->d_meta, inst->dbg};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (inst->h_meta) cudaFreeHost(inst->h_meta);
@@ -728,6 +741,7 @@ ecoserve_status ecoserve_instance_create(const ecoserve_model_shape* shape, cons
     CK(cudaMalloc(&inst->gw_flag, sizeof(int)));
     CK(cudaMemset(inst->gw_flag, 0, sizeof(int)));
   }
+  CK(cudaMalloc(&inst->nrm_ss, sizeof(float) * (int64_t)((H + 255) / 256) * T));
   CK(cudaMalloc(&inst->sk_cnt, sizeof(int) * (int64_t)inst->B_max * Mkv));
   CK(cudaMemset(inst->sk_cnt, 0, sizeof(int) * (int64_t)inst->B_max * Mkv));
   inst->am_ld = (V + 127) / 128;
@@ -1361,11 +1375,32 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
   LAUNCH(P_OTHER, 0, 1, embed_launch(d_ids, inst->embed, inst->x, T, H, inst->V, st));
   if (inst->debug) CK(cudaMemcpyAsync(inst->dbg, inst->x, sizeof(float) * (int64_t)T * H, cudaMemcpyDeviceToDevice, st));
   bool h_ready = false;  // the previous layer's fused TP all-reduce already wrote this layer's norm
+  // deferred RMSNorm (TP=1): the residual epilogues leave h = bf16(x * gamma) and per-tile
+  // sums of x^2, the consumer epilogues multiply by 1/rms (GemmEpi::nrm_*)
+  const bool dnorm = inst->tp == 1 && prefill_dnorm_enabled();
+  bool ss_ready = false;  // h is bf16(x * gamma) and nrm_ss holds the row sums: consumers scale
+  auto nrm_in = [&](GemmEpi& g) {
+    if (!ss_ready) return;
+    g.nrm_ss_in = inst->nrm_ss;
+    g.nrm_ss_ld = inst->T_max;
+    g.nrm_ss_n = (H + 255) / 256;
+    g.nrm_inv_h = 1.f / (float)H;
+    g.nrm_eps = eps;
+  };
+  auto nrm_out = [&](GemmEpi& g, const bf16* gamma) {
+    g.nrm_h = inst->h;
+    g.nrm_ldh = H;
+    g.nrm_gamma = gamma;
+    g.nrm_ss_out = inst->nrm_ss;
+    g.nrm_ss_ld = inst->T_max;
+  };
   for (int l = 0; l < L; ++l) {
     LayerW& w = inst->lw[l];
     if (!h_ready) LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.attn_norm, inst->h, T, H, eps, st));
     h_ready = false;
     GemmEpi e = epi_base(inst);
+    nrm_in(e);
+    ss_ready = false;
     e.mode = EPI_QKV;
     e.pos = d_pos;
     e.slot = d_slot;
@@ -1430,12 +1465,16 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
     } else {
       GemmEpi eo = resid_epi(inst);
       eo.mode = resid_mode_prefill(inst);
+      if (dnorm) nrm_out(eo, w.ffn_norm);
       LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * M * D, 1,
              prefill_gemm(inst, inst->m_ao.a, w.o_a, w.o_b, T, H, M * D, eo));
       ALLREDUCE_X(T);
-      LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, T, H, eps, st));
+      if (dnorm) ss_ready = true;
+      else LAUNCH(P_OTHER, 0, 1, rmsnorm_launch(inst->x, H, nullptr, w.ffn_norm, inst->h, T, H, eps, st));
     }
     GemmEpi eg = epi_base(inst);
+    nrm_in(eg);
+    ss_ready = false;
     eg.mode = EPI_SILU;
     eg.out = inst->act;
     eg.ldo = F;
@@ -1453,9 +1492,12 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
     } else {
       GemmEpi ed = resid_epi(inst);
       ed.mode = resid_mode_prefill(inst);
+      const bool last = l + 1 == L;  // (the LM head normalises its rows itself)
+      if (dnorm && !last) nrm_out(ed, inst->lw[l + 1].attn_norm);
       LAUNCH(P_GEMM_PREFILL, 2.0 * T * H * F, 1,
              prefill_gemm(inst, inst->m_act.a, w.d_a, w.d_b, T, H, F, ed));
       ALLREDUCE_X(T);
+      if (dnorm && !last) h_ready = ss_ready = true;
     }
     if (inst->debug)
       CK(cudaMemcpyAsync(inst->dbg + (int64_t)(l + 1) * inst->T_max * H, inst->x, sizeof(float) * (int64_t)T * H,

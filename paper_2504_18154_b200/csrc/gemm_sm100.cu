@@ -112,10 +112,22 @@ __device__ __forceinline__ float silu_f(float z) { return __fdividef(z, 1.f + __
 
 // ---------------------------------------------------------------- epilogues
 // Non-swapped: this thread owns output row `m` (token), columns n0..n0+31 in v[].
-__device__ __forceinline__ void epi_rows(const GemmEpi& e, int m, int n0, int n_rows, const uint32_t (&v)[32]) {
+// 1/rms of row m from the per-(N tile) sums of squares a residual epilogue left (nrm_ss_in)
+__device__ __forceinline__ float nrm_row_scale(const GemmEpi& e, int m) {
+  if (!e.nrm_ss_in) return 1.f;
+  float ss = 0.f;
+  for (int t = 0; t < e.nrm_ss_n; ++t) ss += __ldcg(e.nrm_ss_in + (int64_t)t * e.nrm_ss_ld + m);
+  return rsqrtf(ss * e.nrm_inv_h + e.nrm_eps);
+}
+
+// Prefill deferred RMSNorm (GemmEpi::nrm_*): a residual epilogue also writes
+// h = bf16(x * gamma) and accumulates the row's sum of x^2 into *ssq; a consumer epilogue
+// (QKV, SiLU) receives its row's 1/rms(x) as `scale`.
+__device__ __forceinline__ void epi_rows(const GemmEpi& e, int m, int n0, int n_rows, const uint32_t (&v)[32],
+                                         float scale = 1.f, float* ssq = nullptr) {
   float f[32];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * scale;
   const int ncols = min(32, n_rows - n0);
   switch (e.mode) {
     case EPI_F32: {
@@ -154,9 +166,36 @@ __device__ __forceinline__ void epi_rows(const GemmEpi& e, int m, int n0, int n_
           float4 r = *reinterpret_cast<float4*>(o + i);
           r.x += f[i]; r.y += f[i + 1]; r.z += f[i + 2]; r.w += f[i + 3];
           *reinterpret_cast<float4*>(o + i) = r;
+          f[i] = r.x; f[i + 1] = r.y; f[i + 2] = r.z; f[i + 3] = r.w;
         }
       } else {
-        for (int i = 0; i < ncols; ++i) o[i] += f[i];
+        for (int i = 0; i < ncols; ++i) {
+          o[i] += f[i];
+          f[i] = o[i];
+        }
+      }
+      if (e.nrm_h) {  // deferred RMSNorm: h = bf16(x * gamma), sum of x^2
+        bf16* hd = e.nrm_h + (int64_t)m * e.nrm_ldh + n0;
+        float sq = 0.f;
+        if (ncols == 32) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            const uint4 gv = *reinterpret_cast<const uint4*>(e.nrm_gamma + n0 + i);
+            *reinterpret_cast<uint4*>(hd + i) = make_uint4(
+                pack_bf16x2(f[i] * bf16_lo(gv.x), f[i + 1] * bf16_hi(gv.x)),
+                pack_bf16x2(f[i + 2] * bf16_lo(gv.y), f[i + 3] * bf16_hi(gv.y)),
+                pack_bf16x2(f[i + 4] * bf16_lo(gv.z), f[i + 5] * bf16_hi(gv.z)),
+                pack_bf16x2(f[i + 6] * bf16_lo(gv.w), f[i + 7] * bf16_hi(gv.w)));
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sq += f[i] * f[i];
+        } else {
+          for (int i = 0; i < ncols; ++i) {
+            hd[i] = __float2bfloat16_rn(f[i] * __bfloat162float(e.nrm_gamma[n0 + i]));
+            sq += f[i] * f[i];
+          }
+        }
+        if (ssq) *ssq += sq;
       }
     } break;
     case EPI_SILU: {  // rows of W_gu are interleaved (gate j, up j) -> output column n0/2 + j
@@ -832,13 +871,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
       } else {
+        const float rsc = m < m_rows ? nrm_row_scale(epi, m) : 1.f;
+        float ssq = 0.f;
         for (int c0 = 0; c0 < BN; c0 += 32) {
           uint32_t v[32];
           tmem_ld32(tbase + c0, v);
           tc_wait_ld();
           const int n0 = nt * BN + c0;
-          if (m < m_rows && n0 < n_rows) epi_rows(epi, m, n0, n_rows, v);
+          if (m < m_rows && n0 < n_rows) epi_rows(epi, m, n0, n_rows, v, rsc, &ssq);
         }
+        if (epi.nrm_ss_out && m < m_rows) epi.nrm_ss_out[(int64_t)nt * epi.nrm_ss_ld + m] = ssq;
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty_bar[acc]);
@@ -1327,13 +1369,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           __syncwarp();
         }
       } else {
+        const float rsc = m < m_rows ? nrm_row_scale(epi, m) : 1.f;
+        float ssq = 0.f;
         for (int c0 = 0; c0 < BN; c0 += 32) {
           uint32_t v[32];
           tmem_ld32(tbase + c0, v);
           tc_wait_ld();
           const int n0 = nt * BN + c0;
-          if (m < m_rows && n0 < n_rows) epi_rows(epi, m, n0, n_rows, v);
+          if (m < m_rows && n0 < n_rows) epi_rows(epi, m, n0, n_rows, v, rsc, &ssq);
         }
+        if (epi.nrm_ss_out && m < m_rows) epi.nrm_ss_out[(int64_t)nt * epi.nrm_ss_ld + m] = ssq;
       }
       tc_fence_before();
       __syncwarp();

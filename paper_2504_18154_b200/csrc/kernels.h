@@ -72,6 +72,17 @@ struct GemmEpi {
   // output element here -- the peer GPU's receive plane over NVLink, same layout as
   // out / resid -- and the epilogue threads end with fence.sys
   float* out2;
+  // Prefill deferred RMSNorm (non-swapped epilogues): EPI_RESID with nrm_h also writes
+  // nrm_h = bf16(x_new * nrm_gamma) [rows][nrm_ldh] and the row's sum of x_new^2 over its
+  // N tile into nrm_ss_out[nt][row] (row stride nrm_ss_ld); EPI_QKV / EPI_SILU with
+  // nrm_ss_in scale every output by rsqrt(sum over nrm_ss_n tiles * nrm_inv_h + nrm_eps).
+  bf16* nrm_h;
+  int64_t nrm_ldh;
+  const bf16* nrm_gamma;
+  float* nrm_ss_out;
+  const float* nrm_ss_in;
+  int nrm_ss_ld, nrm_ss_n;
+  float nrm_inv_h, nrm_eps;
   // Concurrent decode GEMMs (the gate/up second wave beside the down projection's first K
   // part): flag_set -- CTA 0 stores flag_epoch there once its PDL wait returned (its inputs,
   // and so the inputs of later kernels that read the same buffers, are complete);
