@@ -221,6 +221,16 @@ ecoserve_status ecoserve_get_status(const ecoserve_instance* inst, ecoserve_inst
  * (decode, last step). */
 ecoserve_status ecoserve_debug_hidden(ecoserve_instance* inst, int64_t req_id, int32_t layer, float* out);
 
+/* Debug (engine_config.debug_hidden = 1): replace the token the next decode
+ * step of `req_id` feeds (the request's last generated token) by `token`, so a
+ * test can teacher-force the oracle's greedy sequence (the
+ * GPU's argmax is compared with the oracle's at every step whose oracle top-2
+ * margin exceeds 5e-2). Only the fed id changes: n_generated, KV growth and
+ * the returned tokens are unaffected. INVALID_ARG if token is outside
+ * [0, vocab); UNSUPPORTED without debug_hidden; STATE if the request is
+ * unknown, not yet prefilled or finished. Host-only, no device work. */
+ecoserve_status ecoserve_debug_force_token(ecoserve_instance* inst, int64_t req_id, int32_t token);
+
 /* Device-side timing of the phase work, measured with CUDA events on the
  * instance stream: a phase interval starts after its inputs are resident in HBM
  * (after the host->device copy) and ends before the device->host token copy.

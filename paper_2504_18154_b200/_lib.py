@@ -138,6 +138,7 @@ SIGNATURES = {
     "ecoserve_kv_import": (C.c_int, [P, C.POINTER(ReqState), PI32, P]),
     "ecoserve_get_status": (C.c_int, [P, C.POINTER(InstanceStatus), C.POINTER(ReqStatus), I32]),
     "ecoserve_debug_hidden": (C.c_int, [P, I64, I32, PF32]),
+    "ecoserve_debug_force_token": (C.c_int, [P, I64, I32]),
     "ecoserve_set_profiling": (C.c_int, [P, I32]),
     "ecoserve_get_timing": (C.c_int, [P, C.POINTER(Timing), I32]),
     "ecoserve_instance_destroy": (None, [P]),

@@ -2645,4 +2645,13 @@ ecoserve_status ecoserve_debug_hidden(ecoserve_instance* inst, int64_t req_id, i
   return ECOSERVE_OK;
 }
 
+ecoserve_status ecoserve_debug_force_token(ecoserve_instance* inst, int64_t req_id, int32_t token) {
+  if (!inst || token < 0 || token >= inst->V) return ECOSERVE_ERR_INVALID_ARG;
+  if (!inst->debug) return ECOSERVE_ERR_UNSUPPORTED;
+  auto it = inst->reqs.find(req_id);
+  if (it == inst->reqs.end() || it->second.n_gen < 1 || it->second.finished) return ECOSERVE_ERR_STATE;
+  it->second.last_token = token;
+  return ECOSERVE_OK;
+}
+
 }  // extern "C"

@@ -243,6 +243,10 @@ class Instance:
         L.check(self.lib.ecoserve_get_timing(self.h, C.byref(t), 1 if reset else 0), self.h)
         return t.as_dict()
 
+    def force_token(self, req_id: int, token: int) -> None:
+        """Teacher forcing (debug instances): the next decode step of req_id feeds `token`."""
+        L.check(self.lib.ecoserve_debug_force_token(self.h, int(req_id), int(token)), self.h)
+
     def hidden(self, req_id: int, layer: int, rows: int) -> np.ndarray:
         out = np.zeros((rows, self.shape.hidden), dtype=np.float32)
         L.check(self.lib.ecoserve_debug_hidden(self.h, int(req_id), layer, out.ctypes.data_as(L.PF32)), self.h)

@@ -90,6 +90,52 @@ def test_tiny_prefill_then_decode(name):
     inst.close()
 
 
+@pytest.mark.parametrize("name", ["tiny", "tiny-gqa", "tiny-d128"])
+def test_tiny_teacher_forced_decode(name):
+    """Reading A20 as written: the oracle's greedy sequence is teacher-forced on the GPU
+    (ecoserve_debug_force_token before every decode step), so every one of the 8 x 15
+    steps is comparable: the GPU's argmax must equal the oracle's wherever the oracle's
+    top-2 margin exceeds 5e-2, and the decode row's residual stream after every layer is
+    within the A19 bar at every step (the KV it attends over was written by the GPU's own
+    earlier steps on the same forced ids)."""
+    shape, w, inst = build(name)
+    model = T.Model(shape, w.as_f64())
+    reqs = make_trace("tiny", 8, seed=1, vocab=shape.vocab)
+    first = inst.prefill([(r.req_id, r.prompt, r.output_len) for r in reqs])
+    state = {}
+    for i, r in enumerate(reqs):
+        kv, out = model.prefill(list(r.prompt))
+        state[r.req_id] = [kv, out.token]
+        if first[i] != out.token:
+            assert T.top2_margin(out.logits) <= MARGIN, (r.req_id, T.top2_margin(out.logits))
+    steps = reqs[0].output_len - 1
+    ids = [r.req_id for r in reqs]
+    checked = total = 0
+    worst = 0.0
+    for s in range(steps):
+        for r in reqs:
+            inst.force_token(r.req_id, state[r.req_id][1])
+        toks, _ = inst.decode(ids, 1)
+        for i, r in enumerate(reqs):
+            kv, tok = state[r.req_id]
+            out = model.decode(kv, tok, r.prompt_len + s)
+            total += 1
+            if T.top2_margin(out.logits) > MARGIN:
+                assert toks[i, 0] == out.token, (r.req_id, s, int(toks[i, 0]), out.token)
+                checked += 1
+            for l in range(shape.n_layers + 1):
+                e = rel(inst.hidden(r.req_id, l, 1), out.hidden[l][-1:])
+                worst = max(worst, e)
+                assert e <= HID_TOL, (r.req_id, s, l, e)
+            state[r.req_id][1] = out.token
+    print(f"{name}: {checked}/{total} steps with margin > {MARGIN} compared, worst hidden rel {worst:.2e}")
+    assert checked >= 0.8 * total    # the weight recipe gives ~88-92 % (SURVEY.md 8(d))
+    with pytest.raises(Exception):
+        inst.force_token(reqs[0].req_id, shape.vocab)   # out of range
+    inst.release(ids)
+    inst.close()
+
+
 def test_kv_exhausted_is_all_or_nothing():
     shape, w, inst = build("tiny", n_blocks=4, debug=False)
     rng = np.random.default_rng(0)
