@@ -87,6 +87,18 @@ __device__ __forceinline__ float fast_ex2(float x) {  // MUFU.EX2, flush-to-zero
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA pipe (Cody-Waite: x = n + f, n = round(x) via the 1.5 * 2^23 magic
+// addend, f in [-0.5, 0.5]; degree-3 fit of 2^f, max relative error 7.5e-5 -- below the
+// bf16 rounding P gets anyway). Moves part of the softmax exponentials off the MUFU
+// (16 / clk / SM, tools/umma_probe.cu). x >= -126 keeps the result a non-negative float
+// (masked -inf scores give ~1e-38).
+__device__ __forceinline__ float poly_ex2(float x) {
+  x = fmaxf(x, -126.f);
+  const float xr = __fadd_rn(x, 12582912.f);
+  const float f = x - __fsub_rn(xr, 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05517146f, f, 0.24261115f), f, 0.69326103f), f, 0.99992806f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(xr) << 23));
+}
 // O[tmem] (+)= A[tmem] * B[smem desc]: A (M x 16 bf16 per step, K-major) read from TMEM,
 // 16 bf16 = 8 columns per K step
 __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
@@ -113,6 +125,8 @@ struct TcAttnParams {
   float scale_log2;
   int pv_wait;             // experiment switch: wait for PV(j) before S(j+2) reuses its buffer
   const int* ctx_off;      // optional [n_seq]: cached tokens before this chunk (chunked prefill)
+  long long* trace;        // timing probe: [20][64] clock64 stamps of CTA (trace_tile, 0), or null
+  int trace_tile;
 };
 
 template <int HP>
@@ -368,6 +382,300 @@ __global__ void __launch_bounds__(AttnCfg<HP>::THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// 128-key variant: one q head per CTA, K / V consumed 128 keys (two pool blocks) per step.
+// tools/umma_probe.cu measured why this pays: a tcgen05.mma of N = 64 occupies the pipe
+// ~48 cycles against 32 for its work (N >= 128 runs at the 4096 MAC/cycle rate), and a
+// commit + wait round trip on the issuer's own MMAs costs ~350 idle cycles. Here every
+// MMA has N = 128 (S = Q K^T over 128 keys; O += P V with 128 head dims), and the issuer
+// never waits on its own MMAs: S and P are both double buffered in TMEM and disjoint,
+//   TMEM: S[0] [0,128)  S[1] [128,256)  O [256,384)  P[0] [384,448)  P[1] [448,512)
+// so S(j+2) overwrites only scores the softmax has finished reading, and the softmax
+// writes P(j) into P[j%2] only after PV(j-2) has consumed it.
+//   warp 0   TMA producer: Q (2 panels), then per key tile j the K tile (both 64-key
+//            pool blocks into one 32 KB [128 keys][128 dims] stage, so the S MMA's B
+//            operand is one descriptor) and the two V blocks (16 KB stages: a PV MMA
+//            covers 16 keys, never straddling blocks)
+//   warp 1   TMEM owner + MMA issuer: S(0), S(1); per j: PV(j), S(j+2)
+//   warps 2-5 softmax, thread r = query row r (TMEM lane)
+// A missing second block of the last tile (odd block count) is loaded from the
+// sequence's first block: finite values under keys the causal mask removes.
+namespace t128 {
+constexpr int TKT = 128;                       // keys per step
+constexpr int K_STAGES = 3;                    // 32 KB K tiles
+constexpr int V_STAGES = 6;                    // 16 KB V blocks (3 tiles)
+constexpr int KT_BYTES = TKT * HD * 2;         // 32 KB: 2 panels [128 keys][64 dims]
+constexpr int SMEM = Q_BYTES + K_STAGES * KT_BYTES + V_STAGES * V_BYTES + 1024 + 512;
+constexpr int THREADS = 192;                   // producer, issuer, 4 softmax warps
+constexpr uint32_t S_COL = 0, O_COL = 256, P_COL = 384;
+}  // namespace t128
+
+template <int POLY>
+__global__ void __launch_bounds__(t128::THREADS, 1)
+    attn_prefill_t128_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kvmap,
+                             TcAttnParams p) {
+  using namespace t128;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm;                              // [Q_BYTES]
+  uint8_t* sK = sQ + Q_BYTES;                    // [K_STAGES][KT_BYTES]
+  uint8_t* sV = sK + K_STAGES * KT_BYTES;        // [V_STAGES][V_BYTES]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + V_STAGES * V_BYTES);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = q_full + 1;
+  uint64_t* k_empty = k_full + K_STAGES;
+  uint64_t* v_full = k_empty + K_STAGES;
+  uint64_t* v_empty = v_full + V_STAGES;
+  uint64_t* s_full = v_empty + V_STAGES;   // [2] by buffer
+  uint64_t* p_full = s_full + 2;           // [2]
+  uint64_t* o_done = p_full + 2;           // [2] PV(j) complete, by j parity
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(o_done + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tile = blockIdx.x, h = blockIdx.y;
+  long long* const tr = (p.trace && tile == p.trace_tile && blockIdx.y == 0) ? p.trace : nullptr;
+  const int kvh = h / (p.n_heads / p.n_kv);
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < K_STAGES; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < V_STAGES; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 4);
+      mbar_init(&o_done[b], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&qmap);
+    tma_prefetch(&kvmap);
+  }
+  if (warp == 1) tmem_alloc(tmem_ptr, 512);
+  tc_fence_before();
+  __syncwarp();  // lanes of the role warps reconverge: bar.sync counts whole warps
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_ptr;
+  pdl_trigger();
+  pdl_wait();
+
+  const int seq = p.tiles[2 * tile], q_start = p.tiles[2 * tile + 1];
+  const int tok0 = p.cu_seqlens[seq];
+  const int len = p.cu_seqlens[seq + 1] - tok0;
+  const int off = p.ctx_off ? p.ctx_off[seq] : 0;  // chunked prefill: cached tokens before the chunk
+  const int n_keys = off + min(q_start + TQ, len);  // causal: keys < off + q_start + 128
+  const int n_blk = (n_keys + TK - 1) / TK;
+  const int n_t = (n_keys + TKT - 1) / TKT;
+  const int* bt = p.block_tables + (int64_t)seq * p.bt_ld;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, Q_BYTES);
+      for (int pn = 0; pn < 2; ++pn) tma_load_3d(sQ + pn * (TQ * 128), &qmap, q_full, pn * 64, h, tok0 + q_start);
+      // pool rows: ((block * L + layer) * 2 + kv) * Mkv * 64 + kvh * 64 + token
+      auto row = [&](int b, int kv) {
+        const int blk = bt[b < n_blk ? b : 0];
+        return (int)(((((int64_t)blk * p.n_layers + p.layer) * 2 + kv) * p.n_kv + kvh) * TK);
+      };
+      for (int j = 0; j < n_t; ++j) {
+        const int ks = j % K_STAGES;
+        if (j >= K_STAGES) mbar_wait(&k_empty[ks], ((j / K_STAGES) - 1) & 1);
+        uint8_t* sk = sK + ks * KT_BYTES;
+        mbar_arrive_expect_tx(&k_full[ks], KT_BYTES);
+        for (int hb = 0; hb < 2; ++hb) {
+          const int kr = row(2 * j + hb, 0);
+          for (int pn = 0; pn < 2; ++pn)
+            tma_load_2d(sk + pn * (TKT * 128) + hb * (TK * 128), &kvmap, &k_full[ks], pn * 64, kr);
+        }
+        for (int hb = 0; hb < 2; ++hb) {
+          const int b = 2 * j + hb, vs = b % V_STAGES;
+          if (b >= V_STAGES) mbar_wait(&v_empty[vs], ((b / V_STAGES) - 1) & 1);
+          uint8_t* sv = sV + vs * V_BYTES;
+          const int vr = row(b, 1);
+          mbar_arrive_expect_tx(&v_full[vs], V_BYTES);
+          for (int pn = 0; pn < 2; ++pn) tma_load_2d(sv + pn * (TK * 128), &kvmap, &v_full[vs], pn * 64, vr);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_s = idesc(TQ, TKT, 0);
+      constexpr uint32_t id_o = idesc(TQ, HD, 1);
+      const uint32_t aq = smem_u32(sQ);
+      auto mma_s = [&](int j) {  // S[j%2] = Q K_j^T
+        const int ks = j % K_STAGES;
+        mbar_wait(&k_full[ks], (j / K_STAGES) & 1);
+        tc_fence_after();
+        const uint32_t ak = smem_u32(sK + ks * KT_BYTES);
+        const uint32_t d = tmem + S_COL + (j & 1) * 128;
+#pragma unroll
+        for (int pn = 0; pn < 2; ++pn) {
+          const uint64_t da = umma_desc_sw128(aq + pn * (TQ * 128)), db = umma_desc_sw128(ak + pn * (TKT * 128));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) tc_mma_f16(d, da + 2 * k, db + 2 * k, id_s, (pn | k) ? 1u : 0u);
+        }
+        tc_commit(&s_full[j & 1]);
+        tc_commit(&k_empty[ks]);
+      };
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      mma_s(0);
+      if (n_t > 1) mma_s(1);
+      for (int j = 0; j < n_t; ++j) {
+        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+        tc_fence_after();
+        if (tr && j < 64) tr[16 * 64 + j] = clock64();   // row 16: P_j seen by the issuer
+        const uint32_t ap = tmem + P_COL + (j & 1) * 64;
+#pragma unroll
+        for (int hb = 0; hb < 2; ++hb) {
+          const int b = 2 * j + hb, vs = b % V_STAGES;
+          mbar_wait(&v_full[vs], (b / V_STAGES) & 1);
+          tc_fence_after();
+          const uint32_t av = smem_u32(sV + vs * V_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)  // 16 keys per MMA: +8 TMEM columns of P, +2 x 1024 B along V rows
+            tc_mma_ts(tmem + O_COL, ap + 8 * (4 * hb + k), desc_mn_sw128(av + k * 2048, TK * 128), id_o,
+                      (j > 0 || hb > 0 || k > 0) ? 1u : 0u);
+          tc_commit(&v_empty[vs]);
+        }
+        tc_commit(&o_done[j & 1]);
+        if (j + 2 < n_t) {
+          mma_s(j + 2);
+          if (tr && j < 64) tr[18 * 64 + j] = clock64();   // row 18: S(j+2) issued
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warps
+    const int q = warp & 3;                   // TMEM lane quarter accessible to this warp
+    const int r = q * 32 + lane;              // query row = TMEM lane
+    const int qpos = off + q_start + r;       // position of this query row
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < n_t; ++j) {
+      const uint32_t sb = lane_base + S_COL + (j & 1) * 128;
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      const bool trw = tr && lane == 0 && j < 64;
+      if (trw) tr[(8 + warp - 2) * 64 + j] = clock64();   // rows 8..11: S_j seen by softmax warp
+      float sv[TKT];
+#pragma unroll
+      for (int c0 = 0; c0 < TKT; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(sb + c0, v);
+        tc_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[c0 + i] = __uint_as_float(v[i]);
+      }
+      // causal mask on the diagonal tiles; the row max in raw score units (scale > 0)
+      if (j * TKT + TKT - 1 > off + q_start) {
+#pragma unroll
+        for (int c = 0; c < TKT; ++c)
+          if (j * TKT + c > qpos) sv[c] = -INFINITY;
+      }
+      float mx8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx8[i] = sv[i];
+#pragma unroll
+      for (int c = 8; c < TKT; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], sv[c]);
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * p.scale_log2;
+      const float m_new = fmaxf(m_run, mx);
+      if (j == 0) {
+        m_run = m_new;
+      } else {
+        const bool need = m_new > m_run + RESCALE_LOG2;
+        if (__any_sync(0xffffffffu, need)) {
+          // O (TMEM) *= exp2(m_run - m_new) for the rows whose max grew past the threshold;
+          // PV(j-1) must have landed, PV(j) is not issued before this warp's P_j arrives
+          const float corr = need ? exp2f(m_run - m_new) : 1.f;
+          if (need) m_run = m_new;
+          l_run *= corr;
+          mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c0 = 0; c0 < HD; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(lane_base + O_COL + c0, v);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+            tmem_st32(lane_base + O_COL + c0, v);
+          }
+        }
+      }
+      // P = 2^(s * scale - m_run); key 0 is never masked, so m_run is finite for every row
+      float rs8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rs8[i] = 0.f;
+      const float neg_m = -m_run;
+      // P[j%2] was last read by PV(j-2): wait for it before overwriting (long complete)
+      if (j >= 2) {
+        mbar_wait(&o_done[j & 1], ((j - 2) >> 1) & 1);
+        tc_fence_after();
+      }
+#pragma unroll
+      for (int h32 = 0; h32 < 2; ++h32) {  // 64 keys -> 32 columns of bf16 pairs per store
+        uint32_t pk[32];
+#pragma unroll
+        for (int c = 0; c < 64; c += 2) {
+          const int cc = h32 * 64 + c;
+          const bool poly = ((c >> 1) & 7) < POLY;
+          const float xa = fmaf(sv[cc], p.scale_log2, neg_m), xb = fmaf(sv[cc + 1], p.scale_log2, neg_m);
+          const float a = poly ? poly_ex2(xa) : fast_ex2(xa);
+          const float b = poly ? poly_ex2(xb) : fast_ex2(xb);
+          rs8[(c >> 1) & 7] += a + b;
+          pk[c / 2] = pack_bf16x2(a, b);
+        }
+        tmem_st32(lane_base + P_COL + (j & 1) * 64 + h32 * 32, pk);
+      }
+      l_run += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+      tc_wait_st();
+      if (trw) tr[(warp - 2) * 64 + j] = clock64();   // rows 0..3: P_j stored by softmax warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[j & 1]);
+    }
+    if (n_t > 0) {
+      mbar_wait(&o_done[(n_t - 1) & 1], ((n_t - 1) >> 1) & 1);
+      tc_fence_after();
+    }
+    const float inv = 1.f / l_run;
+    const int lrow = q_start + r;             // row of the chunk
+    bf16* dst = p.out + (int64_t)(tok0 + lrow) * p.n_heads * HD + h * HD;
+#pragma unroll
+    for (int c0 = 0; c0 < HD; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(lane_base + O_COL + c0, v);
+      tc_wait_ld();
+      if (lrow < len) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+          *reinterpret_cast<uint4*>(dst + c0 + i) = make_uint4(
+              pack_bf16x2(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv),
+              pack_bf16x2(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv),
+              pack_bf16x2(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv),
+              pack_bf16x2(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncwarp();  // lanes of the role warps reconverge: bar.sync counts whole warps
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    __syncwarp();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // q: [q_rows][n_heads][128] bf16 (TMA 3D map over the whole buffer); pool: the instance's
 // block-major pool (2D map over rows of 128 elements).
 int make_attn_tc_maps(CUtensorMap* qmap, CUtensorMap* kvmap, const void* q, int64_t q_rows, int n_heads,
@@ -382,11 +690,43 @@ int make_attn_tc_maps(CUtensorMap* qmap, CUtensorMap* kvmap, const void* q, int6
   return make_tmap_bf16_nd(kvmap, pool, 2, kd, ks, kb);
 }
 
+static long long* g_trace = nullptr;
+static int g_trace_tile = 0;
+void attn_tc_set_trace(long long* trace, int trace_tile) {
+  g_trace = trace;
+  g_trace_tile = trace_tile;
+}
+
 cudaError_t attn_prefill_tc_launch(const CUtensorMap* qmap, const CUtensorMap* kvmap, const int* cu_seqlens,
                                    const int* block_tables, int bt_ld, const int* tiles, int n_tiles, bf16* out,
                                    int n_heads, int n_kv, int layer, int n_layers, cudaStream_t s,
                                    const int* ctx_off) {
   if (n_kv < 1 || n_heads % n_kv) return cudaErrorInvalidValue;
+  static const int t128_mode = [] {
+    const char* ev = getenv("ECOSERVE_ATTN_T128");
+    return ev ? atoi(ev) : 0;
+  }();
+  if (t128_mode) {  // opt-in 128-key kernel; 2 = with the poly-exp2 offload
+    auto k = t128_mode == 2 ? attn_prefill_t128_kernel<1> : attn_prefill_t128_kernel<0>;
+    cudaError_t e = ensure_smem(k, t128::SMEM);
+    if (e != cudaSuccess || n_tiles == 0) return e;
+    TcAttnParams p;
+    p.cu_seqlens = cu_seqlens;
+    p.block_tables = block_tables;
+    p.bt_ld = bt_ld;
+    p.tiles = tiles;
+    p.out = out;
+    p.n_heads = n_heads;
+    p.n_kv = n_kv;
+    p.layer = layer;
+    p.n_layers = n_layers;
+    p.scale_log2 = (float)(1.4426950408889634 / sqrt((double)HD));
+    p.ctx_off = ctx_off;
+    p.pv_wait = 0;
+    p.trace = g_trace;
+    p.trace_tile = g_trace_tile;
+    return launch_k(k, dim3(n_tiles, n_heads), dim3(t128::THREADS), t128::SMEM, s, *qmap, *kvmap, p);
+  }
   const bool pair = (n_heads / n_kv) % 2 == 0;  // two q heads of one kv head per CTA
   cudaError_t e = pair ? ensure_smem(attn_prefill_tc_kernel<2>, AttnCfg<2>::SMEM)
                        : ensure_smem(attn_prefill_tc_kernel<1>, AttnCfg<1>::SMEM);
@@ -404,6 +744,8 @@ cudaError_t attn_prefill_tc_launch(const CUtensorMap* qmap, const CUtensorMap* k
   p.n_layers = n_layers;
   p.scale_log2 = (float)(1.4426950408889634 / sqrt((double)HD));
   p.ctx_off = ctx_off;
+  p.trace = nullptr;
+  p.trace_tile = 0;
   {
     const char* ev = getenv("ECOSERVE_ATTN_PVWAIT");
     p.pv_wait = (ev && ev[0] == '0') ? 0 : 1;

@@ -213,6 +213,9 @@ int make_attn_tc_maps(CUtensorMap* qmap, CUtensorMap* kvmap, const void* q, int6
                       const void* pool, int64_t pool_rows);
 // ctx_off (optional [n_seq]): tokens of each sequence already in the pool before this
 // chunk; its q rows sit at positions ctx_off + i and attend to pool keys 0..position.
+// timing probe (tools/attn_bench): when set, CTA (trace_tile, 0) of the next launches
+// records clock64 stamps per KV block into trace[20][64] (see attention_tc.cu)
+void attn_tc_set_trace(long long* trace, int trace_tile);
 cudaError_t attn_prefill_tc_launch(const CUtensorMap* qmap, const CUtensorMap* kvmap, const int* cu_seqlens,
                                    const int* block_tables, int bt_ld, const int* tiles, int n_tiles, bf16* out,
                                    int n_heads, int n_kv, int layer, int n_layers, cudaStream_t s,

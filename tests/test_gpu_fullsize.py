@@ -146,7 +146,7 @@ def test_fullwidth_70b_tp2():
 
 
 @pytest.mark.parametrize("env", ["ECOSERVE_GU_SK=1", "ECOSERVE_FLOW=1", "ECOSERVE_ATTN_SK=1", "ECOSERVE_GU_WAVES=1",
-                                 "ECOSERVE_QKV_FUSE=1"])
+                                 "ECOSERVE_QKV_FUSE=1", "ECOSERVE_ATTN_T128=1"])
 def test_fullwidth_decode_variants(env):
     """Every decode variant switch at full 8B / 34B widths and bench-like batches, against
     the same oracle bars (fresh process: the switches are read once). GU_SK: stream-K

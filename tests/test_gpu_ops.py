@@ -205,6 +205,26 @@ def test_attention_prefill_tcgen05(ops, M, Mkv, lens):
         assert rel_err(got[cu[i]:cu[i + 1]], ref) < 1e-2, (i, S)
 
 
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_attention_prefill_t128_variant(mode):
+    """The opt-in 128-key prefill attention kernel (ECOSERVE_ATTN_T128=1; =2 adds the
+    polynomial exp2 offload) against the same oracle cases as the default kernel --
+    ragged lengths, odd block counts, GQA groups 1 / 4 and chunked prefill (fresh
+    process: the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("ECOSERVE_ATTN_T128") == mode:
+        pytest.skip("already running with this switch")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.abspath(__file__), "-k",
+                        "attention_prefill_tcgen05 or (attention_prefill_chunked and True)"],
+                       env={**os.environ, "ECOSERVE_ATTN_T128": mode}, cwd=root, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
+
+
 @pytest.mark.parametrize("tc", [False, True])
 @pytest.mark.parametrize("M,Mkv", [(8, 2), (4, 4)])
 def test_attention_prefill_chunked(ops, tc, M, Mkv):

@@ -106,6 +106,25 @@ int main(int argc, char** argv) {
       return best * 1e3f;
     };
     const float t_tc = time(run_tc), t_mma = time(run_mma);
+    if (getenv("ATTN_TRACE") && n == 1) {   // per-block clock64 stamps of one 64-block CTA (tile 31)
+      long long* d_tr;
+      cudaMalloc(&d_tr, 20 * 64 * sizeof(long long));
+      cudaMemset(d_tr, 0, 20 * 64 * sizeof(long long));
+      attn_tc_set_trace(d_tr, 31);
+      run_tc();
+      cudaStreamSynchronize(st);
+      attn_tc_set_trace(nullptr, 0);
+      long long h[20 * 64];
+      cudaMemcpy(h, d_tr, sizeof(h), cudaMemcpyDeviceToHost);
+      const long long t0 = h[8 * 64];
+      printf("# j: P stored by softmax warps 2..9 | S seen by warps 2..9 | P0, P1 seen by issuer | S(j+2) 0, 1 issued (cycles)\n");
+      for (int j = 0; j < 64; ++j) {
+        printf("%2d", j);
+        for (int r = 0; r < 20; ++r) printf(" %7lld", h[r * 64 + j] ? h[r * 64 + j] - t0 : -1);
+        printf("\n");
+      }
+      cudaFree(d_tr);
+    }
     double flop = 0;
     for (int s : lens) flop += 2.0 * M * D * (double)s * (s + 1);  // causal QK^T + PV
     cudaError_t err = cudaStreamSynchronize(st);
