@@ -40,6 +40,19 @@ ecoserve_status ecoserve_op_gemm_swap_bf16(const void* W, const void* X, int32_t
 ecoserve_status ecoserve_op_gemm_decode(const void* W, const void* X, int32_t m, int32_t n, int32_t k, int32_t r,
                                         int32_t splits, float* ws, float* out, int32_t bn, void* stream);
 
+/* The same decode GEMM with the balanced split-K (the engine's O / down / QKV
+ * projections when their weight tiles are fewer than the SMs; Table 2 P:232-236,
+ * SURVEY 8(a) rows a13, a15): the ceil(m/128) x ceil(k/64) sequence of (weight tile,
+ * K block) units is cut into equal chunks of *chunk units, one CTA per chunk, so every
+ * SM streams the same number of weight blocks; each CTA writes the f32 partial of every
+ * tile its chunk touches into slot (cta - first cta of the tile) of ws, and the reduction
+ * sums each tile's slots in K order. n <= bn (one token tile). ws: f32
+ * [max_slots][n][m] (device, caller-owned). *chunk (host) receives the chunk length
+ * used (0: no balanced split exists for these sizes -> ECOSERVE_ERR_INVALID_ARG). */
+ecoserve_status ecoserve_op_gemm_decode_balanced(const void* W, const void* X, int32_t m, int32_t n, int32_t k,
+                                                 int32_t max_slots, float* ws, float* out, int32_t bn,
+                                                 int32_t* chunk, void* stream);
+
 /* Decode GEMM with the K split over the CTAs of a thread-block cluster and the split
  * reduction in distributed shared memory (no partials in HBM): out f32 [n][m] =
  * X W^T, partials summed in split order. splits 2..4 (clamped so every split owns a

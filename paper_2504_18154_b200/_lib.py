@@ -162,6 +162,7 @@ SIGNATURES = {
     "ecoserve_op_gemm_swap_bf16": (C.c_int, [P, P, I32, I32, I32, I32, P, P, P, I32, P]),
     "ecoserve_op_gemm_cluster": (C.c_int, [P, P, I32, I32, I32, I32, P, I32, P]),
     "ecoserve_op_gemm_decode": (C.c_int, [P, P, I32, I32, I32, I32, I32, P, P, I32, P]),
+    "ecoserve_op_gemm_decode_balanced": (C.c_int, [P, P, I32, I32, I32, I32, P, P, I32, PI32, P]),
     "ecoserve_op_lm_argmax": (C.c_int, [P, P, I32, I32, I32, P, P, P, P]),
     "ecoserve_op_rmsnorm": (C.c_int, [P, P, P, P, I32, I32, F32, P]),
     "ecoserve_op_attention_prefill": (C.c_int, [P, P, I64, I32, I32, I32, PI32, I32, P, I32, P, P, PI32]),

@@ -1141,6 +1141,26 @@ unsigned long long* gu_trace_buf(ecoserve_instance* inst) {
   return inst->gu_trace;
 }
 
+// ECOSERVE_DEC_SK=1: the split decode projections (O, down, QKV when their weight tiles
+// are fewer than the SMs) use the balanced split (GemmEpi::sk_L) instead of a uniform one
+bool dec_sk_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_DEC_SK");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// Chunk length of the balanced split of an n_out x K decode projection (0 = use the
+// uniform split): one token tile, at most 8 partial slots per tile (inst->part holds 8
+// planes of B_max x the widest split output).
+int balanced_chunk(ecoserve_instance* inst, int n_out, int K, int B) {
+  const int bn = B <= 64 ? 64 : 128;
+  if (!dec_sk_enabled() || B > bn) return 0;
+  return gemm_sk_chunk((n_out + 127) / 128, (K + 63) / 64, inst->num_sms, 8);
+}
+
 cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const ActMaps& xm, int n_out, int K, int B,
                         int mode, GemmEpi e, int* nk, const bf16* norm_gamma = nullptr, bf16* norm_out = nullptr,
                         bool* fused = nullptr, const CUtensorMap* wmap256 = nullptr) {
@@ -1205,14 +1225,20 @@ cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const 
   ge.mode = EPI_SWAP_F32;
   ge.out = inst->part;
   ge.ldo = n_out;
-  cudaError_t r =
-      gemm_launch_r(wm, &xm.b[bn_index(bn)], n_out, B, K, bn, var, splits, ge, inst->num_sms, inst->stream);
+  int sk_L = 0;
+  if (!r2 && var == 1) sk_L = balanced_chunk(inst, n_out, K, B);
+  if (sk_L > 0) {  // balanced split: equal K-block chunks on every SM
+    ge.sk_L = e.sk_L = sk_L;
+    ge.sk_kbt = e.sk_kbt = (K + 63) / 64;
+  }
+  cudaError_t r = gemm_launch_r(wm, &xm.b[bn_index(bn)], n_out, B, K, bn, var, sk_L > 0 ? 1 : splits, ge,
+                                inst->num_sms, inst->stream);
   if (r != cudaSuccess) return r;
   if (norm_gamma && mode == EPI_SWAP_RESID && n_out == inst->H) {
     *nk = 2;
     if (fused) *fused = true;
     return splitk_resid_rmsnorm_launch(inst->part, splits, B, inst->x, norm_gamma, norm_out, inst->H,
-                                       inst->shape.rms_eps, inst->stream);
+                                       inst->shape.rms_eps, inst->stream, ge.sk_L, ge.sk_kbt);
   }
   const int red = mode == EPI_SWAP_QKV ? RED_QKV : mode == EPI_SWAP_SILU ? RED_SILU
                 : mode == EPI_SWAP_RESID ? RED_RESID : mode == EPI_SWAP_STORE ? RED_F32 : RED_BF16;
@@ -1240,8 +1266,9 @@ GemmEpi tp_push_epi(ecoserve_instance* inst, int ep) {
 
 // Decode O / down projection of a TP rank: raw f32 split partials [splits][B][n_out] in
 // inst->part (bulk-stored, L2-resident), summed and pushed row by row by tp_push_rows.
+// sk (optional): the balanced split's chunk / K blocks when it was used (sk[0] = 0 otherwise)
 cudaError_t decode_partials(ecoserve_instance* inst, const CUtensorMap& wmap, const ActMaps& xm, int n_out, int K,
-                            int B, int* splits_out) {
+                            int B, int* splits_out, int* sk = nullptr) {
   const int bn = B <= 64 ? 64 : 128;
   const int splits = gemm_effective_splits(K, gemm_decode_splits(n_out, K, inst->num_sms));
   GemmEpi ge = epi_base(inst);
@@ -1250,7 +1277,17 @@ cudaError_t decode_partials(ecoserve_instance* inst, const CUtensorMap& wmap, co
   ge.ldo = n_out;
   ge.indep = 1;
   *splits_out = splits;
-  return gemm_launch_r(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, decode_variant(), splits, ge, inst->num_sms,
+  const int var = decode_variant();
+  const int L = (sk && splits > 1 && var == 1) ? balanced_chunk(inst, n_out, K, B) : 0;
+  if (sk) {
+    sk[0] = L;
+    sk[1] = (K + 63) / 64;
+  }
+  if (L > 0) {
+    ge.sk_L = L;
+    ge.sk_kbt = (K + 63) / 64;
+  }
+  return gemm_launch_r(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, var, L > 0 ? 1 : splits, ge, inst->num_sms,
                        inst->stream);
 }
 
@@ -1283,8 +1320,11 @@ cudaError_t decode_partials_push(ecoserve_instance* inst, const CUtensorMap& wma
   return gemm_launch_r(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, 1, splits, ge, inst->num_sms, inst->stream);
 }
 
-cudaError_t tp_push_rows(ecoserve_instance* inst, int ep, int splits, int rows, const bf16* gamma, bf16* h) {
+cudaError_t tp_push_rows(ecoserve_instance* inst, int ep, int splits, int rows, const bf16* gamma, bf16* h,
+                         const int* sk = nullptr) {
   TpRowsArgs a;
+  a.sk_L = sk ? sk[0] : 0;
+  a.sk_kbt = sk ? sk[1] : 0;
   a.part = inst->part;
   a.splits = splits;
   a.plane = (int64_t)rows * inst->H;
@@ -1784,8 +1824,9 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
                decode_partials_push(inst, w.o_a, inst->m_ao, H, M * D, B, ep, &sp));
         LAUNCH(P_OTHER, 0, 1, tp_allreduce(inst, ep, B, w.ffn_norm, inst->h, sp));
       } else {
-        LAUNCH(P_GEMM_DECODE, 2.0 * H * M * D, 1, decode_partials(inst, w.o_a, inst->m_ao, H, M * D, B, &sp));
-        LAUNCH(P_OTHER, 0, 1, tp_push_rows(inst, ep, sp, B, w.ffn_norm, inst->h));
+        int skp[2] = {0, 0};
+        LAUNCH(P_GEMM_DECODE, 2.0 * H * M * D, 1, decode_partials(inst, w.o_a, inst->m_ao, H, M * D, B, &sp, skp));
+        LAUNCH(P_OTHER, 0, 1, tp_push_rows(inst, ep, sp, B, w.ffn_norm, inst->h, skp));
       }
     } else {
       GemmEpi eo = resid_epi(inst);
@@ -1896,8 +1937,9 @@ static ecoserve_status run_layers_decode(ecoserve_instance* inst, int B, const i
         LAUNCH(P_GEMM_DECODE, 2.0 * H * F, 1, decode_partials_push(inst, w.d_a, inst->m_act, H, F, B, ep, &sp));
         LAUNCH(P_OTHER, 0, 1, tp_allreduce(inst, ep, B, g_next, h_next, sp));
       } else {
-        LAUNCH(P_GEMM_DECODE, 2.0 * H * F, 1, decode_partials(inst, w.d_a, inst->m_act, H, F, B, &sp));
-        LAUNCH(P_OTHER, 0, 1, tp_push_rows(inst, ep, sp, B, g_next, h_next));
+        int skp[2] = {0, 0};
+        LAUNCH(P_GEMM_DECODE, 2.0 * H * F, 1, decode_partials(inst, w.d_a, inst->m_act, H, F, B, &sp, skp));
+        LAUNCH(P_OTHER, 0, 1, tp_push_rows(inst, ep, sp, B, g_next, h_next, skp));
       }
       fused = true;
     } else {

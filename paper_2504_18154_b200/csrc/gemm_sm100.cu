@@ -14,6 +14,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <map>
 #include <mutex>
 
@@ -346,6 +347,36 @@ __device__ __forceinline__ void epi_swap(const GemmEpi& e, int m, int m_rows, in
   }
 }
 
+// The p-th work piece of this CTA: weight tile mt, token tile nt, K blocks [kb0, kb1),
+// partial plane ks. Uniform split: unit w = blockIdx.x + p * gridDim.x of the
+// (tile, split) grid. Balanced split (epi.sk_L > 0, one token tile): the tiles this CTA's
+// chunk [c * L, (c + 1) * L) of the (tile, K block) sequence touches, in order.
+struct GemmPieces {
+  int n_work, splits, n_tiles, kb_total, kb_per, sk_L, sk_units;
+  __device__ __forceinline__ bool get(int p, int& mt, int& nt, int& ks, int& kb0, int& kb1) const {
+    if (sk_L > 0) {
+      const int u0 = blockIdx.x * sk_L, u1 = min(sk_units, u0 + sk_L);
+      const int t = u0 / kb_total + p;
+      if (t * kb_total >= u1) return false;
+      mt = t;
+      nt = 0;
+      kb0 = max(u0, t * kb_total) - t * kb_total;
+      kb1 = min(u1, (t + 1) * kb_total) - t * kb_total;
+      ks = blockIdx.x - (t * kb_total) / sk_L;
+      return true;
+    }
+    const int w = blockIdx.x + p * gridDim.x;
+    if (w >= n_work) return false;
+    ks = w % splits;
+    const int t = w / splits;
+    mt = t / n_tiles;
+    nt = t % n_tiles;
+    kb0 = ks * kb_per;
+    kb1 = min(kb_total, kb0 + kb_per);
+    return true;
+  }
+};
+
 template <int BN, int RV>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int m_rows,
@@ -373,6 +404,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int kb_total = (K + BK - 1) / BK;
   const int kb_per = (kb_total + splits - 1) / splits;
   const int n_work = m_tiles * n_tiles * splits;
+  const GemmPieces pcs{n_work, splits, n_tiles, kb_total, kb_per, epi.sk_L, m_tiles * kb_total};
   // bulk-store epilogue: f32 partials / SiLU output with 16-byte aligned token rows
   const bool bulk_epi =
       C::BULK_EPI && (reinterpret_cast<uintptr_t>(epi.out) & 15) == 0 &&
@@ -491,17 +523,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      // iteration cursor over this CTA's (work unit, K block) sequence
-      int w = blockIdx.x, kb = -1, kb1 = 0, mt = 0, nt = 0;
+      // iteration cursor over this CTA's (work piece, K block) sequence
+      int p = 0, kb = -1, kb1 = 0, mt = 0, nt = 0;
       auto next = [&]() -> bool {
         if (kb >= 0 && kb + 1 < kb1) { ++kb; return true; }
-        if (kb >= 0) w += gridDim.x;
-        if (w >= n_work) return false;
-        const int ks = w % splits, t = w / splits;
-        mt = t / n_tiles;
-        nt = t % n_tiles;
-        kb = ks * kb_per;
-        kb1 = min(kb_total, kb + kb_per);
+        if (kb >= 0) ++p;
+        int ks_, kb0_;
+        if (!pcs.get(p, mt, nt, ks_, kb0_, kb1)) return false;
+        kb = kb0_;
         return true;
       };
       // 1) the operand that does not depend on the previous kernel (the weights) is
@@ -522,13 +551,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         //     the previous kernel's tail (attention / reduction, SMs freeing up under PDL)
         //     also streams this GEMM's weights; the loads after the wait then hit L2
         if (indep == 1 && epi.l2_pf_kb > 0) {
-          const int sw = w, skb = kb, skb1 = kb1, smt = mt, snt = nt;
+          const int sw = p, skb = kb, skb1 = kb1, smt = mt, snt = nt;
           for (int n = 0; n < epi.l2_pf_kb && next(); ++n)
             asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
                              reinterpret_cast<uint64_t>(&mapA)),
                          "r"(kb * BK), "r"(mt * BM * R)
                          : "memory");
-          w = sw; kb = skb; kb1 = skb1; mt = smt; nt = snt;  // rewind the cursor
+          p = sw; kb = skb; kb1 = skb1; mt = smt; nt = snt;  // rewind the cursor
         }
       }
       gemm_dep_wait(epi);
@@ -575,9 +604,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       bool first = true;
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-        const int ks = w % splits;
-        const int kb0 = ks * kb_per, kb1 = min(kb_total, kb0 + kb_per);
+      int mt_, nt_, ks_, kb0, kb1;
+      for (int p = 0; pcs.get(p, mt_, nt_, ks_, kb0, kb1); ++p) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
@@ -612,10 +640,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int ep_tid = (warp - 2) * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-      const int ks = w % splits;
-      const int t = w / splits;
-      const int mt = t / n_tiles, nt = t % n_tiles;
+    int mt, nt, ks, kb0_, kb1_;
+    for (int p = 0; pcs.get(p, mt, nt, ks, kb0_, kb1_); ++p) {
+      const int t = mt * n_tiles + nt;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       if (threadIdx.x == 64) trace_mark(epi, 5);  // accumulator ready
@@ -1533,6 +1560,17 @@ int gemm_decode_splits(int m_rows, int K, int num_sms) {
   return best;
 }
 
+int gemm_sk_chunk(int m_tiles, int kbt, int num_sms, int max_slots) {
+  const int U = m_tiles * kbt;
+  if (m_tiles <= 0 || kbt <= 0 || m_tiles >= num_sms) return 0;
+  for (int L = (U + num_sms - 1) / num_sms; L <= kbt; ++L) {
+    int mx = 0;
+    for (int t = 0; t < m_tiles; ++t) mx = std::max(mx, sk_slots(t, kbt, L));
+    if (mx <= max_slots) return L;
+  }
+  return 0;
+}
+
 int gemm_smem_bytes(int bn) {
   switch (bn) {
     case 64: return GemmCfg<64, 1>::SMEM;
@@ -1549,7 +1587,8 @@ static cudaError_t launch_bn(const CUtensorMap* mapA, const CUtensorMap* mapB, i
   if (e != cudaSuccess) return e;
   const int m_tiles = (m_rows + BM * C::RT - 1) / (BM * C::RT), n_tiles = (n_rows + BN - 1) / BN;
   const int work = m_tiles * n_tiles * splits;
-  const int grid = work < num_sms ? work : num_sms;
+  int grid = work < num_sms ? work : num_sms;
+  if (epi.sk_L > 0) grid = (m_tiles * epi.sk_kbt + epi.sk_L - 1) / epi.sk_L;  // one chunk per CTA
   if (grid <= 0) return cudaSuccess;
   return launch_k(gemm_tc_kernel<BN, R>, dim3(grid), dim3(GEMM_THREADS), C::SMEM, stream, *mapA, *mapB, m_rows,
                   n_rows, K, splits, epi);
@@ -1558,6 +1597,10 @@ static cudaError_t launch_bn(const CUtensorMap* mapA, const CUtensorMap* mapB, i
 cudaError_t gemm_launch_r(const CUtensorMap* mapA, const CUtensorMap* mapB, int m_rows, int n_rows, int K, int bn,
                           int r, int splits, const GemmEpi& epi, int num_sms, cudaStream_t stream) {
   if (splits < 1) return cudaErrorInvalidValue;
+  if (epi.sk_L > 0 && (epi.mode != EPI_SWAP_F32 || r != 1 || splits != 1 || n_rows > bn ||
+                       epi.sk_kbt != (K + BK - 1) / BK ||
+                       (int64_t)((m_rows + BM - 1) / BM) * epi.sk_kbt > (int64_t)epi.sk_L * num_sms))
+    return cudaErrorInvalidValue;
   if (splits > 1 && epi.mode != EPI_SWAP_F32 && epi.mode < EPI_SWAP_BF16) return cudaErrorInvalidValue;
   if (splits > 1 && epi.mode >= EPI_SWAP_BF16 && (!epi.part || !epi.counters)) return cudaErrorInvalidValue;
   splits = gemm_effective_splits(K, splits);

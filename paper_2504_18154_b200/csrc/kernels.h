@@ -99,7 +99,22 @@ struct GemmEpi {
   // deferred RMSNorm (decode flow path): the GEMM input was bf16(x * gamma), so the QKV
   // epilogues (EPI_SWAP_QKV, RED_QKV) multiply token n's outputs by rvec[n] = 1/rms(x_n)
   const float* rvec;
+  // balanced split-K of a decode projection (EPI_SWAP_F32 partials, one token tile,
+  // sk_L > 0): the m_tiles x sk_kbt sequence of (weight tile, K block) units is cut into
+  // equal chunks of sk_L units and CTA c streams chunk c, so every SM streams the same
+  // number of K blocks (a uniform split leaves tiles x splits CTAs, e.g. 128 of 148 SMs,
+  // busy). Its piece of tile t goes to partial slot c - (t * sk_kbt) / sk_L; tile t has
+  // sk_slots(t) slots, summed in slot (= K) order by the reductions.
+  int sk_L, sk_kbt;
 };
+
+// Partial slots of weight tile `tile` under the balanced split (see GemmEpi::sk_L).
+__host__ __device__ __forceinline__ int sk_slots(int tile, int kbt, int L) {
+  return ((tile + 1) * kbt - 1) / L - (tile * kbt) / L + 1;
+}
+// Balanced chunk length for m_tiles weight tiles of kbt K blocks on num_sms SMs, at
+// most max_slots partial slots per tile; 0 when a uniform split is at least as balanced.
+int gemm_sk_chunk(int m_tiles, int kbt, int num_sms, int max_slots);
 
 // Split count for a decode GEMM: minimises waves x K-blocks per CTA (+ a per-split reduction cost).
 int gemm_choose_splits(int m_rows, int n_rows, int K, int bn, int num_sms, int max_splits);
@@ -298,6 +313,7 @@ struct TpRowsArgs {
   const int* my_flags;
   int* err;                // as TpAllreduceArgs
   unsigned long long timeout_ns;
+  int sk_L, sk_kbt;        // balanced split (GemmEpi::sk_L): per-tile slot counts instead of splits
 };
 cudaError_t tp_push_rows_launch(const TpRowsArgs& a, int num_sms, cudaStream_t s);
 
@@ -370,13 +386,14 @@ cudaError_t row_gather_launch(const bf16* s0, const bf16* s1, const bf16* s2, co
                               int nrows, int cols, cudaStream_t s);
 // x[row] += sum_s part[s][row] (split order); out[row] = bf16(rmsnorm(x[row]) * gamma). part plane = rows x H.
 cudaError_t splitk_resid_rmsnorm_launch(const float* part, int splits, int rows, float* x, const bf16* gamma,
-                                        bf16* out, int H, float eps, cudaStream_t s);
+                                        bf16* out, int H, float eps, cudaStream_t s, int sk_L = 0, int sk_kbt = 0);
 // tokens[i] = argmax over the [n][parts] (val, idx) partials; NaN wins, and a NaN row
 // yields ECO_TOKEN_NAN (reading A6) instead of a token id.
 constexpr int ECO_TOKEN_NAN = -2;
 cudaError_t argmax_reduce_launch(const float* val, const int* idx, int n, int parts, int ld, int* tokens,
                                  cudaStream_t s);
-// Decode epilogues (after a split-K swap GEMM): sum partial[split][row][col] in fixed split order, then
+// Decode epilogues (after a split-K swap GEMM): sum partial[split][row][col] in fixed split order
+// (epi.sk_L > 0: the balanced split's sk_slots(col / 128) slots), then
 enum RedMode : int { RED_BF16 = 0, RED_RESID = 1, RED_SILU = 2, RED_QKV = 3, RED_F32 = 4 };
 cudaError_t splitk_reduce_launch(int mode, const float* part, int splits, int rows, int cols, int64_t ld_part,
                                  const GemmEpi& epi, cudaStream_t s);

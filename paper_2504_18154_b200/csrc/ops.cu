@@ -137,6 +137,36 @@ ecoserve_status ecoserve_op_gemm_decode(const void* W, const void* X, int32_t m,
   return ECOSERVE_OK;
 }
 
+ecoserve_status ecoserve_op_gemm_decode_balanced(const void* W, const void* X, int32_t m, int32_t n, int32_t k,
+                                                 int32_t max_slots, float* ws, float* out, int32_t bn,
+                                                 int32_t* chunk, void* stream) {
+  if (!W || !X || !ws || !out || !chunk || m < 1 || n < 1 || k < 1 || k % 8 || m % 4 || max_slots < 1 ||
+      (bn != 64 && bn != 128) || n > bn)
+    return ECOSERVE_ERR_INVALID_ARG;
+  const int kbt = (k + 63) / 64;
+  const int L = gemm_sk_chunk((m + 127) / 128, kbt, num_sms(), max_slots);
+  *chunk = L;
+  if (L <= 0) return ECOSERVE_ERR_INVALID_ARG;
+  CUtensorMap ma, mb;
+  if (make_tmap_bf16(&ma, W, m, k, 128) || make_tmap_bf16(&mb, X, n, k, bn)) return ECOSERVE_ERR_CUDA;
+  GemmEpi e;
+  memset(&e, 0, sizeof(e));
+  e.mode = EPI_SWAP_F32;
+  e.out = ws;
+  e.ldo = m;
+  e.sk_L = L;
+  e.sk_kbt = kbt;
+  OPCK(gemm_launch_r(&ma, &mb, m, n, k, bn, 1, 1, e, num_sms(), (cudaStream_t)stream));
+  GemmEpi red;
+  memset(&red, 0, sizeof(red));
+  red.out = out;
+  red.ldo = m;
+  red.sk_L = L;
+  red.sk_kbt = kbt;
+  OPCK(splitk_reduce_launch(RED_F32, ws, 1, n, m, m, red, (cudaStream_t)stream));
+  return ECOSERVE_OK;
+}
+
 ecoserve_status ecoserve_op_lm_argmax(const void* W, const void* X, int32_t V, int32_t n, int32_t k, float* ws_val,
                                       int32_t* ws_idx, int32_t* tokens, void* stream) {
   if (!W || !X || !ws_val || !ws_idx || !tokens || V < 1 || n < 1 || k < 1 || k % 8) return ECOSERVE_ERR_INVALID_ARG;

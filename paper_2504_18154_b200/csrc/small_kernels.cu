@@ -150,7 +150,7 @@ cudaError_t argmax_reduce_launch(const float* val, const int* idx, int n, int pa
 // One CTA per row; each thread keeps its <= 4 float4 of the row in registers.
 __global__ void __launch_bounds__(1024) splitk_resid_rmsnorm_kernel(const float* __restrict__ part, int splits, int rows,
                                             float* __restrict__ x, const bf16* __restrict__ gamma,
-                                            bf16* __restrict__ out, int H, float eps) {
+                                            bf16* __restrict__ out, int H, float eps, int sk_L, int sk_kbt) {
   pdl_trigger();
   pdl_wait();
   const int row = blockIdx.x;
@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(1024) splitk_resid_rmsnorm_kernel(const float*
     const int c = (threadIdx.x + j * blockDim.x) * 4;
     if (c < H) {
       float4 a = *reinterpret_cast<const float4*>(x + (int64_t)row * H + c);
-      for (int s = 0; s < splits; ++s) {
+      const int ns = sk_L > 0 ? sk_slots(c / 128, sk_kbt, sk_L) : splits;
+      for (int s = 0; s < ns; ++s) {
         const float4 p = *reinterpret_cast<const float4*>(part + s * plane + (int64_t)row * H + c);
         a.x += p.x; a.y += p.y; a.z += p.z; a.w += p.w;
       }
@@ -198,13 +199,13 @@ __global__ void __launch_bounds__(1024) splitk_resid_rmsnorm_kernel(const float*
 }
 
 cudaError_t splitk_resid_rmsnorm_launch(const float* part, int splits, int rows, float* x, const bf16* gamma,
-                                        bf16* out, int H, float eps, cudaStream_t s) {
+                                        bf16* out, int H, float eps, cudaStream_t s, int sk_L, int sk_kbt) {
   if (rows == 0) return cudaSuccess;
   // one float4 per thread up to H = 4096 (more loads in flight: only `rows` CTAs run)
   const int threads = H >= 4096 ? 1024 : (H >= 1024 ? 256 : 64);
   if (H % 4 || H > threads * 16) return cudaErrorInvalidValue;
   return launch_k(splitk_resid_rmsnorm_kernel, dim3(rows), dim3(threads), 0, s, part, splits, rows, x, gamma, out, H,
-                  eps);
+                  eps, sk_L, sk_kbt);
 }
 
 // TP=2 all-reduce fused with the residual add and the next RMSNorm, over NVLink peer
@@ -349,7 +350,8 @@ __global__ void __launch_bounds__(1024) tp_push_rows_kernel(TpRowsArgs a) {
       const int c = (threadIdx.x + j * blockDim.x) * 4;
       if (c < H) {
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int s = 0; s < a.splits; ++s) {
+        const int ns = a.sk_L > 0 ? sk_slots(c / 128, a.sk_kbt, a.sk_L) : a.splits;
+        for (int s = 0; s < ns; ++s) {
           const float4 p = *reinterpret_cast<const float4*>(a.part + s * a.plane + (int64_t)row * a.ldp + c);
           acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
         }
@@ -434,7 +436,8 @@ __global__ void splitk_reduce_kernel(int mode, const float* __restrict__ part, i
   const int row = gid / pairs, c = 2 * (int)(gid % pairs);
   float a = 0.f, b = 0.f;
   const int64_t plane = (int64_t)rows * ld_part;
-  for (int s = 0; s < splits; ++s) {  // fixed order: deterministic
+  const int ns = e.sk_L > 0 ? sk_slots(c / 128, e.sk_kbt, e.sk_L) : splits;
+  for (int s = 0; s < ns; ++s) {  // fixed order: deterministic
     const float2 v = *reinterpret_cast<const float2*>(part + s * plane + (int64_t)row * ld_part + c);
     a += v.x;
     b += v.y;

@@ -58,6 +58,20 @@ def gemm_decode(W: torch.Tensor, X: torch.Tensor, r: int = 2, splits: int = 1, b
     return out
 
 
+def gemm_decode_balanced(W: torch.Tensor, X: torch.Tensor, max_slots: int = 8, bn: int = 128):
+    """out f32 [n][m] = X W^T with the balanced split-K (equal K-block chunks per CTA);
+    returns (out, chunk length)."""
+    import ctypes
+    m, k = W.shape
+    n = X.shape[0]
+    ws = torch.empty(max_slots, n, m, dtype=torch.float32, device=W.device)
+    out = torch.empty(n, m, dtype=torch.float32, device=W.device)
+    chunk = ctypes.c_int32(0)
+    L.check(L.load().ecoserve_op_gemm_decode_balanced(W.data_ptr(), X.data_ptr(), m, n, k, max_slots, ws.data_ptr(),
+                                                      out.data_ptr(), bn, ctypes.byref(chunk), _s()))
+    return out, chunk.value
+
+
 def gemm_cluster(W: torch.Tensor, X: torch.Tensor, splits: int, bn: int = 128) -> torch.Tensor:
     """out f32 [n][m] = X W^T, K split over a thread-block cluster, reduced in DSMEM."""
     m, k = W.shape

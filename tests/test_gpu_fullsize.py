@@ -146,14 +146,15 @@ def test_fullwidth_70b_tp2():
 
 
 @pytest.mark.parametrize("env", ["ECOSERVE_GU_SK=1", "ECOSERVE_FLOW=1", "ECOSERVE_ATTN_SK=1", "ECOSERVE_GU_WAVES=1",
-                                 "ECOSERVE_QKV_FUSE=1", "ECOSERVE_ATTN_T128=1"])
+                                 "ECOSERVE_QKV_FUSE=1", "ECOSERVE_ATTN_T128=1", "ECOSERVE_DEC_SK=1"])
 def test_fullwidth_decode_variants(env):
     """Every decode variant switch at full 8B / 34B widths and bench-like batches, against
     the same oracle bars (fresh process: the switches are read once). GU_SK: stream-K
     gate/up (224 / 344 tiles balanced, two-way tile sums); FLOW: the O -> gate/up -> down
     dataflow kernel; ATTN_SK: persistent stream-K decode attention; GU_WAVES: gate/up
     in two waves, the second beside the down GEMM's first K part; QKV_FUSE:
-    the QKV reduction in the attention prologue."""
+    the QKV reduction in the attention prologue; DEC_SK: balanced split-K for the split
+    decode projections."""
     import os
     import subprocess
     import sys

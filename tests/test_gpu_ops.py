@@ -84,6 +84,25 @@ def test_gemm_decode_dual_tile(ops, m, n, k, r, splits, bn):
     assert rel_err(got, x @ w.T) < 1e-5
 
 
+@pytest.mark.parametrize("m,n,k,bn", [(4096, 128, 14336, 128), (4096, 128, 4096, 128), (6144, 128, 4096, 128),
+                                      (8192, 128, 4096, 128), (8192, 128, 14336, 128), (5120, 100, 8192, 128),
+                                      (1000, 37, 4104, 64), (256, 3, 192, 64), (512, 64, 768, 64)])
+def test_gemm_decode_balanced(ops, m, n, k, bn):
+    """Balanced split-K (equal K-block chunks per CTA, per-tile partial slots summed in K
+    order) == X W^T; deterministic; every chunk length leaves <= 8 slots per tile."""
+    rng = np.random.default_rng(m + 3 * n + k)
+    w, W = bf16_rand(rng, (m, k), 1.0 / np.sqrt(k))
+    x, X = bf16_rand(rng, (n, k))
+    got, L = ops.gemm_decode_balanced(W, X, 8, bn)
+    got = got.cpu().numpy()
+    assert L > 0
+    kbt, tiles = (k + 63) // 64, (m + 127) // 128
+    assert tiles * kbt <= L * torch.cuda.get_device_properties(0).multi_processor_count
+    assert rel_err(got, x @ w.T) < 1e-5
+    again, _ = ops.gemm_decode_balanced(W, X, 8, bn)
+    assert np.array_equal(got, again.cpu().numpy())
+
+
 @pytest.mark.parametrize("m,n,k,splits,bn", [(640, 37, 1024, 2, 64), (640, 37, 1024, 3, 128), (6144, 128, 4096, 3, 128),
                                              (4096, 128, 4096, 4, 128), (4096, 200, 14336, 4, 128), (300, 5, 192, 3, 64),
                                              (256, 64, 256, 4, 64)])

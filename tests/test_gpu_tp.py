@@ -40,15 +40,17 @@ def _worker(rank, nccl_id, q):
         q.put((rank, None, None, None, repr(e)))
 
 
-@pytest.mark.parametrize("fused", ["1", "0", "push"])
+@pytest.mark.parametrize("fused", ["1", "0", "push", "sk"])
 def test_tp2_pair_matches_oracle(fused, monkeypatch):
     """fused=1: all-reduce + residual + RMSNorm over NVLink peer memory (N2; prefill
     tiles pushed from the GEMM epilogue, decode rows pushed by the reduction kernel);
     push: the decode GEMM epilogue also pushes its split partials (opt-in);
+    sk: balanced split-K decode partials (per-tile slot counts in the row push);
     fused=0: NCCL all-reduce + separate RMSNorm."""
     # inherited by the spawned ranks
     monkeypatch.setenv("ECOSERVE_TP_FUSED", "0" if fused == "0" else "1")
     monkeypatch.setenv("ECOSERVE_TP_DECODE_PUSH", "1" if fused == "push" else "0")
+    monkeypatch.setenv("ECOSERVE_DEC_SK", "1" if fused == "sk" else "0")
     if torch.cuda.device_count() < 2:
         pytest.skip("TP=2 needs 2 GPUs (gpurun --gpus 2)")
     from oracle import transformer as T
