@@ -183,7 +183,10 @@ def load(path: str = LIB_PATH) -> C.CDLL:
             raise ImportError(f"{path} is missing: run `python -m paper_2504_18154_b200.build` "
                               "(the hot path has no CPU fallback)")
         lib = C.CDLL(path)
+        ab = "ECOSERVE_LIB_AB" in os.environ
         for name, (res, args) in SIGNATURES.items():
+            if ab and not hasattr(lib, name):
+                continue  # an older build under A/B timing may lack newer entry points
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(DecodeAttnArgs a, cons
 }
 
 // ------------------------------------------------------------------ decode, stream-K
-// Persistent variant of the TMA decode kernel (head_dim 128, G <= 4 q heads per kv head).
+// Persistent variant of the TMA decode kernel (head_dim 128, G <= 8 q heads per kv head).
 // tools/attn_decode_probe.py: at B = 128 the per-item kernel pays ~37 us per launch on
 // top of streaming (ctx 1300: 129.5 us; ctx 2600: 222.3 us, i.e. 7.4 TB/s marginal) --
 // each CTA's start-up round trips and the last partial wave (1024 CTAs = 3.46 waves of
@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(128) attn_decode_sk_kernel(DecodeAttnArgs a, c
     float o[ND][4];
 #pragma unroll
     for (int i = 0; i < ND; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-    float mrow = -INFINITY, lrow = 0.f;  // row g (rows g + 8 are padding: G <= 4)
+    float mrow = -INFINITY, lrow = 0.f;  // row g (rows g + 8 are padding: G <= 8)
     for (int blk = blk0; blk < blk1; ++blk) {
       const int j = j0 + (blk - blk0);
       if (tid == 0 && j + DEC_STAGES - 1 < n_units) {
@@ -714,22 +714,11 @@ __global__ void __launch_bounds__(128) attn_decode_sk_kernel(DecodeAttnArgs a, c
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
-    // ---- the part's (m, l, o) over its blocks: warps combined in fixed order
+    // ---- the part's (m, l, o) over its blocks: warps combined in fixed order, GMAX rows
+    //      of red at a time (G = 8: two rounds)
     lrow += __shfl_xor_sync(0xffffffffu, lrow, 1);
     lrow += __shfl_xor_sync(0xffffffffu, lrow, 2);
     float* myred = red + warp * GMAX * RS;
-    if (g < G) {
-#pragma unroll
-      for (int i = 0; i < ND; ++i) {
-        myred[g * RS + i * 8 + 2 * t4] = o[i][0];
-        myred[g * RS + i * 8 + 2 * t4 + 1] = o[i][1];
-      }
-      if (t4 == 0) {
-        myred[g * RS + D] = mrow;
-        myred[g * RS + D + 1] = lrow;
-      }
-    }
-    __syncthreads();
     const bool whole = blk0 == 0 && blk1 == nb;
     const int item = r * a.n_kv + kvh;
     // part index within the item: CTAs from the owner of the item's first unit
@@ -737,25 +726,42 @@ __global__ void __launch_bounds__(128) attn_decode_sk_kernel(DecodeAttnArgs a, c
     const int c_lo = (int)(((long long)(iu0 + 1) * Ctot - 1) / U);
     const int c_hi = (int)(((long long)(iu0 + nb) * Ctot - 1) / U);
     const int pidx = c - c_lo, nparts = c_hi - c_lo + 1;
-    for (int i = tid; i < G * D; i += 128) {
-      const int row = i / D, dd = i % D;
-      float M = -INFINITY;
-      for (int w = 0; w < 4; ++w) M = fmaxf(M, red[(w * GMAX + row) * RS + D]);
-      float acc = 0.f, l = 0.f;
-      for (int w = 0; w < 4; ++w) {
-        const float mw = red[(w * GMAX + row) * RS + D];
-        const float f = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
-        acc += f * red[(w * GMAX + row) * RS + dd];
-        l += f * red[(w * GMAX + row) * RS + D + 1];
+    for (int rb = 0; rb < G; rb += GMAX) {
+      const int nr = min(GMAX, G - rb);
+      if (rb > 0) __syncthreads();  // previous round's reads of red are done
+      if (g >= rb && g < rb + nr) {
+        const int gr = g - rb;
+#pragma unroll
+        for (int i = 0; i < ND; ++i) {
+          myred[gr * RS + i * 8 + 2 * t4] = o[i][0];
+          myred[gr * RS + i * 8 + 2 * t4 + 1] = o[i][1];
+        }
+        if (t4 == 0) {
+          myred[gr * RS + D] = mrow;
+          myred[gr * RS + D + 1] = lrow;
+        }
       }
-      if (whole) {
-        a.out[(int64_t)seq * a.n_heads * D + (kvh * G + row) * D + dd] = __float2bfloat16_rn(acc / l);
-      } else {
-        const int64_t pi = (int64_t)item * a.sk_maxp + pidx;
-        part_w[(pi * G + row) * D + dd] = acc;
-        if (dd == 0) {
-          part_ml[(pi * G + row) * 2] = M;
-          part_ml[(pi * G + row) * 2 + 1] = l;
+      __syncthreads();
+      for (int i = tid; i < nr * D; i += 128) {
+        const int rr = i / D, row = rb + rr, dd = i % D;
+        float M = -INFINITY;
+        for (int w = 0; w < 4; ++w) M = fmaxf(M, red[(w * GMAX + rr) * RS + D]);
+        float acc = 0.f, l = 0.f;
+        for (int w = 0; w < 4; ++w) {
+          const float mw = red[(w * GMAX + rr) * RS + D];
+          const float f = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
+          acc += f * red[(w * GMAX + rr) * RS + dd];
+          l += f * red[(w * GMAX + rr) * RS + D + 1];
+        }
+        if (whole) {
+          a.out[(int64_t)seq * a.n_heads * D + (kvh * G + row) * D + dd] = __float2bfloat16_rn(acc / l);
+        } else {
+          const int64_t pi = (int64_t)item * a.sk_maxp + pidx;
+          part_w[(pi * G + row) * D + dd] = acc;
+          if (dd == 0) {
+            part_ml[(pi * G + row) * 2] = M;
+            part_ml[(pi * G + row) * 2 + 1] = l;
+          }
         }
       }
     }
@@ -803,7 +809,7 @@ int attn_decode_sk_grid(int total_units, int max_item_blocks, int min_item_block
     const char* e = getenv("ECOSERVE_ATTN_SK");
     mode = (e && e[0] == '1') ? 1 : 0;
   }
-  if (!(mode || force) || head_dim != 128 || n_heads / n_kv > 4) return 0;
+  if (!(mode || force) || head_dim != 128 || n_heads / n_kv > 8) return 0;
   const int grid = 2 * num_sms;
   if (total_units < 4 * grid) return 0;  // (short work: the per-item kernel)
   const int per = total_units / grid;    // units per CTA (floor)

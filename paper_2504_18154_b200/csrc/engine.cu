@@ -2449,7 +2449,7 @@ ecoserve_status ecoserve_decode_phase(ecoserve_instance* inst, const int64_t* re
         max_nb = std::max(max_nb, nb);
         min_nb = std::min(min_nb, nb);
       }
-      if (inst->attn_tc && inst->tp == 1)
+      if (inst->attn_tc)
         sk.grid = attn_decode_sk_grid(skp[B] * inst->Mkv, max_nb, min_nb, inst->M, inst->Mkv, inst->D, inst->num_sms,
                                       &sk.maxp);
     }

@@ -306,11 +306,14 @@ def test_attention_decode(ops, D, M, Mkv, splits, bps, tma):
         assert rel_err(got[i], ref) < 1e-2, (i, c)
 
 
-@pytest.mark.parametrize("M,Mkv,ctx_kind", [(32, 8, "mixed"), (32, 8, "one_long"), (16, 8, "mixed"), (8, 8, "uniform")])
+@pytest.mark.parametrize("M,Mkv,ctx_kind", [(32, 8, "mixed"), (32, 8, "one_long"), (16, 8, "mixed"), (8, 8, "uniform"),
+                                             (32, 4, "mixed"), (32, 4, "one_long"), (24, 4, "uniform")])
 def test_attention_decode_stream_k(ops, M, Mkv, ctx_kind):
     """Persistent stream-K decode attention (the engine's default for large decode steps):
     items cut between CTAs -- including one 8k-token sequence spread over several CTAs --
-    combined by their last contributor; every output row against the fp64 definition."""
+    combined by their last contributor; every output row against the fp64 definition.
+    G = 8 (the 70B rank shard: 32 q heads on 4 kv heads) and G = 6 combine their rows in
+    two rounds of the 4-row reduction buffer."""
     D = 128
     rng = np.random.default_rng(M + Mkv + len(ctx_kind))
     if ctx_kind == "mixed":
