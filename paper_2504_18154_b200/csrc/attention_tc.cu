@@ -700,13 +700,18 @@ void attn_tc_set_trace(long long* trace, int trace_tile) {
 cudaError_t attn_prefill_tc_launch(const CUtensorMap* qmap, const CUtensorMap* kvmap, const int* cu_seqlens,
                                    const int* block_tables, int bt_ld, const int* tiles, int n_tiles, bf16* out,
                                    int n_heads, int n_kv, int layer, int n_layers, cudaStream_t s,
-                                   const int* ctx_off) {
+                                   const int* ctx_off, int mean_keys) {
   if (n_kv < 1 || n_heads % n_kv) return cudaErrorInvalidValue;
-  static const int t128_mode = [] {
+  // ECOSERVE_ATTN_T128 = 0 / 1 / 2 forces the choice; unset: the 128-key kernel when the
+  // batch's queries attend >= 2048 keys on average (prompts of ~4k tokens and more). Measured
+  // (profiles/r02_attn_prefill_t128_ab.log): 1 x 8k 616 vs 702 us, 4 x 2k equal (mean 1024
+  // keys), 8 x U{512..2048} 176.6 vs 170.0 us (mean ~720 keys), 16 x 512 113.8 vs 92.2 us.
+  static const int t128_env = [] {
     const char* ev = getenv("ECOSERVE_ATTN_T128");
-    return ev ? atoi(ev) : 0;
+    return ev ? atoi(ev) : -1;
   }();
-  if (t128_mode) {  // opt-in 128-key kernel; 2 = with the poly-exp2 offload
+  const int t128_mode = t128_env >= 0 ? t128_env : (mean_keys >= 2048 ? 1 : 0);
+  if (t128_mode) {  // 128-key kernel; 2 = with the poly-exp2 offload
     auto k = t128_mode == 2 ? attn_prefill_t128_kernel<1> : attn_prefill_t128_kernel<0>;
     cudaError_t e = ensure_smem(k, t128::SMEM);
     if (e != cudaSuccess || n_tiles == 0) return e;

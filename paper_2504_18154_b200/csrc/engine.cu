@@ -854,9 +854,19 @@ struct LayerIO {
   const int* slot;   // device
 };
 
+static bool epi_bulk_enabled() {  // ECOSERVE_EPI_BULK=1: GemmEpi::bulk_copy
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_EPI_BULK");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 GemmEpi epi_base(ecoserve_instance* inst) {
   GemmEpi e;
   memset(&e, 0, sizeof(e));
+  e.bulk_copy = epi_bulk_enabled() ? 1 : 0;
   e.rope_cos = inst->rope_cos;
   e.rope_sin = inst->rope_sin;
   e.indep = 2;  // prefill: the weights are the B operand
@@ -1467,7 +1477,8 @@ static ecoserve_status run_layers_prefill(ecoserve_instance* inst, int T, const 
       if (inst->attn_tc)
         LAUNCH(P_ATTN_PREFILL, attn_flop, 1,
                attn_prefill_tc_launch(&inst->attn_qmap, &inst->attn_kvmap, d_cu, d_bt, bt_ld, d_tiles, n_tiles,
-                                      inst->ao, M, inst->Mkv, l, inst->L, st, a.ctx_off));
+                                      inst->ao, M, inst->Mkv, l, inst->L, st, a.ctx_off,
+                                      (int)(attn_flop / (4.0 * M * D * std::max(1, T)))));
       else
         LAUNCH(P_ATTN_PREFILL, attn_flop, 1, attn_prefill_launch(a, D, st));
     }

@@ -410,6 +410,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       C::BULK_EPI && (reinterpret_cast<uintptr_t>(epi.out) & 15) == 0 &&
       ((epi.mode == EPI_SWAP_F32 && m_rows % 4 == 0 && epi.ldo % 4 == 0) ||
        (epi.mode == EPI_SWAP_SILU && splits == 1 && m_rows % 16 == 0 && epi.ldo % 8 == 0));
+  // ... whose staged token rows leave by async bulk copies (one per row, issued by one
+  // thread each) instead of 16-byte st.global from 4 warps (epi.bulk_copy): the per-CTA
+  // trace measured that copy-out at ~4700 cycles of the ~3.4 us epilogue tail
+  // (profiles/r01_gemm_trace_epi.log), but the decode step got slower with it
+  // (8B 7.95-8.02 vs 7.86-7.89 ms, profiles/r02_epi_bulk_copy_ab.jsonl)
+  const bool bulk_copy = bulk_epi && !epi.out2 && epi.bulk_copy;
 
   if (threadIdx.x == 0) {
     trace_mark(epi, 0);  // CTA start
@@ -755,6 +761,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const uint32_t stg_base = smem_u32(staging);
           for (int h = 0; h < 2; ++h) {
             c0_ = clk();
+            if (bulk_copy) bulk_wait_read0();  // this thread's row copies have read the staging
             asm volatile("bar.sync 1, 128;" ::: "memory");  // staging free (previous copy-out done)
             c_wr += clk() - c0_;
 #pragma unroll 1
@@ -793,9 +800,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               __syncwarp();
               if (lane == 0) mbar_arrive(&tempty_bar[acc]);
             }
+            if (bulk_copy) fence_proxy_async();  // this thread's st.shared -> the bulk copies
             asm volatile("bar.sync 1, 128;" ::: "memory");  // staging complete
             const int n0 = nt * BN + h * HALF;
             const int rows = max(0, min(HALF, n_rows - n0));
+            if (bulk_copy) {
+              if (ep_tid < rows && vec_per_row > 0) {
+                bulk_store(gbase + (int64_t)(n0 + ep_tid) * gstride, staging + ep_tid * stg_row, vec_per_row * 16);
+                bulk_commit();
+              }
+            } else
             for (int idx = ep_tid; idx < rows * vec_per_row; idx += 128) {
               const int r = idx / vec_per_row, c = idx % vec_per_row;
               const uint4 val = lds128(stg_base + (uint32_t)(r * stg_row + c * 16));
@@ -805,6 +819,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             c_out += clk() - c0_;
           }
         }
+        if (bulk_copy) bulk_wait_read0();  // (the staging is reused by the next unit / freed at exit)
         if (threadIdx.x == 64) {
           trace_put(epi, 8, c_wr);
           trace_put(epi, 9, c_ld);

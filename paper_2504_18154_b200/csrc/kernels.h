@@ -106,6 +106,10 @@ struct GemmEpi {
   // busy). Its piece of tile t goes to partial slot c - (t * sk_kbt) / sk_L; tile t has
   // sk_slots(t) slots, summed in slot (= K) order by the reductions.
   int sk_L, sk_kbt;
+  // bulk-store epilogues: 1 = copy the staged token rows out with one async bulk copy per
+  // row (cp.async.bulk) instead of 16-byte st.global from the 4 epilogue warps
+  // (ECOSERVE_EPI_BULK=1; measured slower in the decode step, so off by default)
+  int bulk_copy;
 };
 
 // Partial slots of weight tile `tile` under the balanced split (see GemmEpi::sk_L).
@@ -234,7 +238,9 @@ void attn_tc_set_trace(long long* trace, int trace_tile);
 cudaError_t attn_prefill_tc_launch(const CUtensorMap* qmap, const CUtensorMap* kvmap, const int* cu_seqlens,
                                    const int* block_tables, int bt_ld, const int* tiles, int n_tiles, bf16* out,
                                    int n_heads, int n_kv, int layer, int n_layers, cudaStream_t s,
-                                   const int* ctx_off = nullptr);
+                                   const int* ctx_off = nullptr, int mean_keys = 0);
+// (mean_keys: keys attended per query token, averaged over the batch -- selects the
+// 128-key kernel for long prompts unless ECOSERVE_ATTN_T128 forces a choice)
 
 // Decode split-K paged attention + combine.
 struct DecodeAttnArgs {

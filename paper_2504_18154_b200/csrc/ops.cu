@@ -249,12 +249,15 @@ ecoserve_status ecoserve_op_attention_prefill_tc(const void* q, const void* pool
   if (!q || !pool || !cu_seqlens_host || !block_tables || !out || n_seq < 1 || n_heads % n_kv || num_blocks < 1)
     return ECOSERVE_ERR_INVALID_ARG;
   std::vector<int> tiles;
+  double keys = 0;  // keys attended, summed over the queries (the engine's kernel choice)
   for (int s = 0; s < n_seq; ++s) {
     const int len = cu_seqlens_host[s + 1] - cu_seqlens_host[s];
     const int off = ctx_off_host ? ctx_off_host[s] : 0;
     if (len < 1 || off < 0 || (off + len + 63) / 64 > bt_ld) return ECOSERVE_ERR_INVALID_ARG;
     for (int qs = 0; qs < len; qs += 128) { tiles.push_back(s); tiles.push_back(qs); }
+    keys += (double)len * off + 0.5 * len * (len + 1.0);
   }
+  const int mean_keys = (int)(keys / std::max(1, cu_seqlens_host[n_seq]));
   CUtensorMap qm, km;
   if (make_attn_tc_maps(&qm, &km, q, cu_seqlens_host[n_seq], n_heads, pool, num_blocks * 2 * n_kv * 64))
     return ECOSERVE_ERR_CUDA;
@@ -269,7 +272,7 @@ ecoserve_status ecoserve_op_attention_prefill_tc(const void* q, const void* pool
   OPCK(oe);
   const cudaError_t e = attn_prefill_tc_launch(&qm, &km, d, block_tables, bt_ld, d + n_seq + 1,
                                                (int)tiles.size() / 2, (bf16*)out, n_heads, n_kv, 0, 1,
-                                               (cudaStream_t)stream, d_off);
+                                               (cudaStream_t)stream, d_off, mean_keys);
   cudaFreeAsync(d, (cudaStream_t)stream);
   return e == cudaSuccess ? ECOSERVE_OK : ECOSERVE_ERR_CUDA;
 }

@@ -201,8 +201,10 @@ def test_attention_prefill(ops, D, M, Mkv):
 
 
 @pytest.mark.parametrize("M,Mkv,lens", [(8, 2, [1, 63, 64, 65, 200, 130]), (32, 8, [128, 129, 255, 256, 520, 7]),
-                                         (4, 4, [1000, 3])])
+                                         (4, 4, [1000, 3]), (8, 2, [4500, 70]), (4, 1, [8192])])
 def test_attention_prefill_tcgen05(ops, M, Mkv, lens):
+    """The default choice: batches whose queries attend >= 2048 keys on average (the
+    4500 / 8192-token cases) run the 128-key kernel, the others the 2-head kernel."""
     D = 128
     rng = np.random.default_rng(M + len(lens))
     nb = [(s + 63) // 64 for s in lens]
