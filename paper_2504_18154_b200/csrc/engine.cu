@@ -1151,6 +1151,15 @@ unsigned long long* gu_trace_buf(ecoserve_instance* inst) {
   return inst->gu_trace;
 }
 
+bool qkv_inkernel_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ECOSERVE_QKV_INKERNEL");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 // ECOSERVE_DEC_SK=1: the split decode projections (O, down, QKV when their weight tiles
 // are fewer than the SMs) use the balanced split (GemmEpi::sk_L) instead of a uniform one
 bool dec_sk_enabled() {
@@ -1229,6 +1238,15 @@ cudaError_t decode_gemm(ecoserve_instance* inst, const CUtensorMap& wmap, const 
       *nk = 1;
       return gemm_cluster_launch(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, sc, e, inst->stream);
     }
+  }
+  // ECOSERVE_QKV_INKERNEL=1: the QKV split reduction (+ RoPE, K/V append) by the last CTA
+  // of each weight tile inside the GEMM (GemmEpi::part / counters) instead of a reduction kernel
+  if (mode == EPI_SWAP_QKV && qkv_inkernel_enabled() && var == 1 && !r2 && (B + bn - 1) / bn == 1) {
+    e.mode = mode;
+    e.part = inst->part;
+    e.counters = inst->counters;
+    *nk = 1;
+    return gemm_launch_r(&wmap, &xm.b[bn_index(bn)], n_out, B, K, bn, 1, splits, e, inst->num_sms, inst->stream);
   }
   // split-K: f32 partials, then one fixed-order reduction kernel applying the epilogue
   GemmEpi ge = e;

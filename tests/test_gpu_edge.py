@@ -75,7 +75,7 @@ def test_decode_batch_sizes(setup, B):
 @pytest.mark.parametrize("env", ["ECOSERVE_FLOW=1", "ECOSERVE_QKV_FUSE=1", "ECOSERVE_GU_SK=1", "ECOSERVE_ATTN_SK=1",
                                  "ECOSERVE_CHAIN=1", "ECOSERVE_DEC_VARIANT=4", "ECOSERVE_PAIR_TILES=1", "ECOSERVE_DEC_R2=1",
                                  "ECOSERVE_ATTN_STAGES=2", "ECOSERVE_PDL=0", "ECOSERVE_DEC_SK=1",
-                                 "ECOSERVE_EPI_BULK=1"])
+                                 "ECOSERVE_EPI_BULK=1", "ECOSERVE_QKV_INKERNEL=1"])
 @pytest.mark.parametrize("shape", ["tiny", "tiny-d128"])
 def test_opt_in_decode_variants_match_oracle(env, shape):
     """The opt-in decode variants (ECOSERVE_FLOW=1 is the decode
