@@ -809,12 +809,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 bulk_store(gbase + (int64_t)(n0 + ep_tid) * gstride, staging + ep_tid * stg_row, vec_per_row * 16);
                 bulk_commit();
               }
-            } else
-            for (int idx = ep_tid; idx < rows * vec_per_row; idx += 128) {
-              const int r = idx / vec_per_row, c = idx % vec_per_row;
-              const uint4 val = lds128(stg_base + (uint32_t)(r * stg_row + c * 16));
-              *reinterpret_cast<uint4*>(gbase + (int64_t)(n0 + r) * gstride + c * 16) = val;
-              if (gbase2) *reinterpret_cast<uint4*>(gbase2 + (int64_t)(n0 + r) * gstride + c * 16) = val;
+            } else {
+              for (int idx = ep_tid; idx < rows * vec_per_row; idx += 128) {
+                const int r = idx / vec_per_row, c = idx % vec_per_row;
+                const uint4 val = lds128(stg_base + (uint32_t)(r * stg_row + c * 16));
+                *reinterpret_cast<uint4*>(gbase + (int64_t)(n0 + r) * gstride + c * 16) = val;
+                if (gbase2) *reinterpret_cast<uint4*>(gbase2 + (int64_t)(n0 + r) * gstride + c * 16) = val;
+              }
             }
             c_out += clk() - c0_;
           }
