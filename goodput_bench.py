@@ -54,6 +54,8 @@ def main():
                          "decode-only instances with the KV moved over NVLink")
     ap.add_argument("--fudg-prefill", type=int, default=0, help="fudg: prefill instances (default half)")
     ap.add_argument("--chunk-budget", type=int, default=1024, help="sarathi: tokens per hybrid iteration")
+    ap.add_argument("--tp", type=int, choices=(1, 2), default=1,
+                    help="2: every instance is a TP=2 pair of GPUs (configs[3], e.g. --shape 70b), padg only")
     args = ap.parse_args()
 
     import torch
@@ -69,7 +71,30 @@ def main():
     shape = get_shape(args.shape)
     n_gpu = min(args.gpus, torch.cuda.device_count())
     insts = []
-    for g in range(n_gpu):
+    if args.tp == 2:
+        import dataclasses
+
+        from paper_2504_18154_b200.instance import TpPairInstance
+        assert args.policy == "padg" and n_gpu >= 2
+        n_gpu -= n_gpu % 2
+        local = dataclasses.replace(shape, n_heads=shape.n_heads // 2, n_kv_heads=shape.n_kv_heads // 2,
+                                    ffn_dim=shape.ffn_dim // 2, tp_size=1)
+        for g in range(0, n_gpu, 2):
+            ws = []
+            for r in range(2):
+                dev = torch.device("cuda", g + r)
+                torch.cuda.set_device(dev)
+                w = random_device_weights(local, seed=100 + g + r, device=dev)
+                gen = torch.Generator(device=dev)  # replicated tensors: identical on both ranks
+                gen.manual_seed(4321 + g)
+                for k in ("embed", "lm_head"):
+                    w[k] = (torch.randn(w[k].shape, generator=gen, device=dev) * 0.02).to(torch.bfloat16)
+                w["final_norm"] = torch.ones_like(w["final_norm"])
+                ws.append(w)
+            insts.append(TpPairInstance(dataclasses.replace(shape, tp_size=2), ws, args.blocks, (g, g + 1),
+                                        token_budget=16384, max_batch=512, max_positions=8192 + args.max_out,
+                                        free_raw_after_create=True))
+    for g in range(n_gpu if args.tp == 1 else 0):
         dev = torch.device("cuda", g)
         torch.cuda.set_device(dev)
         w = random_device_weights(shape, seed=100 + g, device=dev)
@@ -118,7 +143,7 @@ def main():
     else:
         gp = MX.bisect_goodput(attain_at, args.p, args.lo, args.hi, args.iters)
     line = {"metric": "goodput req/s at TTFT/TPOT SLO", "value": gp, "unit": "req/s", "n_gpus": n_gpu,
-            "instances": len(insts), "p": args.p, "slo": {"ttft_s": args.slo_ttft, "tpot_s": args.slo_tpot},
+            "instances": len(insts), "tp": args.tp, "p": args.p, "slo": {"ttft_s": args.slo_ttft, "tpot_s": args.slo_tpot},
             "config": {"workload": f"{args.preset} Poisson, max({args.n_req}, rate x {args.duration:g} s) req/probe, "
                                    f"outputs <= {args.max_out}",
                        "shape": args.shape,

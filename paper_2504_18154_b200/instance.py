@@ -251,3 +251,57 @@ class Instance:
         out = np.zeros((rows, self.shape.hidden), dtype=np.float32)
         L.check(self.lib.ecoserve_debug_hidden(self.h, int(req_id), layer, out.ctypes.data_as(L.PF32)), self.h)
         return out
+
+
+class TpPairInstance:
+    """One TP=2 instance of a macro instance (configs[3]: Llama-2-70B, TP=2 per
+    instance): rank 0 on GPU `devices[0]`, rank 1 on
+    `devices[1]`, both in this process. Every phase call runs on the two ranks
+    concurrently (one thread each; the ctypes calls release the GIL) and the ranks
+    meet in their fused all-reduce on the device, so the pair is driven like one
+    instance by a serving worker. The ranks compute bitwise-identical tokens
+    (tests/test_gpu_tp.py); rank 0's are returned. weights[r]: rank r's shard
+    (shard_weights); the replicated tensors must be identical on both ranks."""
+
+    def __init__(self, shape, weights: Sequence[Dict], num_blocks: int, devices: Sequence[int] = (0, 1), **kw):
+        from concurrent.futures import ThreadPoolExecutor
+        if len(devices) != 2 or len(weights) != 2:
+            raise ValueError("a TP pair needs two devices and two weight shards")
+        self._ex = ThreadPoolExecutor(2)
+        nid = nccl_unique_id()
+        futs = [self._ex.submit(Instance, shape, weights[r], num_blocks, devices[r], tp_size=2, tp_rank=r,
+                                nccl_id=nid, **kw) for r in range(2)]
+        self.ranks = [f.result() for f in futs]
+        self.shape = shape
+        self.device = self.ranks[0].device
+        self.num_blocks = num_blocks
+
+    def _both(self, name: str, *args):
+        futs = [self._ex.submit(getattr(inst, name), *args) for inst in self.ranks]
+        res = [f.result() for f in futs]  # re-raises a rank's EcoError
+        return res[0]
+
+    def prefill(self, reqs):
+        return self._both("prefill", reqs)
+
+    def decode(self, req_ids, steps: int):
+        return self._both("decode", req_ids, steps)
+
+    def release(self, req_ids) -> None:
+        self._both("release", req_ids)
+
+    def status(self, cap: int = 4096):
+        return self.ranks[0].status(cap)
+
+    def set_profiling(self, level: int) -> None:
+        self._both("set_profiling", level)
+
+    def timing(self, reset: bool = False) -> Dict:
+        return self._both("timing", reset)
+
+    def close(self):
+        for inst in getattr(self, "ranks", []):
+            inst.close()
+        if getattr(self, "_ex", None):
+            self._ex.shutdown(wait=True)
+            self._ex = None

@@ -162,7 +162,10 @@ def test_fullwidth_decode_variants(env):
     k, v = env.split("=")
     if os.environ.get(k) == v:
         pytest.skip(f"already running with {env}")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.abspath(__file__), "-k",
-                        "single_gpu or sampled"], env={**os.environ, k: v}, cwd=root,
+    # the 8B-width prefill + decode test and the B = 128 decode batch (the 34B-width and
+    # B = 100 cases run once, in the default configuration)
+    f = os.path.abspath(__file__)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", f + "::test_fullwidth_single_gpu[8b-L2]",
+                        f + "::test_fullwidth_decode_batch_sampled[128]"], env={**os.environ, k: v}, cwd=root,
                        capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

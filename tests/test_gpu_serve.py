@@ -107,3 +107,43 @@ def test_preempt_admission_on_gpu_matches_oracle():
             checked += 1
     assert checked >= 0.5 * sum(r.G for r in out.values())
     inst.close()
+
+
+def test_live_macro_of_tp2_pairs_matches_oracle():
+    """configs[3] in miniature: a macro instance whose instances are TP=2 pairs
+    (TpPairInstance: rank 0 / rank 1 on two GPUs, both driven from one worker; the
+    ranks meet in the fused all-reduce). Two pairs on 4 GPUs (one pair on 2): every
+    request completes and the served greedy tokens equal the fp64 oracle's (TP=1
+    definition, C4) wherever its top-2 margin is decisive (A20)."""
+    from paper_2504_18154_b200.instance import TpPairInstance, device_weights_from_host, shard_weights
+    from paper_2504_18154_b200.serve import PaDGServer
+    import dataclasses
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("TP=2 pairs need 2 GPUs (gpurun --gpus 2)")
+    shape = dataclasses.replace(get_shape("tiny"), tp_size=2)
+    w = make_weights(get_shape("tiny"), seed=0)
+    insts = []
+    for g in range(0, n - n % 2, 2)[:2]:
+        ws = [shard_weights(device_weights_from_host(w, f"cuda:{g + r}"), shape, 2, r) for r in range(2)]
+        insts.append(TpPairInstance(shape, ws, 256, (g, g + 1), token_budget=2048, max_batch=64,
+                                    max_positions=2048))
+    trace = make_trace("tiny", 16, seed=13, rate_per_s=200.0, vocab=shape.vocab)
+    srv = PaDGServer(insts, slo_ttft_ns=10 ** 10, slo_tpot_ns=10 ** 9, reserve_tokens=16, token_budget=2048)
+    out = srv.run(trace, timeout_s=300)
+    assert all(r.t_done_ns >= 0 and len(r.tokens) == r.G for r in out.values())
+    for i in insts:
+        _, rs = i.status()
+        assert not rs, "every request released"
+    model = T.Model(get_shape("tiny"), w.as_f64())
+    checked = 0
+    for r in list(out.values())[:6]:
+        toks, outs = model.generate(list(r.prompt), r.G)
+        for k in range(r.G):
+            if r.tokens[k] != toks[k]:
+                assert T.top2_margin(outs[k].logits) <= 5e-2
+                break
+            checked += 1
+    assert checked >= 0.6 * 6 * 16
+    for i in insts:
+        i.close()
