@@ -117,6 +117,13 @@ class Worker(threading.Thread):
         self.total_blocks = int(getattr(inst, "num_blocks", 1 << 30))
         self.committed: Dict[int, int] = {}
         self.commit_sum = 0
+        # mitosis (N1, live): a contracted instance drains -- every prefilled request moves
+        # with its paged KV (export_kv / import_kv over NVLink) to drain_dst(), pending ones
+        # are re-queued there -- and then idles until the macro grows again
+        self.draining = False
+        self.drain_dst = None
+        self.n_migrated_out = 0
+        self.migrate_ns = 0
 
     def _fits(self, r: LiveReq, extra: int = 0) -> bool:
         if self.admission == "preempt":  # the prompt (plus regenerated tokens) must fit now
@@ -149,18 +156,65 @@ class Worker(threading.Thread):
 
     def push_status(self, fin: Sequence[LiveReq] = ()):
         live = list(self.pending) + self.waiting + self.running
+        if self.role == "both":  # requests migrated here whose KV is not imported yet
+            live += [r for r, _ in self.imports]
         recs = [(r.req_id, r.arrival_ns, r.S, r.t_first_ns, r.n_gen, False) for r in live]
         recs += [(r.req_id, r.arrival_ns, r.S, r.t_first_ns, r.n_gen, True) for r in fin]
         self.status_q.put((self.idx, self.phase, self.t_switch, recs))
 
+    def _take(self, item) -> None:
+        if isinstance(item, tuple) and item[0] == "import":  # a migrated request and its staged KV
+            self.imports.append((item[1], item[2]))
+        elif isinstance(item, tuple) and item[0] == "drain":
+            self.draining = True
+        else:
+            self.pending.append(item)
+
     def _drain_inbox(self, block: bool):
         try:
-            r = self.inbox.get(timeout=0.002) if block else self.inbox.get_nowait()
-            self.pending.append(r)
+            self._take(self.inbox.get(timeout=0.002) if block else self.inbox.get_nowait())
             while True:
-                self.pending.append(self.inbox.get_nowait())
+                self._take(self.inbox.get_nowait())
         except queue.Empty:
             pass
+
+    def _drain_out(self) -> None:
+        """Mitosis contraction: hand every request of this instance to the
+        remaining ones -- prefilled requests with their KV blocks (NVLink peer copy into a
+        staging buffer on the destination GPU, imported by the destination's own worker),
+        queued ones as plain arrivals -- and leave the instance empty."""
+        t0 = time.perf_counter_ns()
+        for r in self.waiting + self.running:
+            dst = self.drain_dst()
+            handle = self.inst.export_kv(r.req_id, dst.inst.device)
+            self.commit_sum -= self.committed.pop(r.req_id, 0)
+            r.inst = dst.idx
+            dst.inbox.put(("import", r, handle))
+            self.n_migrated_out += 1
+        for r, handle in list(self.imports):  # in transit through this instance: forward
+            dst = self.drain_dst()
+            r.inst = dst.idx
+            dst.inbox.put(("import", r, handle))
+        while self.pending:
+            r = self.pending.popleft()
+            self.commit_sum -= self.committed.pop(r.req_id, 0)
+            dst = self.drain_dst()
+            r.inst = dst.idx
+            dst.inbox.put(r)
+        self.waiting, self.running = [], []
+        self.imports.clear()
+        self.migrate_ns += time.perf_counter_ns() - t0
+        self.draining = False
+        self.phase, self.t_switch = IDLE, self.clock.now()
+        self.push_status()
+
+    def _admit_imports(self) -> None:
+        """Migrated requests join this instance's decode set once their blocks fit."""
+        while self.imports and self._fits(self.imports[0][0]):
+            r, handle = self.imports.popleft()
+            self.inst.import_kv(handle)
+            self._commit(r)
+            (self.running if self.phase == DECODE else self.waiting).append(r)
 
     def run(self):
         try:
@@ -232,6 +286,11 @@ class Worker(threading.Thread):
     def _loop(self):
         while not self.stop_flag.is_set():
             self._drain_inbox(block=False)
+            if self.draining:
+                self._drain_out()
+                continue
+            if self.imports:
+                self._admit_imports()
             if self.role == "prefill" and self.decode_full():
                 # back-pressure: the decode instances have FUDG_BACKLOG staged requests each
                 # (their KV waits in staging buffers on the decode GPUs); prefill again later
@@ -391,9 +450,19 @@ class PaDGServer:
     def __init__(self, instances: Sequence, slo_ttft_ns: int, slo_tpot_ns: int, reserve_tokens: int,
                  predictor_table=None, token_budget: int = 16384, decode_steps_per_poll: int = 1,
                  probe_printed: bool = False, policy: str = "padg", chunk_budget: int = 1024,
-                 fudg_prefill: int = 0, admission: str = "reserve"):
+                 fudg_prefill: int = 0, admission: str = "reserve", resize=None):
+        """resize (mitosis, N1 live; padg only): [(t_s, n_active), ...] -- from t_s seconds
+        into the run the macro holds instances [0, n_active): expansion activates the next
+        instances (the router starts probing them), contraction drains the highest ones into
+        the remaining (running requests move with their KV over NVLink). Before the first
+        event all instances are active unless the first event is at t_s = 0."""
         if policy not in ("padg", "nodg", "sarathi", "fudg"):
             raise ValueError(f"unknown policy {policy!r}")
+        if resize and policy != "padg":
+            raise ValueError("live mitosis (resize) is implemented for the padg policy")
+        self.resize = sorted(resize or [])
+        self.n_active = len(instances)
+        self.resize_log: List[tuple] = []
         self.policy = policy
         self._rr = 0
         self.clock = Clock()
@@ -441,11 +510,32 @@ class PaDGServer:
                 idx, phase, t_switch, recs = self.status_q.get_nowait()
             except queue.Empty:
                 break
-            self.macro.update_status(idx, phase, t_switch, self.workers[idx].inst.num_blocks, recs)
+            self.macro.update_status(idx, phase, t_switch, self.workers[idx].inst.num_blocks, recs,
+                                     alive=idx < self.n_active)
             n += 1
         if n:
             for rid, i in self.macro.drain_deferred(self.clock.now()):
                 self._send(self.reqs[rid], i)
+
+    def _apply_resize(self, n_new: int) -> None:
+        """Mitosis step: grow or shrink the active prefix of the macro to n_new instances."""
+        n_new = max(1, min(n_new, len(self.workers)))
+        n_old, self.n_active = self.n_active, n_new
+        self.resize_log.append((self.clock.now(), n_old, n_new))
+        for idx in range(min(n_old, n_new), max(n_old, n_new)):
+            w = self.workers[idx]
+            if n_new < n_old:  # contraction: drain into the remaining instances, round-robin
+                rr = [0]
+                keep = self.workers[:n_new]
+
+                def dst(keep=keep, rr=rr):
+                    d = keep[rr[0] % len(keep)]
+                    rr[0] += 1
+                    return d
+                w.drain_dst = dst
+                w.inbox.put(("drain",))
+            # the router's view: alive only inside the active prefix (expansion: empty status)
+            self.macro.update_status(idx, w.phase, w.t_switch, w.inst.num_blocks, [], alive=idx < n_new)
 
     def _send(self, r: LiveReq, i: int):
         r.inst = i
@@ -462,10 +552,15 @@ class PaDGServer:
             lr = LiveReq(r.req_id, t_start + r.arrival_ns, np.asarray(r.prompt, np.int32), r.output_len)
             self.reqs[r.req_id] = lr
         pending = deque(self.reqs[r.req_id] for r in reqs)
+        events = deque(self.resize)
+        if events and events[0][0] <= 0:
+            self._apply_resize(events.popleft()[1])
         deadline = time.perf_counter() + timeout_s
         while time.perf_counter() < deadline:
             self._apply_statuses()
             now = self.clock.now()
+            while events and now - t_start >= events[0][0] * 1e9:
+                self._apply_resize(events.popleft()[1])
             while pending and pending[0].arrival_ns <= now:
                 lr = pending.popleft()
                 if self.policy != "padg":  # immediate round-robin dispatch (NoDG / FuDG prefill instances)

@@ -147,3 +147,37 @@ def test_live_macro_of_tp2_pairs_matches_oracle():
     assert checked >= 0.6 * 6 * 16
     for i in insts:
         i.close()
+
+
+def test_mitosis_live_same_tokens_as_static_macro():
+    """Mitosis live (N1): a macro of 4 tiny-decoder instances (spread over the visible
+    GPUs) starts with 2, expands to 4 and contracts to 1 while serving; the contracted
+    instances' running requests move with their paged KV (NVLink peer copy when the
+    instances sit on different GPUs). Every request completes, and the tokens equal those
+    of the same trace served by a static macro (the KV move is bit-exact and a token's
+    arithmetic does not depend on its batch)."""
+    from paper_2504_18154_b200.instance import Instance, device_weights_from_host
+    from paper_2504_18154_b200.serve import PaDGServer
+    shape = get_shape("tiny-gqa")
+    w = make_weights(shape, seed=0)
+    n_dev = max(1, torch.cuda.device_count())
+    dws = [device_weights_from_host(w, f"cuda:{d}") for d in range(min(n_dev, 4))]
+    insts = [Instance(shape, dws[i % len(dws)], 256, i % len(dws), token_budget=2048, max_batch=64,
+                      max_positions=2048) for i in range(4)]
+    trace = make_trace("tiny", 40, seed=21, rate_per_s=400.0, vocab=shape.vocab)
+    got, moved = {}, 0
+    for resize in (None, [(0, 2), (0.03, 4), (0.08, 1)]):
+        srv = PaDGServer(insts, slo_ttft_ns=10 ** 10, slo_tpot_ns=10 ** 9, reserve_tokens=16, token_budget=2048,
+                         resize=resize)
+        out = srv.run(trace, timeout_s=120)
+        assert all(r.t_done_ns >= 0 and len(r.tokens) == r.G for r in out.values())
+        got[resize is None] = {rid: list(r.tokens) for rid, r in out.items()}
+        if resize:
+            moved = sum(wk.n_migrated_out for wk in srv.workers)
+        for i in insts:
+            _, rs = i.status()
+            assert not rs, "every request released"
+    assert got[True] == got[False]
+    assert moved > 0, "the contraction moved running requests with their KV"
+    for i in insts:
+        i.close()

@@ -279,3 +279,37 @@ def test_preempt_admission_recomputes_under_kv_pressure(S):
         assert r.arrival_ns <= r.t_first_ns <= r.t_decode_begin_ns <= r.t_done_ns
     with pytest.raises(ValueError):
         S.PaDGServer([inst], 1, 1, 0, policy="sarathi", admission="preempt")
+
+
+def test_mitosis_resize_migrates_and_completes(S):
+    """Mitosis live (8(f) N1): the macro starts with 2 of 4 instances, expands
+    to 4, then contracts to 1 -- the contracted instances hand their prefilled requests
+    over with the KV (export / import) and their queued ones as arrivals. Every request
+    completes with its G tokens, in the same sequence as without migration; the router
+    only uses the active prefix between resize events."""
+    from paper_2504_18154_b200.serve import PaDGServer
+    insts = [FakeKVInstance(scale=1.0) for _ in range(4)]
+    trace = make_trace("alpaca", 90, seed=12, rate_per_s=200.0, vocab=1000)
+    for r in trace:
+        r.output_len = min(r.output_len, 24)
+    srv = PaDGServer(insts, slo_ttft_ns=8_000_000, slo_tpot_ns=SEC // 50, reserve_tokens=32,
+                     predictor_table=((16, 4096), (2_000_000, 60_000_000)), token_budget=4096,
+                     resize=[(0, 2), (0.12, 4), (0.3, 1)])
+    out = srv.run(trace, timeout_s=60)
+    assert all(r.t_done_ns >= 0 and len(r.tokens) == r.G for r in out.values()), "request lost"
+    for r in out.values():  # the fake's token k of request rid is (rid + k) % 997 wherever it ran
+        assert r.tokens[0] == r.req_id % 997
+        assert r.tokens[1:] == [(r.req_id + k) % 997 for k in range(1, r.G)]
+    (t_grow, _, n1), (t_shrink, _, n2) = srv.resize_log[1], srv.resize_log[2]
+    assert (n1, n2) == (4, 1)
+    for t, rid, i in srv.route_log:
+        if i >= 0 and t < t_grow:
+            assert i < 2
+        if i >= 0 and t >= t_shrink:
+            assert i == 0
+    assert sum(w.n_migrated_out for w in srv.workers[1:]) > 0, "contraction moved running requests"
+    exports = sum(1 for d in insts[1:] for c in d.calls if c[0] == "export")
+    imports = sum(1 for c in insts[0].calls if c[0] == "import")
+    assert exports == imports == sum(w.n_migrated_out for w in srv.workers)
+    for d in insts:
+        assert not d.gen, "every request released"
