@@ -214,7 +214,12 @@ class Worker(threading.Thread):
             r, handle = self.imports.popleft()
             self.inst.import_kv(handle)
             self._commit(r)
-            (self.running if self.phase == DECODE else self.waiting).append(r)
+            if self.phase == DECODE:  # joins the running decode set now
+                if r.t_decode_begin_ns < 0:
+                    r.t_decode_begin_ns = self.clock.now()
+                self.running.append(r)
+            else:  # joins at this instance's next switch to decode
+                self.waiting.append(r)
 
     def run(self):
         try:

@@ -311,5 +311,7 @@ def test_mitosis_resize_migrates_and_completes(S):
     exports = sum(1 for d in insts[1:] for c in d.calls if c[0] == "export")
     imports = sum(1 for c in insts[0].calls if c[0] == "import")
     assert exports == imports == sum(w.n_migrated_out for w in srv.workers)
+    for r in out.values():  # timestamps stay ordered across a move (TPOT counts from the decode start)
+        assert r.arrival_ns <= r.t_first_ns <= r.t_decode_begin_ns <= r.t_done_ns
     for d in insts:
         assert not d.gen, "every request released"
