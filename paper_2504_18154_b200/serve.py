@@ -167,6 +167,11 @@ class Worker(threading.Thread):
             self.imports.append((item[1], item[2]))
         elif isinstance(item, tuple) and item[0] == "drain":
             self.draining = True
+        elif isinstance(item, tuple) and item[0] == "requeue":  # from a drained instance: arrival order
+            r, i = item[1], len(self.pending)
+            while i > 0 and self.pending[i - 1].arrival_ns > r.arrival_ns:
+                i -= 1
+            self.pending.insert(i, r)
         else:
             self.pending.append(item)
 
@@ -200,7 +205,7 @@ class Worker(threading.Thread):
             self.commit_sum -= self.committed.pop(r.req_id, 0)
             dst = self.drain_dst()
             r.inst = dst.idx
-            dst.inbox.put(r)
+            dst.inbox.put(("requeue", r))
         self.waiting, self.running = [], []
         self.imports.clear()
         self.migrate_ns += time.perf_counter_ns() - t0
@@ -529,14 +534,12 @@ class PaDGServer:
         self.resize_log.append((self.clock.now(), n_old, n_new))
         for idx in range(min(n_old, n_new), max(n_old, n_new)):
             w = self.workers[idx]
-            if n_new < n_old:  # contraction: drain into the remaining instances, round-robin
-                rr = [0]
+            if n_new < n_old:  # contraction: drain into the least-loaded remaining instance
                 keep = self.workers[:n_new]
 
-                def dst(keep=keep, rr=rr):
-                    d = keep[rr[0] % len(keep)]
-                    rr[0] += 1
-                    return d
+                def dst(keep=keep):
+                    return min(keep, key=lambda k: (len(k.pending) + len(k.waiting) + len(k.running) +
+                                                    len(k.imports) + k.inbox.qsize(), k.idx))
                 w.drain_dst = dst
                 w.inbox.put(("drain",))
             # the router's view: alive only inside the active prefix (expansion: empty status)

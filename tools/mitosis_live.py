@@ -46,6 +46,7 @@ def main():
     ap.add_argument("--slo-tpot", type=float, default=0.1)
     ap.add_argument("--max-out", type=int, default=512)
     ap.add_argument("--blocks", type=int, default=5000)
+    ap.add_argument("--contract-delay-s", type=float, default=20.0)
     args = ap.parse_args()
     import torch
     from paper_2504_18154_b200 import build as B
@@ -70,9 +71,11 @@ def main():
         r.output_len = min(r.output_len, args.max_out)
     slo_t, slo_p = int(args.slo_ttft * 1e9), int(args.slo_tpot * 1e9)
     small = max(1, n // 2)
-    # grow to n at the rate step, contract back to n/2 at the step down
+    # grow to n when the rate steps up; contract back to n/2 once the load has been low for a
+    # while after the step down ("sustained resource underutilization")
+    t_c = 2 * args.step_s + args.contract_delay_s
     runs = [("static-small", [(0, small)]), ("static-full", None),
-            ("mitosis", [(0, small), (args.step_s, n), (2 * args.step_s, small)])]
+            ("mitosis", [(0, small), (args.step_s, n), (t_c, small)])]
     for name, resize in runs:
         srv = PaDGServer(insts, slo_t, slo_p, reserve_tokens=64, predictor_table=(lens, ns), resize=resize)
         out = srv.run(trace, timeout_s=len(rates) * args.step_s + 600)
