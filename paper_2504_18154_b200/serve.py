@@ -470,6 +470,8 @@ class PaDGServer:
             raise ValueError(f"unknown policy {policy!r}")
         if resize and policy != "padg":
             raise ValueError("live mitosis (resize) is implemented for the padg policy")
+        if resize and not all(hasattr(i, "export_kv") and hasattr(i, "import_kv") for i in instances):
+            raise ValueError("live mitosis moves KV: every instance needs export_kv / import_kv (TP=1)")
         self.resize = sorted(resize or [])
         self.n_active = len(instances)
         self.resize_log: List[tuple] = []
