@@ -165,6 +165,8 @@ def test_mitosis_live_same_tokens_as_static_macro():
     insts = [Instance(shape, dws[i % len(dws)], 256, i % len(dws), token_budget=2048, max_batch=64,
                       max_positions=2048) for i in range(4)]
     trace = make_trace("tiny", 40, seed=21, rate_per_s=400.0, vocab=shape.vocab)
+    for r in trace:  # longer decodes: requests are still running when the macro contracts
+        r.output_len = 64
     got, moved = {}, 0
     for resize in (None, [(0, 2), (0.03, 4), (0.08, 1)]):
         srv = PaDGServer(insts, slo_ttft_ns=10 ** 10, slo_tpot_ns=10 ** 9, reserve_tokens=16, token_budget=2048,
