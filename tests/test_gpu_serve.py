@@ -157,20 +157,23 @@ def test_mitosis_live_same_tokens_as_static_macro():
     of the same trace served by a static macro (the KV move is bit-exact and a token's
     arithmetic does not depend on its batch)."""
     from paper_2504_18154_b200.instance import Instance, device_weights_from_host
-    from paper_2504_18154_b200.serve import PaDGServer
+    from paper_2504_18154_b200.serve import PaDGServer, profile_prefill
     shape = get_shape("tiny-gqa")
     w = make_weights(shape, seed=0)
     n_dev = max(1, torch.cuda.device_count())
     dws = [device_weights_from_host(w, f"cuda:{d}") for d in range(min(n_dev, 4))]
     insts = [Instance(shape, dws[i % len(dws)], 256, i % len(dws), token_budget=2048, max_batch=64,
                       max_positions=2048) for i in range(4)]
-    trace = make_trace("tiny", 40, seed=21, rate_per_s=400.0, vocab=shape.vocab)
+    lens, ns = profile_prefill(insts[0], lens=(32, 128, 512), vocab=shape.vocab)
+    trace = make_trace("tiny", 60, seed=21, rate_per_s=400.0, vocab=shape.vocab)
     for r in trace:  # longer decodes: requests are still running when the macro contracts
         r.output_len = 64
     got, moved = {}, 0
-    for resize in (None, [(0, 2), (0.03, 4), (0.08, 1)]):
-        srv = PaDGServer(insts, slo_ttft_ns=10 ** 10, slo_tpot_ns=10 ** 9, reserve_tokens=16, token_budget=2048,
-                         resize=resize)
+    # a TTFT SLO near one prefill makes Alg. 1 spread the arrivals over the active
+    # instances (with a loose one the sticky cyclic routing keeps them all on instance 0)
+    for resize in (None, [(0, 2), (0.02, 4), (0.07, 1)]):
+        srv = PaDGServer(insts, slo_ttft_ns=3 * max(ns), slo_tpot_ns=20_000_000, reserve_tokens=16,
+                         predictor_table=(lens, ns), token_budget=2048, resize=resize)
         out = srv.run(trace, timeout_s=120)
         assert all(r.t_done_ns >= 0 and len(r.tokens) == r.G for r in out.values())
         got[resize is None] = {rid: list(r.tokens) for rid, r in out.items()}
