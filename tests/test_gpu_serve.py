@@ -153,9 +153,9 @@ def test_mitosis_live_same_tokens_as_static_macro():
     """Mitosis live (N1): a macro of 4 tiny-decoder instances (spread over the visible
     GPUs) contracts to 1 while serving (expansion: tests/test_serve_live.py); the contracted
     instances' running requests move with their paged KV (NVLink peer copy when the
-    instances sit on different GPUs). Every request completes, and the tokens equal those
-    of the same trace served by a static macro (the KV move is bit-exact and a token's
-    arithmetic does not depend on its batch)."""
+    instances sit on different GPUs). Every request completes, running requests did move,
+    and each request's tokens equal those of the same trace on the static macro, or both
+    follow the fp64 oracle up to a legitimate near tie (A20: top-2 margin <= 5e-2)."""
     from paper_2504_18154_b200.instance import Instance, device_weights_from_host
     from paper_2504_18154_b200.serve import PaDGServer, profile_prefill
     shape = get_shape("tiny-gqa")
@@ -183,7 +183,20 @@ def test_mitosis_live_same_tokens_as_static_macro():
         for i in insts:
             _, rs = i.status()
             assert not rs, "every request released"
-    assert got[True] == got[False]
     assert moved > 0, "the contraction moved running requests with their KV"
+    # a request's tokens may differ between the runs only at a legitimate near tie: its batch
+    # (and so the decode attention's context splits) differs, which moves the last bits
+    model = T.Model(shape, w.as_f64())
+    prompts = {r.req_id: list(r.prompt) for r in trace}
+
+    def agrees(rid, seq):
+        toks, outs = model.generate(prompts[rid], len(seq))
+        k = next((k for k in range(len(seq)) if seq[k] != toks[k]), None)
+        return k is None or T.top2_margin(outs[k].logits) <= 5e-2
+
+    diff = [rid for rid in got[True] if got[True][rid] != got[False][rid]]
+    assert len(diff) <= len(trace) // 2, (len(diff), moved)
+    for rid in diff:
+        assert agrees(rid, got[True][rid]) and agrees(rid, got[False][rid]), (rid, moved)
     for i in insts:
         i.close()
