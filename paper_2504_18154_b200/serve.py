@@ -465,9 +465,17 @@ class PaDGServer:
         into the run the macro holds instances [0, n_active): expansion activates the next
         instances (the router starts probing them), contraction drains the highest ones into
         the remaining (running requests move with their KV over NVLink). Before the first
-        event all instances are active unless the first event is at t_s = 0."""
+        event all instances are active unless the first event is at t_s = 0. A dict
+        ({n_min, n_max, n_start, up_s, down_s, down_live, cooldown_s}) selects the automatic
+        triggers of _auto_resize instead."""
         if policy not in ("padg", "nodg", "sarathi", "fudg"):
             raise ValueError(f"unknown policy {policy!r}")
+        if isinstance(resize, dict):  # automatic triggers (P:592), see _auto_resize
+            self.auto = dict(n_min=1, n_max=len(instances), up_s=0.5, down_s=10.0, down_live=2, cooldown_s=5.0)
+            self.auto.update(resize)
+            resize = [(0, self.auto.pop("n_start", self.auto["n_min"]))]
+        else:
+            self.auto = None
         if resize and policy != "padg":
             raise ValueError("live mitosis (resize) is implemented for the padg policy")
         if resize and not all(hasattr(i, "export_kv") and hasattr(i, "import_kv") for i in instances):
@@ -475,6 +483,7 @@ class PaDGServer:
         self.resize = sorted(resize or [])
         self.n_active = len(instances)
         self.resize_log: List[tuple] = []
+        self.n_deferred = 0
         self.policy = policy
         self._rr = 0
         self.clock = Clock()
@@ -527,6 +536,7 @@ class PaDGServer:
             n += 1
         if n:
             for rid, i in self.macro.drain_deferred(self.clock.now()):
+                self.n_deferred -= 1
                 self._send(self.reqs[rid], i)
 
     def _apply_resize(self, n_new: int) -> None:
@@ -547,6 +557,32 @@ class PaDGServer:
             # the router's view: alive only inside the active prefix (expansion: empty status)
             self.macro.update_status(idx, w.phase, w.t_switch, w.inst.num_blocks, [], alive=idx < n_new)
 
+    def _auto_resize(self, now: int) -> None:
+        """Mitosis triggers (scale "when the system fails to meet the defined SLOs or
+        when there is sustained resource underutilization"): expand by one instance once
+        requests have stayed Deferred -- no active instance passes Alg. 2 -- for up_s seconds;
+        contract by one once nothing was deferred for down_s seconds and the last active
+        instance holds <= down_live live requests (they move with their KV). One step per
+        cooldown_s."""
+        a = self.auto
+        if now - self._auto_last < a["cooldown_s"] * 1e9:
+            return
+        if self.n_deferred > 0:
+            self._auto_quiet = now
+            if self._auto_busy < 0:
+                self._auto_busy = now
+            if now - self._auto_busy >= a["up_s"] * 1e9 and self.n_active < a["n_max"]:
+                self._apply_resize(self.n_active + 1)
+                self._auto_last, self._auto_busy = now, -1
+            return
+        self._auto_busy = -1
+        w = self.workers[self.n_active - 1]
+        live = len(w.pending) + len(w.waiting) + len(w.running) + len(w.imports)
+        if (now - self._auto_quiet >= a["down_s"] * 1e9 and self.n_active > a["n_min"] and
+                live <= a["down_live"]):
+            self._apply_resize(self.n_active - 1)
+            self._auto_last, self._auto_quiet = now, now
+
     def _send(self, r: LiveReq, i: int):
         r.inst = i
         self.route_log.append((self.clock.now(), r.req_id, i))
@@ -565,12 +601,16 @@ class PaDGServer:
         events = deque(self.resize)
         if events and events[0][0] <= 0:
             self._apply_resize(events.popleft()[1])
+        self._auto_last = self._auto_quiet = t_start
+        self._auto_busy = -1
         deadline = time.perf_counter() + timeout_s
         while time.perf_counter() < deadline:
             self._apply_statuses()
             now = self.clock.now()
             while events and now - t_start >= events[0][0] * 1e9:
                 self._apply_resize(events.popleft()[1])
+            if self.auto is not None:
+                self._auto_resize(now)
             while pending and pending[0].arrival_ns <= now:
                 lr = pending.popleft()
                 if self.policy != "padg":  # immediate round-robin dispatch (NoDG / FuDG prefill instances)
@@ -581,6 +621,7 @@ class PaDGServer:
                 if i < 0:
                     self.route_log.append((now, lr.req_id, -1))
                     self.macro.defer(lr.req_id, lr.arrival_ns, lr.S)
+                    self.n_deferred += 1
                 else:
                     self._send(lr, i)
             for w in self.workers:

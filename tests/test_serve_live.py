@@ -315,3 +315,33 @@ def test_mitosis_resize_migrates_and_completes(S):
         assert r.arrival_ns <= r.t_first_ns <= r.t_decode_begin_ns <= r.t_done_ns
     for d in insts:
         assert not d.gen, "every request released"
+
+
+def test_mitosis_auto_triggers(S):
+    """Mitosis triggers: a burst that no single instance can admit under the TTFT
+    SLO keeps requests Deferred -> the macro expands; a later quiet period -> it contracts.
+    Every request completes with its token sequence."""
+    from paper_2504_18154_b200.serve import PaDGServer
+    insts = [FakeKVInstance(scale=1.0) for _ in range(4)]
+    burst = make_trace("alpaca", 120, seed=31, rate_per_s=1500.0, vocab=1000)
+    late = make_trace("alpaca", 6, seed=32, rate_per_s=20.0, vocab=1000)
+    for k, r in enumerate(late):
+        r.req_id = 1000 + k
+        r.arrival_ns += int(0.5 * SEC)
+    trace = burst + late
+    for r in trace:
+        r.output_len = min(r.output_len, 24)
+    srv = PaDGServer(insts, slo_ttft_ns=8_000_000, slo_tpot_ns=SEC // 50, reserve_tokens=32,
+                     predictor_table=((16, 4096), (2_000_000, 60_000_000)), token_budget=4096,
+                     resize=dict(n_min=1, n_max=4, n_start=1, up_s=0.01, down_s=0.15, down_live=4,
+                                 cooldown_s=0.02))
+    out = srv.run(trace, timeout_s=60)
+    assert all(r.t_done_ns >= 0 and len(r.tokens) == r.G for r in out.values())
+    for r in out.values():
+        assert r.tokens[1:] == [(r.req_id + k) % 997 for k in range(1, r.G)]
+    sizes = [b for _, _, b in srv.resize_log]
+    assert max(sizes) > 1, f"the burst expanded the macro: {srv.resize_log}"
+    peak = sizes.index(max(sizes))
+    assert min(sizes[peak:]) < max(sizes), f"the quiet period contracted it: {srv.resize_log}"
+    for d in insts:
+        assert not d.gen

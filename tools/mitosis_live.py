@@ -47,6 +47,7 @@ def main():
     ap.add_argument("--max-out", type=int, default=512)
     ap.add_argument("--blocks", type=int, default=5000)
     ap.add_argument("--contract-delay-s", type=float, default=20.0)
+    ap.add_argument("--only", default="", help="comma list of runs (static-small, static-full, mitosis, mitosis-auto)")
     args = ap.parse_args()
     import torch
     from paper_2504_18154_b200 import build as B
@@ -75,7 +76,13 @@ def main():
     # while after the step down ("sustained resource underutilization")
     t_c = 2 * args.step_s + args.contract_delay_s
     runs = [("static-small", [(0, small)]), ("static-full", None),
-            ("mitosis", [(0, small), (args.step_s, n), (t_c, small)])]
+            ("mitosis", [(0, small), (args.step_s, n), (t_c, small)]),
+            # the paper's triggers: expand while requests stay Deferred, contract after
+            # a quiet period (serve.PaDGServer._auto_resize)
+            ("mitosis-auto", dict(n_min=small, n_max=n, n_start=small, up_s=1.0, down_s=15.0, down_live=4,
+                                  cooldown_s=5.0))]
+    if args.only:
+        runs = [x for x in runs if x[0] in args.only.split(",")]
     for name, resize in runs:
         srv = PaDGServer(insts, slo_t, slo_p, reserve_tokens=64, predictor_table=(lens, ns), resize=resize)
         out = srv.run(trace, timeout_s=len(rates) * args.step_s + 600)
