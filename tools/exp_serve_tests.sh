@@ -1,6 +1,4 @@
-# live mitosis GPU test x3 on 2 GPUs and once on one GPU
+# serving GPU tests (live macro, FuDG, preemption, TP=2 pair macro, live mitosis) + TP tests on 2 GPUs
 mkdir -p gpurun_out
-: > gpurun_out/serve_tests.txt
-for i in 1 2 3; do timeout 300 python -m pytest -q tests/test_gpu_serve.py -k mitosis 2>&1 | tail -12 >> gpurun_out/serve_tests.txt; done
-CUDA_VISIBLE_DEVICES=0 timeout 300 python -m pytest -q tests/test_gpu_serve.py -k mitosis 2>&1 | tail -12 >> gpurun_out/serve_tests.txt
+timeout 1500 python -m pytest -q tests/test_gpu_serve.py tests/test_gpu_tp.py tests/test_gpu_migrate.py 2>&1 | tail -6 > gpurun_out/serve_tests.txt
 cat gpurun_out/serve_tests.txt
